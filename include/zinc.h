@@ -1,0 +1,181 @@
+/*
+ * zinc.h -- C ABI of libzinc.so, the B200 (sm_100a) hot path of arXiv 2408.07304
+ * ("Zinc"): batched CKKS/RLWE public-key encryption over RNS polynomials, in the
+ * vanilla form (Eq. 8) and the Zinc form (PAPER.md:214-223,
+ * Algorithm 1), plus the supporting keygen (Eq. 7), cache precompute
+ * (PAPER.md:164-166), encode and decrypt/decode (Eq. 10) calls.
+ *
+ * The calls follow the paper's problem statement Pi~ = (Gen, Enc_z, Dec)
+ * extending Pi = (Gen, Enc, Dec, +, x).  Numeric contract
+ * (primes, psi, NTT order, Philox layout, encoding): docs/CONVENTIONS.md
+ * (C-1..C-10).
+ *
+ * Conventions for every call below
+ *  - Buffers are DEVICE pointers owned by the caller (e.g. torch tensors) on the
+ *    context's device unless a parameter says "host".  They must be 16-byte
+ *    aligned.  The library never keeps a pointer after a call returns.
+ *  - Layouts are C order:  RNS polynomial uint64[L][N]; ciphertext, public key
+ *    and cache uint64[2][L][N] with component 0 = the paper's c1 (carries m,
+ *    PAPER.md:185) and 1 = c2; a batch is uint64[B][2][L][N].  Every stored word
+ *    is the canonical residue in [0, q_i).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Device calls are asynchronous on it and never synchronise the host; faults
+ *    surface at the caller's next synchronisation.
+ *  - Every call returns a zinc_status; on failure zinc_last_error() returns a
+ *    thread-local message.  Arguments are validated before any launch:
+ *    NULL pointers, bad enums, misaligned pointers -> ZINC_EINVAL.  batch == 0
+ *    is a no-op returning ZINC_OK.
+ *  - Randomness: a (seed, message index) pair is a nonce; the caller must never
+ *    reuse one.  Message b of a batch uses msg = msg_base + b, so a batch split
+ *    across GPUs with msg_base = global offset gives bit-identical output.
+ *  - There is no CPU fallback: every compute step runs in this library's CUDA
+ *    kernels.
+ */
+#ifndef ZINC_H
+#define ZINC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct zinc_ctx zinc_ctx; /* opaque: params + device tables, bound to one device */
+typedef void *zinc_stream_t;      /* a cudaStream_t */
+
+typedef enum {
+  ZINC_OK = 0,
+  ZINC_EINVAL = -1,       /* bad argument */
+  ZINC_EUNSUPPORTED = -2, /* valid but not implemented (e.g. a kind at this N) */
+  ZINC_ECUDA = -3,        /* a CUDA runtime call or launch failed */
+  ZINC_ENOMEM = -4,       /* device or host allocation failed */
+  ZINC_EPARAMS = -5       /* no parameter set exists (no prime found, ...) */
+} zinc_status;
+
+/* Ciphertext / cache representation (reading A4).  NTT: both
+ * components stored as NTT(c) in the order of C-3; COEFF: coefficient vectors.
+ * NTT(COEFF-form ct) == NTT-form ct bit for bit. */
+typedef enum { ZINC_FORM_NTT = 0, ZINC_FORM_COEFF = 1 } zinc_form;
+
+/* Plaintext input kinds.  COEFF_I64: int64[B][N] integer plaintext polynomial
+ * (the bit-exact contract); SLOTS_F64: double[B][N/2] real slots;
+ * SLOTS_C128: double[B][N/2][2] complex slots (re, im).  Slots are encoded per
+ * C-6 (canonical embedding, scale 2^log_scale) inside the library. */
+typedef enum { ZINC_PT_COEFF_I64 = 0, ZINC_PT_SLOTS_F64 = 1, ZINC_PT_SLOTS_C128 = 2 } zinc_pt_kind;
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Create a context on CUDA device `device`: ring degree N = 2^log_n
+ * (12 <= log_n <= 15), L = num_limbs RNS primes (1 <= L <= 32) of the listed
+ * bit sizes (20 <= bits <= 60; the lazy butterfly needs q < 2^62), chosen per
+ * C-1 (largest primes q < 2^b, q = 1 mod 2N); psi per C-2; scale
+ * Delta = 2^log_scale (1 <= log_scale <= 60).  Builds the twiddle and FFT tables
+ * on the host and uploads them (synchronous; not a hot call).  *out receives
+ * the context; free it with zinc_ctx_destroy.  Limb 0 must be the largest prime
+ * (decryption's CRT check, C-10) or ZINC_EPARAMS is returned. */
+zinc_status zinc_ctx_create(int log_n, int num_limbs, const int *limb_bits, int log_scale,
+                            int device, zinc_ctx **out);
+zinc_status zinc_ctx_destroy(zinc_ctx *ctx);
+
+/* Host copies of the moduli q_i and roots psi_i (arrays of L, host pointers). */
+zinc_status zinc_ctx_moduli(const zinc_ctx *ctx, uint64_t *q_out, uint64_t *psi_out);
+/* N, L, log_scale of the context (host pointers, each may be NULL). */
+zinc_status zinc_ctx_info(const zinc_ctx *ctx, int *log_n, int *num_limbs, int *log_scale);
+
+/* ---- Gen: Eq. 7, C-5 ----------------------------------- */
+
+/* sk <- R_2, a <- R_q, e <- chi (CBD eta=21, reading A3);
+ * pk1 = [-a.sk + e]_q, pk2 = a.  Outputs (device): sk_ntt uint64[L][N] (NTT
+ * form), sk_coeff int8[N] in {-1,0,1} (may be NULL), pk_ntt uint64[2][L][N]
+ * (NTT form). */
+zinc_status zinc_keygen(const zinc_ctx *ctx, uint64_t seed, uint64_t *sk_ntt, int8_t *sk_coeff,
+                        uint64_t *pk_ntt, zinc_stream_t stream);
+
+/* ---- Zinc precomputation: PAPER.md:164-166 ("caches a single Enc(0)"), C-8 - */
+
+/* cache = vanilla Enc(0) under pk_ntt with message index 2^64-1 and seed
+ * `seed`, stored in `form`.  cache: uint64[2][L][N]. */
+zinc_status zinc_precompute_cache(const zinc_ctx *ctx, const uint64_t *pk_ntt, uint64_t seed,
+                                  zinc_form form, uint64_t *cache, zinc_stream_t stream);
+
+/* ---- Enc_z: Algorithm 1, Eq. 4 + Eq. 9, C-9 ------------ */
+
+/* For b in [0, batch): c = zero + m_b (m added to c1 only, reading A2);
+ * e1', e2' <- chi (Philox stream (seed, msg_base + b), tags 7/8);
+ * ct_b = ([c1 + e1']_q, [c2 + e2']_q), in the cache's form (the caller passes the
+ * form the cache was built in).  In NTT form the added polynomials are
+ * transformed (NTT(m + e1'), NTT(e2')).  pt: see zinc_pt_kind.
+ * ct: uint64[batch][2][L][N]. */
+zinc_status zinc_encrypt_batch(const zinc_ctx *ctx, const uint64_t *cache, zinc_form form,
+                               zinc_pt_kind kind, const void *pt, size_t batch, uint64_t seed,
+                               uint64_t msg_base, uint64_t *ct, zinc_stream_t stream);
+
+/* ---- Enc: Eq. 8 with c2 = [pk2.u + e2]_q (reading A1), C-7 */
+
+/* For b in [0, batch): u <- R_2, e1, e2 <- chi (tags 4/5/6);
+ * c1 = [pk1.u + e1 + m_b]_q, c2 = [pk2.u + e2]_q, stored in `form`.
+ * pk_ntt: uint64[2][L][N] NTT form.  ct: uint64[batch][2][L][N]. */
+zinc_status ckks_encrypt_batch(const zinc_ctx *ctx, const uint64_t *pk_ntt, zinc_form form,
+                               zinc_pt_kind kind, const void *pt, size_t batch, uint64_t seed,
+                               uint64_t msg_base, uint64_t *ct, zinc_stream_t stream);
+
+/* ---- Dec: Eq. 10, C-10 --------------------------------- */
+
+/* x = [c1 + c2.sk]_q per limb; coeff_out[b] (int64[N], may be NULL) = x
+ * centred mod q_0; status_out[b] (int32, may be NULL) = 0 if x_0 mod q_i ==
+ * x^(i) on every limb (CRT consistency), else 1; slots_out[b] (double[N/2][2],
+ * may be NULL) = decode(x) = (1/Delta) sum_j x_j zeta^(g_k j).  ct in `form`. */
+zinc_status ckks_decrypt_batch(const zinc_ctx *ctx, const uint64_t *sk_ntt, zinc_form form,
+                               const uint64_t *ct, size_t batch, double *slots_out,
+                               int64_t *coeff_out, int32_t *status_out, zinc_stream_t stream);
+
+/* ---- support / test exports ---------------------------------------------- */
+
+/* Encode slots (kind SLOTS_F64 or SLOTS_C128) to int64[batch][N] per C-6. */
+zinc_status ckks_encode_batch(const zinc_ctx *ctx, zinc_pt_kind kind, const void *slots,
+                              size_t batch, int64_t *m_out, zinc_stream_t stream);
+
+/* In-place forward (C-3) / inverse NTT of `count` RNS polynomials uint64[count][L][N]
+ * (inputs must be canonical residues). */
+zinc_status zinc_ntt_forward(const zinc_ctx *ctx, uint64_t *data, size_t count, zinc_stream_t stream);
+zinc_status zinc_ntt_inverse(const zinc_ctx *ctx, uint64_t *data, size_t count, zinc_stream_t stream);
+
+/* Draw n coefficients of the Philox stream (seed, msg, tag, limb) per C-4.
+ * tag 1..8.  Ternary tags (1, 4) and CBD tags (2, 5, 6, 7, 8) write int64 values
+ * (limb ignored); the uniform tag 3 writes uint64 residues mod q_limb. */
+zinc_status zinc_debug_sample(const zinc_ctx *ctx, int tag, uint64_t seed, uint64_t msg,
+                              int limb, size_t n, void *out, zinc_stream_t stream);
+
+/* Integer-peak microkernel: `iters` rounds of 8 independent
+ * register-resident lazy Shoup butterflies per thread with limb 0's modulus,
+ * grid = blocks x 256 threads; writes a checksum to sink[0] (device uint64).
+ * *butterflies (host) receives the number of butterflies launched. */
+zinc_status zinc_int_peak(const zinc_ctx *ctx, int blocks, int iters, uint64_t *sink,
+                          double *butterflies, zinc_stream_t stream);
+
+/* Host-buffer encryption (end-to-end API): the same result as
+ * zinc_encrypt_batch / ckks_encrypt_batch (path 0 = Zinc with `key` = cache,
+ * path 1 = vanilla with `key` = pk_ntt, both device pointers) but pt and ct are
+ * HOST pointers.  The batch is pipelined in chunks of `chunk` messages over two
+ * internal streams: H2D of the plaintexts, the kernels, D2H of the ciphertexts,
+ * overlapped.  Host buffers should be pinned (cudaHostAlloc / torch
+ * pin_memory) for full bandwidth.  Blocks the calling thread until the last
+ * ciphertext has reached the host. */
+zinc_status zinc_encrypt_batch_host(const zinc_ctx *ctx, int path, const uint64_t *key,
+                                    zinc_form form, zinc_pt_kind kind, const void *pt_host,
+                                    size_t batch, uint64_t seed, uint64_t msg_base,
+                                    uint64_t *ct_host, size_t chunk);
+
+/* Number of kernel launches this library issued since the last reset (all
+ * threads); used by bench.py's gpu_launches claim. */
+uint64_t zinc_launch_count(void);
+void zinc_launch_count_reset(void);
+
+/* Thread-local message for the last non-OK status of this thread. */
+const char *zinc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZINC_H */

@@ -1,0 +1,270 @@
+"""paper_2408_07304_b200 -- B200 (sm_100a) hot path of arXiv 2408.07304 ("Zinc").
+
+Thin Python binding of ``libzinc.so`` (C ABI in ``include/zinc.h``): argument
+marshalling only.  Every step of the encryption path runs in the library's CUDA
+kernels; PyTorch supplies device memory and streams.  There is no CPU fallback:
+if the shared library is missing or cannot be loaded, importing this package's
+functions raises.
+
+Function names follow the ABI (``zinc_keygen``, ``zinc_precompute_cache``,
+``zinc_encrypt_batch``, ``ckks_encrypt_batch``, ``ckks_decrypt_batch``, ...).
+Tensors: uint64 ciphertexts ``[B, 2, L, N]``, keys ``[2, L, N]``, secret key
+``[L, N]``; int64 plaintexts ``[B, N]``; float64 slots ``[B, N/2]`` (real) or
+``[B, N/2, 2]`` (complex).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "NTT", "COEFF", "PT_COEFF_I64", "PT_SLOTS_F64", "PT_SLOTS_C128", "ZincError", "Context", "lib",
+    "zinc_keygen", "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch",
+    "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
+    "zinc_debug_sample", "zinc_int_peak", "zinc_encrypt_batch_host", "launch_count",
+    "launch_count_reset", "LIB_PATH", "EXPORTED_SYMBOLS",
+]
+
+NTT, COEFF = 0, 1
+PT_COEFF_I64, PT_SLOTS_F64, PT_SLOTS_C128 = 0, 1, 2
+PATH_ZINC, PATH_VANILLA = 0, 1
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libzinc.so")
+
+# every symbol include/zinc.h declares
+EXPORTED_SYMBOLS = (
+    "zinc_ctx_create", "zinc_ctx_destroy", "zinc_ctx_moduli", "zinc_ctx_info", "zinc_keygen",
+    "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch", "ckks_decrypt_batch",
+    "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse", "zinc_debug_sample", "zinc_int_peak",
+    "zinc_encrypt_batch_host", "zinc_launch_count", "zinc_launch_count_reset", "zinc_last_error",
+)
+
+
+class ZincError(RuntimeError):
+    pass
+
+
+_c = ctypes
+_vp, _u64, _i32, _sz = _c.c_void_p, _c.c_uint64, _c.c_int, _c.c_size_t
+_SIGS = {
+    "zinc_ctx_create": [_i32, _i32, _c.POINTER(_c.c_int), _i32, _i32, _c.POINTER(_vp)],
+    "zinc_ctx_destroy": [_vp],
+    "zinc_ctx_moduli": [_vp, _c.POINTER(_u64), _c.POINTER(_u64)],
+    "zinc_ctx_info": [_vp, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)],
+    "zinc_keygen": [_vp, _u64, _vp, _vp, _vp, _vp],
+    "zinc_precompute_cache": [_vp, _vp, _u64, _i32, _vp, _vp],
+    "zinc_encrypt_batch": [_vp, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _vp],
+    "ckks_encrypt_batch": [_vp, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _vp],
+    "ckks_decrypt_batch": [_vp, _vp, _i32, _vp, _sz, _vp, _vp, _vp, _vp],
+    "ckks_encode_batch": [_vp, _i32, _vp, _sz, _vp, _vp],
+    "zinc_ntt_forward": [_vp, _vp, _sz, _vp],
+    "zinc_ntt_inverse": [_vp, _vp, _sz, _vp],
+    "zinc_debug_sample": [_vp, _i32, _u64, _u64, _i32, _sz, _vp, _vp],
+    "zinc_int_peak": [_vp, _i32, _i32, _vp, _c.POINTER(_c.c_double), _vp],
+    "zinc_encrypt_batch_host": [_vp, _i32, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _sz],
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libzinc.so (raises ZincError if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ZincError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = _c.c_int
+        L.zinc_last_error.restype = _c.c_char_p
+        L.zinc_last_error.argtypes = []
+        L.zinc_launch_count.restype = _u64
+        L.zinc_launch_count.argtypes = []
+        L.zinc_launch_count_reset.restype = None
+        L.zinc_launch_count_reset.argtypes = []
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = lib().zinc_last_error().decode(errors="replace")
+        raise ZincError(f"{what}: status {rc}: {msg}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise ZincError("tensor must be contiguous")
+        return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(int(t))
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Context:
+    """A zinc_ctx: ring degree 2^log_n, RNS primes of the given bit sizes (C-1),
+    scale 2^log_scale, bound to CUDA device `device`."""
+
+    def __init__(self, log_n: int, bits, log_scale: int, device: int = 0):
+        arr = (ctypes.c_int * len(bits))(*[int(b) for b in bits])
+        h = ctypes.c_void_p()
+        torch.cuda.init()
+        _check(lib().zinc_ctx_create(log_n, len(bits), arr, log_scale, device, ctypes.byref(h)), "zinc_ctx_create")
+        self._h = h
+        self.log_n, self.L, self.log_scale, self.device = log_n, len(bits), log_scale, device
+        self.n = 1 << log_n
+        q = (ctypes.c_uint64 * self.L)()
+        psi = (ctypes.c_uint64 * self.L)()
+        _check(lib().zinc_ctx_moduli(h, q, psi), "zinc_ctx_moduli")
+        self.q = [int(x) for x in q]
+        self.psi = [int(x) for x in psi]
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.zinc_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # allocation helpers (torch owns device memory)
+    def dev(self):
+        return torch.device("cuda", self.device)
+
+    def empty_ct(self, batch: int) -> torch.Tensor:
+        return torch.empty((batch, 2, self.L, self.n), dtype=torch.uint64, device=self.dev())
+
+    def empty_key(self) -> torch.Tensor:
+        return torch.empty((2, self.L, self.n), dtype=torch.uint64, device=self.dev())
+
+
+def _kind_of(pt: torch.Tensor) -> int:
+    if pt.dtype == torch.int64:
+        return PT_COEFF_I64
+    if pt.dtype == torch.float64:
+        return PT_SLOTS_C128 if pt.dim() == 3 else PT_SLOTS_F64
+    raise ZincError(f"unsupported plaintext dtype {pt.dtype}")
+
+
+def zinc_keygen(ctx: Context, seed: int, stream=None):
+    """Gen (Eq. 7). Returns (sk_ntt [L,N] u64, sk_coeff [N] i8, pk_ntt [2,L,N] u64)."""
+    sk = torch.empty((ctx.L, ctx.n), dtype=torch.uint64, device=ctx.dev())
+    skc = torch.empty((ctx.n,), dtype=torch.int8, device=ctx.dev())
+    pk = ctx.empty_key()
+    _check(lib().zinc_keygen(ctx.handle, seed, _ptr(sk), _ptr(skc), _ptr(pk), _stream(stream)), "zinc_keygen")
+    return sk, skc, pk
+
+
+def zinc_precompute_cache(ctx: Context, pk_ntt: torch.Tensor, seed: int, form: int, out=None, stream=None):
+    """Zinc precomputation: Enc(0) in `form`. Returns [2,L,N] u64."""
+    cache = ctx.empty_key() if out is None else out
+    _check(lib().zinc_precompute_cache(ctx.handle, _ptr(pk_ntt), seed, form, _ptr(cache), _stream(stream)),
+           "zinc_precompute_cache")
+    return cache
+
+
+def zinc_encrypt_batch(ctx: Context, cache: torch.Tensor, form: int, pt: torch.Tensor, seed: int,
+                       msg_base: int = 0, out=None, stream=None):
+    """Enc_z (Algorithm 1) of a batch of plaintexts (int64 [B,N] or slots). Returns [B,2,L,N] u64."""
+    b = pt.shape[0]
+    ct = ctx.empty_ct(b) if out is None else out
+    _check(lib().zinc_encrypt_batch(ctx.handle, _ptr(cache), form, _kind_of(pt), _ptr(pt), b, seed, msg_base,
+                                    _ptr(ct), _stream(stream)), "zinc_encrypt_batch")
+    return ct
+
+
+def ckks_encrypt_batch(ctx: Context, pk_ntt: torch.Tensor, form: int, pt: torch.Tensor, seed: int,
+                       msg_base: int = 0, out=None, stream=None):
+    """Vanilla Enc (Eq. 8, reading A1) of a batch. Returns [B,2,L,N] u64."""
+    b = pt.shape[0]
+    ct = ctx.empty_ct(b) if out is None else out
+    _check(lib().ckks_encrypt_batch(ctx.handle, _ptr(pk_ntt), form, _kind_of(pt), _ptr(pt), b, seed, msg_base,
+                                    _ptr(ct), _stream(stream)), "ckks_encrypt_batch")
+    return ct
+
+
+def ckks_decrypt_batch(ctx: Context, sk_ntt: torch.Tensor, form: int, ct: torch.Tensor, slots: bool = True,
+                       stream=None):
+    """Dec (Eq. 10). Returns (coeff int64 [B,N], status int32 [B], slots complex128 [B,N/2] or None)."""
+    b = ct.shape[0]
+    coeff = torch.empty((b, ctx.n), dtype=torch.int64, device=ctx.dev())
+    status = torch.empty((b,), dtype=torch.int32, device=ctx.dev())
+    z = torch.empty((b, ctx.n // 2, 2), dtype=torch.float64, device=ctx.dev()) if slots else None
+    _check(lib().ckks_decrypt_batch(ctx.handle, _ptr(sk_ntt), form, _ptr(ct), b, _ptr(z), _ptr(coeff), _ptr(status),
+                                    _stream(stream)), "ckks_decrypt_batch")
+    zc = torch.view_as_complex(z) if slots else None
+    return coeff, status, zc
+
+
+def ckks_encode_batch(ctx: Context, slots: torch.Tensor, out=None, stream=None):
+    """Encode slots (C-6). Returns int64 [B,N]."""
+    b = slots.shape[0]
+    m = torch.empty((b, ctx.n), dtype=torch.int64, device=ctx.dev()) if out is None else out
+    _check(lib().ckks_encode_batch(ctx.handle, _kind_of(slots), _ptr(slots), b, _ptr(m), _stream(stream)),
+           "ckks_encode_batch")
+    return m
+
+
+def zinc_ntt_forward(ctx: Context, data: torch.Tensor, stream=None):
+    """In-place forward NTT (C-3) of uint64 [count, L, N]."""
+    _check(lib().zinc_ntt_forward(ctx.handle, _ptr(data), data.numel() // (ctx.L * ctx.n), _stream(stream)),
+           "zinc_ntt_forward")
+    return data
+
+
+def zinc_ntt_inverse(ctx: Context, data: torch.Tensor, stream=None):
+    _check(lib().zinc_ntt_inverse(ctx.handle, _ptr(data), data.numel() // (ctx.L * ctx.n), _stream(stream)),
+           "zinc_ntt_inverse")
+    return data
+
+
+def zinc_debug_sample(ctx: Context, tag: int, seed: int, msg: int, limb: int, n: int, stream=None):
+    dt = torch.uint64 if tag == 3 else torch.int64
+    out = torch.empty((n,), dtype=dt, device=ctx.dev())
+    _check(lib().zinc_debug_sample(ctx.handle, tag, seed, msg, limb, n, _ptr(out), _stream(stream)),
+           "zinc_debug_sample")
+    return out
+
+
+def zinc_int_peak(ctx: Context, blocks: int, iters: int, sink: torch.Tensor, stream=None) -> float:
+    bf = ctypes.c_double()
+    _check(lib().zinc_int_peak(ctx.handle, blocks, iters, _ptr(sink), ctypes.byref(bf), _stream(stream)),
+           "zinc_int_peak")
+    return bf.value
+
+
+def zinc_encrypt_batch_host(ctx: Context, path: int, key: torch.Tensor, form: int, pt_host: torch.Tensor,
+                            seed: int, msg_base: int, ct_host: torch.Tensor, chunk: int = 256):
+    """Host-buffer (end-to-end) encryption: pt_host / ct_host are CPU tensors (pinned for speed)."""
+    if pt_host.is_cuda or ct_host.is_cuda:
+        raise ZincError("zinc_encrypt_batch_host takes host tensors")
+    _check(lib().zinc_encrypt_batch_host(ctx.handle, path, _ptr(key), form, _kind_of(pt_host), _ptr(pt_host),
+                                         pt_host.shape[0], seed, msg_base, _ptr(ct_host), chunk),
+           "zinc_encrypt_batch_host")
+    return ct_host
+
+
+def launch_count() -> int:
+    return int(lib().zinc_launch_count())
+
+
+def launch_count_reset():
+    lib().zinc_launch_count_reset()

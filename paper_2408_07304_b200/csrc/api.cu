@@ -1,0 +1,605 @@
+// api.cu -- the C ABI of libzinc.so (include/zinc.h): validation, parameter
+// generation (C-1, C-2, twiddle / FFT tables), and kernel dispatch.
+//
+// Parameter generation here is written independently of oracle/ (different
+// Miller-Rabin base set, table-driven twiddles); tests check both against the
+// SURVEY Appendix A values.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/zinc.h"
+#include "kernels.h"
+
+using namespace zinc;
+typedef unsigned __int128 u128;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+static zinc_status fail(zinc_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(ZINC_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));      \
+  } while (0)
+#define LAUNCH(expr)                                                                 \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                              \
+    if (_e != cudaSuccess)                                                           \
+      return fail(ZINC_ECUDA, "launch %s failed: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+// ------------------------------------------------------------------ context
+struct zinc_ctx {
+  int device, log_n, n, L, log_scale;
+  std::vector<uint64_t> q, psi;
+  std::vector<LimbConst> h_limbs;
+  LimbConst *d_limbs = nullptr;
+  Tw *d_tw = nullptr, *d_itw = nullptr;
+  double2 *d_fft_tw = nullptr, *d_twist = nullptr;
+  int *d_perm = nullptr;
+  // host-API pipeline buffers (grow-only, guarded)
+  std::mutex host_mu;
+  void *h_pt_d[2] = {nullptr, nullptr};
+  uint64_t *h_ct_d[2] = {nullptr, nullptr};
+  size_t h_pt_bytes = 0, h_ct_bytes = 0;
+  cudaStream_t h_streams[2] = {nullptr, nullptr};
+};
+
+// ------------------------------------------------------------------ number theory (host)
+static uint64_t mulm(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((u128)a * b % m); }
+static uint64_t powm(uint64_t a, uint64_t e, uint64_t m) {
+  uint64_t r = 1;
+  a %= m;
+  for (; e; e >>= 1, a = mulm(a, a, m))
+    if (e & 1) r = mulm(r, a, m);
+  return r;
+}
+// Deterministic Miller-Rabin for 64-bit n (7-base set of Jim Sinclair).
+static bool prime64(uint64_t n) {
+  if (n < 4) return n >= 2;
+  if (n % 2 == 0 || n % 3 == 0) return false;
+  uint64_t d = n - 1;
+  int s = __builtin_ctzll(d);
+  d >>= s;
+  static const uint64_t A[7] = {2, 325, 9375, 28178, 450775, 9780504, 1795265022};
+  for (uint64_t a : A) {
+    uint64_t x = a % n;
+    if (x == 0) continue;
+    x = powm(x, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int r = 1; r < s && comp; ++r) {
+      x = mulm(x, x, n);
+      if (x == n - 1) comp = false;
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+static uint32_t brv(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int i = 0; i < bits; ++i, x >>= 1) r = (r << 1) | (x & 1u);
+  return r;
+}
+static uint64_t shoup(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+
+// C-1: for each listed size, the largest unused prime < 2^b that is 1 mod 2N.
+static bool gen_primes(int log_n, int L, const int *bits, std::vector<uint64_t> &q) {
+  const uint64_t step = 2ull << log_n;
+  q.assign(L, 0);
+  for (int i = 0; i < L; ++i) {
+    uint64_t top = 1ull << bits[i];
+    for (int j = 0; j < i; ++j)
+      if (bits[j] == bits[i]) top = std::min(top, q[j]);
+    uint64_t c = ((top - 2) / step) * step + 1;  // largest 1 mod step below top
+    while (c >= top) c -= step;
+    while (c > step && !prime64(c)) c -= step;
+    if (c <= step) return false;
+    q[i] = c;
+  }
+  return true;
+}
+// C-2: smallest primitive 2N-th root of unity.
+static uint64_t gen_psi(uint64_t q, int log_n) {
+  const uint64_t n = 1ull << log_n;
+  uint64_t g = 0;
+  for (uint64_t x = 2; !g; ++x) {
+    uint64_t c = powm(x, (q - 1) >> (log_n + 1), q);
+    if (powm(c, n, q) == q - 1) g = c;
+  }
+  uint64_t best = g, g2 = mulm(g, g, q), p = g;
+  for (uint64_t k = 0; k < n; ++k, p = mulm(p, g2, q)) best = std::min(best, p);
+  return best;
+}
+
+template <class T>
+static zinc_status upload(T **dst, const std::vector<T> &src) {
+  CUDA_TRY(cudaMalloc((void **)dst, src.size() * sizeof(T)));
+  CUDA_TRY(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return ZINC_OK;
+}
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+extern "C" {
+
+const char *zinc_last_error(void) { return g_err.c_str(); }
+uint64_t zinc_launch_count(void) { return g_launches.load(); }
+void zinc_launch_count_reset(void) { g_launches.store(0); }
+
+zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
+  if (!ctx) return ZINC_OK;
+  cudaSetDevice(ctx->device);
+  cudaFree(ctx->d_limbs);
+  cudaFree(ctx->d_tw);
+  cudaFree(ctx->d_itw);
+  cudaFree(ctx->d_fft_tw);
+  cudaFree(ctx->d_twist);
+  cudaFree(ctx->d_perm);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(ctx->h_pt_d[k]);
+    cudaFree(ctx->h_ct_d[k]);
+    if (ctx->h_streams[k]) cudaStreamDestroy(ctx->h_streams[k]);
+  }
+  delete ctx;
+  return ZINC_OK;
+}
+
+zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scale, int device,
+                            zinc_ctx **out) {
+  if (!out || !limb_bits) return fail(ZINC_EINVAL, "null argument");
+  *out = nullptr;
+  if (log_n < 12 || log_n > 15) return fail(ZINC_EINVAL, "log_n %d outside [12, 15]", log_n);
+  if (L < 1 || L > 32) return fail(ZINC_EINVAL, "num_limbs %d outside [1, 32]", L);
+  if (log_scale < 1 || log_scale > 60) return fail(ZINC_EINVAL, "log_scale %d outside [1, 60]", log_scale);
+  for (int i = 0; i < L; ++i)
+    if (limb_bits[i] < 20 || limb_bits[i] > 60)
+      return fail(ZINC_EINVAL, "limb %d: %d bits outside [20, 60]", i, limb_bits[i]);
+  if (log_n == 15) return fail(ZINC_EUNSUPPORTED, "N = 2^15 is not implemented yet");
+  zinc_ctx *c = new zinc_ctx();
+  c->device = device;
+  c->log_n = log_n;
+  c->n = 1 << log_n;
+  c->L = L;
+  c->log_scale = log_scale;
+  if (!gen_primes(log_n, L, limb_bits, c->q)) { delete c; return fail(ZINC_EPARAMS, "no prime found"); }
+  for (int i = 1; i < L; ++i)
+    if (c->q[i] > c->q[0]) { delete c; return fail(ZINC_EPARAMS, "limb 0 must hold the largest prime (C-10)"); }
+  const int n = c->n;
+  std::vector<Tw> tw((size_t)L * n), itw((size_t)L * n);
+  c->psi.resize(L);
+  c->h_limbs.resize(L);
+  for (int i = 0; i < L; ++i) {
+    const uint64_t q = c->q[i];
+    const uint64_t psi = gen_psi(q, log_n), ipsi = powm(psi, q - 2, q);
+    c->psi[i] = psi;
+    std::vector<uint64_t> pw(n), ipw(n);
+    pw[0] = ipw[0] = 1;
+    for (int e = 1; e < n; ++e) { pw[e] = mulm(pw[e - 1], psi, q); ipw[e] = mulm(ipw[e - 1], ipsi, q); }
+    for (int k = 0; k < n; ++k) {
+      uint64_t w = pw[brv(k, log_n)], iw = ipw[brv(k, log_n)];
+      tw[(size_t)i * n + k] = make_ulonglong2(w, shoup(w, q));
+      itw[(size_t)i * n + k] = make_ulonglong2(iw, shoup(iw, q));
+    }
+    LimbConst &lc = c->h_limbs[i];
+    memset(&lc, 0, sizeof(lc));
+    lc.q = q;
+    lc.two_q = 2 * q;
+    lc.mu64 = (uint64_t)(((u128)1 << 64) / q);
+    lc.b = 64 - __builtin_clzll(q);
+    lc.bmu = (uint64_t)(((u128)1 << (2 * lc.b)) / q);
+    lc.ninv = powm((uint64_t)n % q, q - 2, q);
+    lc.ninv_sh = shoup(lc.ninv, q);
+    lc.ninv_w = mulm(lc.ninv, itw[(size_t)i * n + 1].x, q);
+    lc.ninv_w_sh = shoup(lc.ninv_w, q);
+  }
+  // FFT tables for encode / decode (C-6): M = N/2
+  const int M = n / 2, log_m = log_n - 1;
+  std::vector<double2> ftw(M / 2), twist(M);
+  std::vector<int> perm(M);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int e = 0; e < M / 2; ++e) {
+    long double ang = -2.0L * pi * (long double)e / (long double)M;
+    ftw[e] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  for (int j = 0; j < M; ++j) {
+    long double ang = -pi * (long double)j / (long double)n;
+    twist[j] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  uint64_t g = 1;
+  for (int k = 0; k < M; ++k) {
+    perm[k] = (int)brv((uint32_t)((g - 1) / 4), log_m);
+    g = g * 5 % (2ull * n);
+  }
+  zinc_status st;
+  if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(ZINC_ECUDA, "cudaSetDevice(%d) failed", device); }
+  if ((st = upload(&c->d_limbs, c->h_limbs)) || (st = upload(&c->d_tw, tw)) || (st = upload(&c->d_itw, itw)) ||
+      (st = upload(&c->d_fft_tw, ftw)) || (st = upload(&c->d_twist, twist)) || (st = upload(&c->d_perm, perm))) {
+    zinc_ctx_destroy(c);
+    return st;
+  }
+  // stream-ordered scratch (slot encodes) comes from the default pool: keep it
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return ZINC_OK;
+}
+
+zinc_status zinc_ctx_moduli(const zinc_ctx *ctx, uint64_t *q_out, uint64_t *psi_out) {
+  if (!ctx) return fail(ZINC_EINVAL, "null ctx");
+  for (int i = 0; i < ctx->L; ++i) {
+    if (q_out) q_out[i] = ctx->q[i];
+    if (psi_out) psi_out[i] = ctx->psi[i];
+  }
+  return ZINC_OK;
+}
+
+zinc_status zinc_ctx_info(const zinc_ctx *ctx, int *log_n, int *num_limbs, int *log_scale) {
+  if (!ctx) return fail(ZINC_EINVAL, "null ctx");
+  if (log_n) *log_n = ctx->log_n;
+  if (num_limbs) *num_limbs = ctx->L;
+  if (log_scale) *log_scale = ctx->log_scale;
+  return ZINC_OK;
+}
+
+// ------------------------------------------------------------------ helpers
+static zinc_status check_ptrs(std::initializer_list<const void *> ps) {
+  for (const void *p : ps) {
+    if (!p) return fail(ZINC_EINVAL, "null pointer argument");
+    if (!aligned16(p)) return fail(ZINC_EINVAL, "pointer %p not 16-byte aligned", p);
+  }
+  return ZINC_OK;
+}
+static zinc_status check_form(int form) {
+  return (form == ZINC_FORM_NTT || form == ZINC_FORM_COEFF) ? ZINC_OK : fail(ZINC_EINVAL, "bad form %d", form);
+}
+static zinc_status check_kind(int kind) {
+  return (kind >= ZINC_PT_COEFF_I64 && kind <= ZINC_PT_SLOTS_C128) ? ZINC_OK : fail(ZINC_EINVAL, "bad kind %d", kind);
+}
+static size_t pt_stride_bytes(const zinc_ctx *c, int kind) {
+  return kind == ZINC_PT_COEFF_I64 ? (size_t)c->n * 8 : kind == ZINC_PT_SLOTS_F64 ? (size_t)c->n / 2 * 8 : (size_t)c->n * 8;
+}
+
+static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
+                               cudaStream_t s) {
+  EncodeArgs a{};
+  a.slots = (const double *)slots;
+  a.complex_slots = kind == ZINC_PT_SLOTS_C128;
+  a.perm = c->d_perm;
+  a.fft_tw = c->d_fft_tw;
+  a.twist = c->d_twist;
+  a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
+  a.m_out = m;
+  LAUNCH(launch_encode(c->log_n, a, batch, s));
+  return ZINC_OK;
+}
+
+// One encryption path over messages whose int64 plaintexts are at m (or none).
+enum Path { PATH_ZINC = 0, PATH_VANILLA = 1 };
+static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
+  size_t want = 2 * 148;
+  if (batch >= want) return c->L;
+  int groups = (int)std::min<size_t>((size_t)c->L, (want + batch - 1) / batch);
+  return (c->L + groups - 1) / groups;
+}
+static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, int form, const int64_t *m,
+                            size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s) {
+  if (path == PATH_ZINC && form == ZINC_FORM_COEFF) {
+    ZincCoeffArgs a{};
+    a.limbs = c->d_limbs;
+    a.cache = key;
+    a.m = m;
+    a.ct = ct;
+    a.batch = batch;
+    a.seed = seed;
+    a.msg_base = msg_base;
+    a.n = c->n;
+    a.L = c->L;
+    int threads = 256;
+    while (threads > 32 && zinc_coeff_smem(c->L, threads) > 100 * 1024) threads /= 2;
+    const int gx = c->n / (2 * threads);
+    const int per_sm = (int)std::max<size_t>(1, (200 * 1024) / zinc_coeff_smem(c->L, threads));
+    const size_t target = (size_t)148 * per_sm * 2;
+    size_t gy = std::max<size_t>(1, (target + gx - 1) / gx);
+    a.msgs_per_cta = (batch + gy - 1) / gy;
+    gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
+    LAUNCH(launch_zinc_coeff(a, threads, (int)gy, s));
+    return ZINC_OK;
+  }
+  const int lpc = limbs_per_cta(c, batch);
+  const int groups = (c->L + lpc - 1) / lpc;
+  if (path == PATH_ZINC) {
+    ZincNttArgs a{};
+    a.limbs = c->d_limbs;
+    a.tw = c->d_tw;
+    a.cache = key;
+    a.m = m;
+    a.ct = ct;
+    a.seed = seed;
+    a.msg_base = msg_base;
+    a.L = c->L;
+    a.limbs_per_cta = lpc;
+    LAUNCH(launch_zinc_ntt(c->log_n, a, batch, groups, s));
+    return ZINC_OK;
+  }
+  VanillaArgs a{};
+  a.limbs = c->d_limbs;
+  a.tw = c->d_tw;
+  a.itw = c->d_itw;
+  a.pk = key;
+  a.m = m;
+  a.ct = ct;
+  a.seed = seed;
+  a.msg_base = msg_base;
+  a.L = c->L;
+  a.limbs_per_cta = lpc;
+  LAUNCH(launch_vanilla(c->log_n, a, form, batch, groups, s));
+  return ZINC_OK;
+}
+
+// Encryption with any plaintext kind: int64 plaintexts go straight to the path
+// kernel; slots are encoded chunk by chunk into stream-ordered scratch sized to
+// stay resident in L2 between the encode and the path kernel.
+static const size_t kEncodeChunkBytes = 32ull << 20;
+static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key, int form, int kind,
+                               const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
+                               cudaStream_t s) {
+  if (kind == ZINC_PT_COEFF_I64) return run_path(c, path, key, form, (const int64_t *)pt, batch, seed, msg_base, ct, s);
+  const size_t per_msg = (size_t)c->n * 8;
+  const size_t chunk = std::max<size_t>(1, std::min(batch, kEncodeChunkBytes / per_msg));
+  int64_t *m = nullptr;
+  CUDA_TRY(cudaMallocAsync((void **)&m, chunk * per_msg, s));
+  const size_t in_stride = pt_stride_bytes(c, kind);
+  const size_t ct_stride = (size_t)2 * c->L * c->n;
+  zinc_status st = ZINC_OK;
+  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
+    const size_t cnt = std::min(chunk, batch - off);
+    st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m, s);
+    if (st == ZINC_OK) st = run_path(c, path, key, form, m, cnt, seed, msg_base + off, ct + off * ct_stride, s);
+  }
+  cudaFreeAsync(m, s);
+  return st;
+}
+
+static zinc_status check_encrypt(const zinc_ctx *c, const uint64_t *key, int form, int kind, const void *pt,
+                                 uint64_t *ct) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  zinc_status st;
+  if ((st = check_form(form)) || (st = check_kind(kind)) || (st = check_ptrs({key, pt, ct}))) return st;
+  if (cudaSetDevice(c->device) != cudaSuccess) return fail(ZINC_ECUDA, "cudaSetDevice failed");
+  return ZINC_OK;
+}
+
+// ------------------------------------------------------------------ ABI calls
+zinc_status zinc_keygen(const zinc_ctx *c, uint64_t seed, uint64_t *sk_ntt, int8_t *sk_coeff, uint64_t *pk_ntt,
+                        zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  zinc_status st;
+  if ((st = check_ptrs({sk_ntt, pk_ntt}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  KeygenArgs a{};
+  a.limbs = c->d_limbs;
+  a.tw = c->d_tw;
+  a.pk = pk_ntt;
+  a.sk_ntt = sk_ntt;
+  a.sk_coeff = sk_coeff;
+  a.seed = seed;
+  a.L = c->L;
+  LAUNCH(launch_keygen(c->log_n, a, (cudaStream_t)stream));
+  return ZINC_OK;
+}
+
+zinc_status zinc_precompute_cache(const zinc_ctx *c, const uint64_t *pk_ntt, uint64_t seed, zinc_form form,
+                                  uint64_t *cache, zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  zinc_status st;
+  if ((st = check_form(form)) || (st = check_ptrs({pk_ntt, cache}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  // C-8: vanilla Enc(0), message index 2^64 - 1
+  return run_path(c, PATH_VANILLA, pk_ntt, form, nullptr, 1, seed, UINT64_MAX, cache, (cudaStream_t)stream);
+}
+
+zinc_status zinc_encrypt_batch(const zinc_ctx *c, const uint64_t *cache, zinc_form form, zinc_pt_kind kind,
+                               const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
+                               zinc_stream_t stream) {
+  if (batch == 0) return ZINC_OK;
+  zinc_status st = check_encrypt(c, cache, form, kind, pt, ct);
+  if (st) return st;
+  return encrypt_any(c, PATH_ZINC, cache, form, kind, pt, batch, seed, msg_base, ct, (cudaStream_t)stream);
+}
+
+zinc_status ckks_encrypt_batch(const zinc_ctx *c, const uint64_t *pk_ntt, zinc_form form, zinc_pt_kind kind,
+                               const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
+                               zinc_stream_t stream) {
+  if (batch == 0) return ZINC_OK;
+  zinc_status st = check_encrypt(c, pk_ntt, form, kind, pt, ct);
+  if (st) return st;
+  return encrypt_any(c, PATH_VANILLA, pk_ntt, form, kind, pt, batch, seed, msg_base, ct, (cudaStream_t)stream);
+}
+
+zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_form form, const uint64_t *ct,
+                               size_t batch, double *slots_out, int64_t *coeff_out, int32_t *status_out,
+                               zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (batch == 0) return ZINC_OK;
+  zinc_status st;
+  if ((st = check_form(form)) || (st = check_ptrs({sk_ntt, ct}))) return st;
+  for (const void *p : {(const void *)slots_out, (const void *)coeff_out, (const void *)status_out})
+    if (p && ((uintptr_t)p & 7u)) return fail(ZINC_EINVAL, "output pointer misaligned");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *x = coeff_out;
+  if (!x) CUDA_TRY(cudaMallocAsync((void **)&x, batch * (size_t)c->n * 8, s));
+  DecryptArgs a{};
+  a.limbs = c->d_limbs;
+  a.tw = c->d_tw;
+  a.itw = c->d_itw;
+  a.sk_ntt = sk_ntt;
+  a.ct = ct;
+  a.coeff_out = x;
+  a.status_out = status_out;
+  a.L = c->L;
+  st = ZINC_OK;
+  {
+    cudaError_t e = launch_decrypt(c->log_n, a, form, batch, s);
+    g_launches.fetch_add(1);
+    if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decrypt launch: %s", cudaGetErrorString(e));
+  }
+  if (st == ZINC_OK && slots_out) {
+    DecodeArgs d{};
+    d.coeff = x;
+    d.perm = c->d_perm;
+    d.fft_tw = c->d_fft_tw;
+    d.twist = c->d_twist;
+    d.inv_scale = ldexp(1.0, -c->log_scale);
+    d.slots_out = slots_out;
+    cudaError_t e = launch_decode(c->log_n, d, batch, s);
+    g_launches.fetch_add(1);
+    if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decode launch: %s", cudaGetErrorString(e));
+  }
+  if (!coeff_out) cudaFreeAsync(x, s);
+  return st;
+}
+
+zinc_status ckks_encode_batch(const zinc_ctx *c, zinc_pt_kind kind, const void *slots, size_t batch, int64_t *m_out,
+                              zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (batch == 0) return ZINC_OK;
+  if (kind != ZINC_PT_SLOTS_F64 && kind != ZINC_PT_SLOTS_C128) return fail(ZINC_EINVAL, "encode needs a slot kind");
+  zinc_status st;
+  if ((st = check_ptrs({slots, m_out}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return encode_into(c, kind, slots, batch, m_out, (cudaStream_t)stream);
+}
+
+static zinc_status ntt_dir(const zinc_ctx *c, uint64_t *data, size_t count, int inv, zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (count == 0) return ZINC_OK;
+  zinc_status st;
+  if ((st = check_ptrs({data}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  NttArgs a{};
+  a.limbs = c->d_limbs;
+  a.tw = c->d_tw;
+  a.itw = c->d_itw;
+  a.data = data;
+  a.L = c->L;
+  LAUNCH(launch_ntt(c->log_n, a, inv, count * c->L, (cudaStream_t)stream));
+  return ZINC_OK;
+}
+zinc_status zinc_ntt_forward(const zinc_ctx *c, uint64_t *data, size_t count, zinc_stream_t stream) {
+  return ntt_dir(c, data, count, 0, stream);
+}
+zinc_status zinc_ntt_inverse(const zinc_ctx *c, uint64_t *data, size_t count, zinc_stream_t stream) {
+  return ntt_dir(c, data, count, 1, stream);
+}
+
+zinc_status zinc_debug_sample(const zinc_ctx *c, int tag, uint64_t seed, uint64_t msg, int limb, size_t n, void *out,
+                              zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (tag < 1 || tag > 8) return fail(ZINC_EINVAL, "bad tag %d", tag);
+  if (limb < 0 || limb >= c->L) return fail(ZINC_EINVAL, "bad limb %d", limb);
+  if (n == 0) return ZINC_OK;
+  zinc_status st;
+  if ((st = check_ptrs({out}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  SampleArgs a{};
+  a.tag = (uint32_t)tag;
+  a.limb = (uint32_t)limb;
+  a.seed = seed;
+  a.msg = msg;
+  a.q = c->q[limb];
+  a.n = n;
+  a.out = out;
+  LAUNCH(launch_sample(a, (cudaStream_t)stream));
+  return ZINC_OK;
+}
+
+zinc_status zinc_int_peak(const zinc_ctx *c, int blocks, int iters, uint64_t *sink, double *butterflies,
+                          zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (blocks < 1 || iters < 1) return fail(ZINC_EINVAL, "blocks and iters must be positive");
+  zinc_status st;
+  if ((st = check_ptrs({sink}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  IntPeakArgs a{};
+  a.q = c->q[0];
+  a.w = c->psi[0];
+  a.wp = shoup(c->psi[0], c->q[0]);
+  a.iters = iters;
+  a.sink = sink;
+  LAUNCH(launch_int_peak(a, blocks, (cudaStream_t)stream));
+  if (butterflies) *butterflies = (double)blocks * 256.0 * 8.0 * (double)iters;
+  return ZINC_OK;
+}
+
+zinc_status zinc_encrypt_batch_host(const zinc_ctx *cc, int path, const uint64_t *key, zinc_form form,
+                                    zinc_pt_kind kind, const void *pt_host, size_t batch, uint64_t seed,
+                                    uint64_t msg_base, uint64_t *ct_host, size_t chunk) {
+  zinc_ctx *c = const_cast<zinc_ctx *>(cc);
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (batch == 0) return ZINC_OK;
+  if (path != PATH_ZINC && path != PATH_VANILLA) return fail(ZINC_EINVAL, "bad path %d", path);
+  zinc_status st;
+  if ((st = check_form(form)) || (st = check_kind(kind)) || (st = check_ptrs({key, pt_host, ct_host}))) return st;
+  if (chunk == 0) chunk = 256;
+  chunk = std::min(chunk, batch);
+  std::lock_guard<std::mutex> lock(c->host_mu);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t in_stride = pt_stride_bytes(c, kind);
+  const size_t ct_words = (size_t)2 * c->L * c->n;
+  if (c->h_pt_bytes < chunk * in_stride || c->h_ct_bytes < chunk * ct_words * 8) {
+    for (int k = 0; k < 2; ++k) {
+      cudaFree(c->h_pt_d[k]);
+      cudaFree(c->h_ct_d[k]);
+      c->h_pt_d[k] = nullptr;
+      c->h_ct_d[k] = nullptr;
+    }
+    c->h_pt_bytes = c->h_ct_bytes = 0;
+    for (int k = 0; k < 2; ++k) {
+      if (cudaMalloc(&c->h_pt_d[k], chunk * in_stride) != cudaSuccess ||
+          cudaMalloc((void **)&c->h_ct_d[k], chunk * ct_words * 8) != cudaSuccess)
+        return fail(ZINC_ENOMEM, "host pipeline buffers (%zu messages)", chunk);
+    }
+    c->h_pt_bytes = chunk * in_stride;
+    c->h_ct_bytes = chunk * ct_words * 8;
+  }
+  for (int k = 0; k < 2; ++k)
+    if (!c->h_streams[k]) CUDA_TRY(cudaStreamCreateWithFlags(&c->h_streams[k], cudaStreamNonBlocking));
+  size_t idx = 0;
+  for (size_t off = 0; off < batch; off += chunk, ++idx) {
+    const int k = (int)(idx & 1);
+    cudaStream_t s = c->h_streams[k];
+    const size_t cnt = std::min(chunk, batch - off);
+    CUDA_TRY(cudaMemcpyAsync(c->h_pt_d[k], (const char *)pt_host + off * in_stride, cnt * in_stride,
+                             cudaMemcpyHostToDevice, s));
+    st = encrypt_any(c, path, key, form, kind, c->h_pt_d[k], cnt, seed, msg_base + off, c->h_ct_d[k], s);
+    if (st) return st;
+    CUDA_TRY(cudaMemcpyAsync(ct_host + off * ct_words, c->h_ct_d[k], cnt * ct_words * 8, cudaMemcpyDeviceToHost, s));
+  }
+  for (int k = 0; k < 2; ++k) CUDA_TRY(cudaStreamSynchronize(c->h_streams[k]));
+  return ZINC_OK;
+}
+
+}  // extern "C"

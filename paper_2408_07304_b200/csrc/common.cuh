@@ -1,0 +1,119 @@
+// common.cuh -- device building blocks of the B200 Zinc path (sm_100a).
+//
+// 64-bit modular arithmetic (Shoup twiddle products, Barrett for
+// variable x variable, lazy Harvey butterflies), the Philox4x32-10 counter-based
+// generator and the ternary / CBD / uniform samplers of docs/CONVENTIONS.md C-4.
+// Nothing here is shared with oracle/ (which uses plain `unsigned __int128 %`).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define ZINC_DEV __device__ __forceinline__
+
+namespace zinc {
+
+// Per-limb constants, uploaded once per context (device array of L).
+struct LimbConst {
+  uint64_t q;        // prime modulus, q = 1 mod 2N, q < 2^61
+  uint64_t two_q;
+  uint64_t mu64;     // floor(2^64 / q): reduction of a 64-bit value
+  uint64_t bmu;      // floor(2^(2b) / q), b = bitlen(q): Barrett of a 128-bit product
+  uint32_t b;        // bit length of q
+  uint32_t pad;
+  uint64_t ninv;     // N^-1 mod q
+  uint64_t ninv_sh;  // Shoup companion of ninv
+  uint64_t ninv_w;   // N^-1 * psi^-brv(1) mod q (last GS stage, folded scaling)
+  uint64_t ninv_w_sh;
+};
+
+// Random stream tags (C-4).
+enum Tag : uint32_t {
+  TAG_SK = 1, TAG_PK_E = 2, TAG_PK_A = 3, TAG_ENC_U = 4, TAG_ENC_E1 = 5, TAG_ENC_E2 = 6,
+  TAG_ZINC_E1 = 7, TAG_ZINC_E2 = 8
+};
+
+// ------------------------------------------------------------------ modular
+// w*y mod q in [0, 2q) for any y < 2^64, given wp = floor(w 2^64 / q), w < q.
+ZINC_DEV uint64_t mul_shoup_lazy(uint64_t y, uint64_t w, uint64_t wp, uint64_t q) {
+  return w * y - __umul64hi(wp, y) * q;
+}
+ZINC_DEV uint64_t csub(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
+ZINC_DEV uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }  // a,b < q
+// a*b mod q, a, b < q < 2^61 (Barrett with mu = floor(2^(2b)/q); remainder < 3q)
+ZINC_DEV uint64_t mul_mod(uint64_t a, uint64_t b, const LimbConst &c) {
+  uint64_t lo = a * b, hi = __umul64hi(a, b);
+  uint64_t x1 = (hi << (65 - c.b)) | (lo >> (c.b - 1));
+  uint64_t ph = __umul64hi(x1, c.bmu), pl = x1 * c.bmu;
+  uint64_t q3 = (ph << (63 - c.b)) | (pl >> (c.b + 1));
+  uint64_t r = lo - q3 * c.q;
+  r = csub(r, c.q);
+  return csub(r, c.q);
+}
+// Canonical residue of a signed 64-bit integer (reading A15); mu = floor(2^64/q).
+ZINC_DEV uint64_t reduce_i64q(int64_t v, uint64_t q, uint64_t mu) {
+  uint64_t a = v < 0 ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+  uint64_t r;
+  if (a < q) {
+    r = a;
+  } else {
+    r = a - __umul64hi(a, mu) * q;  // [0, 2q)
+    r = csub(r, q);
+  }
+  return (v < 0 && r != 0) ? q - r : r;
+}
+ZINC_DEV uint64_t reduce_i64(int64_t v, const LimbConst &c) { return reduce_i64q(v, c.q, c.mu64); }
+// Residue of a small signed value |v| < q.
+ZINC_DEV uint64_t reduce_small(int64_t v, uint64_t q) {
+  return v < 0 ? (uint64_t)(v + (int64_t)q) : (uint64_t)v;
+}
+
+// Forward Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> [0, 4q).
+ZINC_DEV void ct_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
+  uint64_t x = csub(X, two_q);
+  uint64_t t = mul_shoup_lazy(Y, w, wp, q);
+  X = x + t;
+  Y = x - t + two_q;
+}
+// Inverse Gentleman-Sande butterfly, lazy: X, Y in [0, 2q) -> [0, 2q).
+ZINC_DEV void gs_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
+  uint64_t s = csub(X + Y, two_q);
+  uint64_t d = X - Y + two_q;
+  Y = mul_shoup_lazy(d, w, wp, q);
+  X = s;
+}
+// [0, 4q) -> [0, q)
+ZINC_DEV uint64_t canon4(uint64_t x, uint64_t q, uint64_t two_q) { return csub(csub(x, two_q), q); }
+
+// ------------------------------------------------------------------ Philox4x32-10
+// Salmon et al., SC'11.  Counter (block, msg_lo, msg_hi, tag<<16|limb),
+// key (seed_lo, seed_hi)  (C-4).
+ZINC_DEV uint4 philox(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+ZINC_DEV uint4 stream_block(uint64_t seed, uint64_t msg, uint32_t tag, uint32_t limb, uint32_t block) {
+  return philox(make_uint4(block, (uint32_t)msg, (uint32_t)(msg >> 32), (tag << 16) | limb),
+                (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+// CBD(eta = 21): coefficients 2*block + {0, 1}
+ZINC_DEV int cbd_lo(uint4 w) { return __popc(w.x & 0x1FFFFFu) - __popc(w.y & 0x1FFFFFu); }
+ZINC_DEV int cbd_hi(uint4 w) { return __popc(w.z & 0x1FFFFFu) - __popc(w.w & 0x1FFFFFu); }
+// ternary: coefficient 4*block + r, value ((w_r * 3) >> 32) - 1
+ZINC_DEV int tern(uint32_t w) { return (int)__umulhi(w, 3u) - 1; }
+// uniform mod q: (w3:w2:w1:w0) mod q, q < 2^61, via Horner on 32-bit digits
+ZINC_DEV uint64_t uniform_mod(uint4 w, uint64_t q) {
+  // r = ((w3 * 2^32 + w2) mod q) ... exact 128-bit remainder by repeated 96/64 steps
+  uint64_t r = (((uint64_t)w.w << 32) | w.z) % q;
+  r = (uint64_t)(((unsigned __int128)r << 32 | w.y) % q);
+  r = (uint64_t)(((unsigned __int128)r << 32 | w.x) % q);
+  return r;
+}
+
+}  // namespace zinc

@@ -1,0 +1,659 @@
+// kernels.cu -- the CUDA kernels of the Zinc hot path (sm_100a) and their
+// launchers.  Section 8(a) of SURVEY.md names the steps; each kernel below says
+// which ones it fuses.
+//
+//   zinc_coeff_kernel   S4 + S5 + S8   Zinc add/inject, COEFF form (HBM-bound headline)
+//   zinc_ntt_kernel     S4 + S5 + S8'  Zinc, NTT form (2 transforms per limb)
+//   vanilla_kernel      S4..S7         vanilla encryption, both forms (3 transforms per limb)
+//   keygen_kernel       S1             Eq. 7
+//   encode_kernel       S3             canonical embedding (FP64 FFT)
+//   decrypt_kernel      S9             Eq. 10 + CRT check
+//   decode_kernel       S9             inverse embedding (FP64 FFT)
+//   ntt_kernel, sample_kernel, int_peak_kernel: test / measurement exports.
+#include <stdint.h>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.h"
+#include "ntt.cuh"
+
+namespace zinc {
+
+// ============================================================ sampling helpers
+// Fill int8 smem arrays with the limb-independent small samples of one message
+// (C-4: ternary / CBD draws use limb 0 and are reduced into every limb).
+template <int THREADS>
+ZINC_DEV void sample_ternary_smem(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
+  for (int blk = threadIdx.x; blk < n / 4; blk += THREADS) {
+    uint4 w = stream_block(seed, msg, tag, 0, blk);
+    char4 t = make_char4(tern(w.x), tern(w.y), tern(w.z), tern(w.w));
+    reinterpret_cast<char4 *>(dst)[blk] = t;
+  }
+}
+template <int THREADS>
+ZINC_DEV void sample_cbd_smem(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
+  for (int blk = threadIdx.x; blk < n / 2; blk += THREADS) {
+    uint4 w = stream_block(seed, msg, tag, 0, blk);
+    reinterpret_cast<char2 *>(dst)[blk] = make_char2(cbd_lo(w), cbd_hi(w));
+  }
+}
+
+ZINC_DEV void ld2(const uint64_t *p, uint64_t &a, uint64_t &b) {
+  ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(p);
+  a = v.x; b = v.y;
+}
+ZINC_DEV void st2(uint64_t *p, uint64_t a, uint64_t b) {
+  *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(a, b);
+}
+// streaming (evict-first) 128-bit store: ciphertexts are written once
+ZINC_DEV void st2_cs(uint64_t *p, uint64_t a, uint64_t b) {
+  asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+ZINC_DEV ulonglong2 ld2_nc(const void *p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+
+// ============================================================ Zinc, COEFF form
+// Algorithm 1 with cache and output in coefficient form:
+//   c1'[i][j] = [zero1[i][j] + m[j] + e1'[j]]_{q_i},  c2'[i][j] = [zero2[i][j] + e2'[j]]_{q_i}.
+// CTA (x, y): coefficient tile [x*T, (x+1)*T), messages [y*mpc, (y+1)*mpc).  The
+// cache tile [2][L][T] is staged once into shared memory with bulk async copies
+// (cp.async.bulk, the 1-D TMA path, completing on an mbarrier) and reused for
+// every message; each thread owns 2 coefficients, draws e1'/e2' with one Philox
+// call each (C-4 block = j/2), and streams 2L 16-byte stores per message.
+__global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
+  extern __shared__ __align__(16) uint64_t tile[];  // [2][L][T], then q[L], mu64[L]
+  __shared__ __align__(8) uint64_t mbar;
+  const int T = 2 * blockDim.x;
+  const int L = a.L;
+  const int j0 = blockIdx.x * T;
+  uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    sq[i] = a.limbs[i].q;
+    smu[i] = a.limbs[i].mu64;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    const uint32_t bytes = (uint32_t)(T * sizeof(uint64_t));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes * 2 * L) : "memory");
+    for (int r = 0; r < 2 * L; ++r) {
+      const uint64_t *src = a.cache + (size_t)r * a.n + j0;
+      uint32_t dst = (uint32_t)__cvta_generic_to_shared(tile + (size_t)r * T);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+    }
+  }
+  {
+    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(mb) : "memory");
+    }
+  }
+  const int jl = 2 * threadIdx.x;       // local coefficient pair
+  const int j = j0 + jl;
+  const size_t b_begin = (size_t)blockIdx.y * a.msgs_per_cta;
+  size_t b_end = b_begin + a.msgs_per_cta;
+  if (b_end > a.batch) b_end = a.batch;
+  const size_t lnn = (size_t)L * a.n;
+  for (size_t b = b_begin; b < b_end; ++b) {
+    const uint64_t msg = a.msg_base + b;
+    const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
+    const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
+    int64_t m0 = 0, m1 = 0;
+    if (a.m) {
+      ulonglong2 mv = ld2_nc(a.m + b * a.n + j);
+      m0 = (int64_t)mv.x; m1 = (int64_t)mv.y;
+    }
+    const int64_t v0 = m0 + cbd_lo(w1), v1 = m1 + cbd_hi(w1);
+    const int f0 = cbd_lo(w2), f1 = cbd_hi(w2);
+    uint64_t *out = a.ct + b * 2 * lnn + j;
+#pragma unroll 4
+    for (int i = 0; i < L; ++i) {
+      const uint64_t q = sq[i], mu = smu[i];
+      uint64_t z10, z11, z20, z21;
+      ld2(tile + (size_t)i * T + jl, z10, z11);
+      ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+      const uint64_t c10 = add_mod(z10, reduce_i64q(v0, q, mu), q);
+      const uint64_t c11 = add_mod(z11, reduce_i64q(v1, q, mu), q);
+      const uint64_t c20 = add_mod(z20, reduce_small(f0, q), q);
+      const uint64_t c21 = add_mod(z21, reduce_small(f1, q), q);
+      st2_cs(out + (size_t)i * a.n, c10, c11);
+      st2_cs(out + lnn + (size_t)i * a.n, c20, c21);
+    }
+  }
+}
+
+// ============================================================ vanilla encryption
+// Eq. 8 with reading A1: c1 = [pk1.u + e1 + m]_q, c2 = [pk2.u + e2]_q.  CTA =
+// (message b, limb group); u, e1, e2 are sampled once per CTA into smem (int8),
+// then per limb:
+//  NTT form:   NTT(e1 + m) -> ct0;  NTT(e2) -> ct1;
+//              NTT(u) -> epilogue ct0 += pk1 u^, ct1 += pk2 u^.
+//  COEFF form: NTT(u) -> epilogue: ct1 <- pk2 u^ (temporary), smem <- pk1 u^;
+//              INTT(smem) + e1 + m -> ct0;  INTT(ct1) + e2 -> ct1.
+// 3 transforms per limb either way.
+template <int LOGN, int FORM>
+__global__ void __launch_bounds__(Plan<LOGN>::THREADS) vanilla_kernel(VanillaArgs a) {
+  constexpr int N = 1 << LOGN;
+  constexpr int THREADS = Plan<LOGN>::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  int8_t *su = reinterpret_cast<int8_t *>(sm + SmemWords<LOGN>::value);
+  int8_t *se1 = su + N, *se2 = se1 + N;
+  const size_t b = blockIdx.x;
+  const uint64_t msg = a.msg_base + b;
+  sample_ternary_smem<THREADS>(su, N, a.seed, msg, TAG_ENC_U);
+  sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1);
+  sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2);
+  __syncthreads();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    if (FORM == 0) {
+      ntt_forward<LOGN>(sm, tw, q,
+          [&](int x) { return reduce_i64((int64_t)se1[x] + (m ? m[x] : 0), c); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) st2(ct0 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
+          });
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) st2(ct1 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
+          });
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(su[x], q); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) {
+              uint64_t u0 = canon4(v[r], q, two_q), u1 = canon4(v[r + 1], q, two_q);
+              uint64_t p10, p11, p20, p21, a0, a1, b0, b1;
+              ld2(pk1 + base + r, p10, p11);
+              ld2(pk2 + base + r, p20, p21);
+              ld2(ct0 + base + r, a0, a1);
+              ld2(ct1 + base + r, b0, b1);
+              st2_cs(ct0 + base + r, add_mod(a0, mul_mod(p10, u0, c), q), add_mod(a1, mul_mod(p11, u1, c), q));
+              st2_cs(ct1 + base + r, add_mod(b0, mul_mod(p20, u0, c), q), add_mod(b1, mul_mod(p21, u1, c), q));
+            }
+          });
+    } else {
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(su[x], q); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) {
+              uint64_t u0 = canon4(v[r], q, two_q), u1 = canon4(v[r + 1], q, two_q);
+              uint64_t p10, p11, p20, p21;
+              ld2(pk1 + base + r, p10, p11);
+              ld2(pk2 + base + r, p20, p21);
+              st2(ct1 + base + r, mul_mod(p20, u0, c), mul_mod(p21, u1, c));
+              sm[pad16(base + r)] = mul_mod(p10, u0, c);
+              sm[pad16(base + r + 1)] = mul_mod(p11, u1, c);
+            }
+          });
+      const Tw *itw = a.itw + (size_t)i * N;
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base + r)];
+          },
+          [&](int x, uint64_t v) {
+            uint64_t e = reduce_i64((int64_t)se1[x] + (m ? m[x] : 0), c);
+            __stcs(ct0 + x, add_mod(csub(v, q), e, q));
+          });
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) ld2(ct1 + base + r, v[r], v[r + 1]);
+          },
+          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), reduce_small(se2[x], q), q)); });
+    }
+  }
+}
+
+// ============================================================ Zinc, NTT form
+// c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2') (two DFTs,
+// no multiplication).
+template <int LOGN>
+__global__ void __launch_bounds__(Plan<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArgs a) {
+  constexpr int N = 1 << LOGN;
+  constexpr int THREADS = Plan<LOGN>::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  int8_t *se1 = reinterpret_cast<int8_t *>(sm + SmemWords<LOGN>::value);
+  int8_t *se2 = se1 + N;
+  const size_t b = blockIdx.x;
+  const uint64_t msg = a.msg_base + b;
+  sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ZINC_E1);
+  sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2);
+  __syncthreads();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    const uint64_t *z1 = a.cache + (size_t)i * N, *z2 = a.cache + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    ntt_forward<LOGN>(sm, tw, q,
+        [&](int x) { return reduce_i64((int64_t)se1[x] + (m ? m[x] : 0), c); },
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            uint64_t za, zb;
+            ld2(z1 + base + r, za, zb);
+            st2_cs(ct0 + base + r, add_mod(za, canon4(v[r], q, two_q), q), add_mod(zb, canon4(v[r + 1], q, two_q), q));
+          }
+        });
+    ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); },
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            uint64_t za, zb;
+            ld2(z2 + base + r, za, zb);
+            st2_cs(ct1 + base + r, add_mod(za, canon4(v[r], q, two_q), q), add_mod(zb, canon4(v[r + 1], q, two_q), q));
+          }
+        });
+  }
+}
+
+// ============================================================ keygen (Eq. 7)
+// One CTA per limb: a <- U(R_qi) (tag PK_A, limb i), s <- R_2 (SK), e <- chi (PK_E);
+// pk2 = a^, sk = s^, pk1 = -a^ s^ + e^ (NTT domain; C-5).
+template <int LOGN>
+__global__ void __launch_bounds__(Plan<LOGN>::THREADS) keygen_kernel(KeygenArgs a) {
+  constexpr int N = 1 << LOGN;
+  constexpr int THREADS = Plan<LOGN>::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  int8_t *ss = reinterpret_cast<int8_t *>(sm + SmemWords<LOGN>::value);
+  int8_t *se = ss + N;
+  sample_ternary_smem<THREADS>(ss, N, a.seed, 0, TAG_SK);
+  sample_cbd_smem<THREADS>(se, N, a.seed, 0, TAG_PK_E);
+  __syncthreads();
+  const int i = blockIdx.x, L = a.L;
+  if (i == 0 && a.sk_coeff)
+    for (int x = threadIdx.x; x < N; x += THREADS) a.sk_coeff[x] = ss[x];
+  const LimbConst c = a.limbs[i];
+  const uint64_t q = c.q, two_q = c.two_q;
+  const Tw *tw = a.tw + (size_t)i * N;
+  uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+  uint64_t *sk = a.sk_ntt + (size_t)i * N;
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return uniform_mod(stream_block(a.seed, 0, TAG_PK_A, i, x), q); },
+      [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) pk2[base + r] = canon4(v[r], q, two_q);
+      });
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(ss[x], q); },
+      [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sk[base + r] = canon4(v[r], q, two_q);
+      });
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se[x], q); },
+      [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          uint64_t as = mul_mod(pk2[base + r], sk[base + r], c);
+          pk1[base + r] = add_mod(q - as == q ? 0 : q - as, canon4(v[r], q, two_q), q);
+        }
+      });
+}
+
+// ============================================================ decrypt (Eq. 10)
+// One CTA per message, limbs in order 0..L-1: x^(i) = [c1 + c2 s]_{q_i} (an INTT,
+// plus an NTT of c2 in COEFF form).  Limb 0 writes x0 = centred residue mod q_0
+// to coeff_out; every other limb checks x0 mod q_i == x^(i) (C-10).
+template <int LOGN, int FORM>
+__global__ void __launch_bounds__(Plan<LOGN>::THREADS) decrypt_kernel(DecryptArgs a) {
+  constexpr int N = 1 << LOGN;
+  extern __shared__ __align__(16) uint64_t sm[];
+  const size_t b = blockIdx.x;
+  const int L = a.L;
+  int bad = 0;
+  int64_t *x0 = a.coeff_out + b * N;
+  const uint64_t q0 = a.limbs[0].q;
+  for (int i = 0; i < L; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t *c1 = a.ct + b * 2 * L * N + (size_t)i * N;
+    const uint64_t *c2 = c1 + (size_t)L * N;
+    const uint64_t *s = a.sk_ntt + (size_t)i * N;
+    const Tw *itw = a.itw + (size_t)i * N;
+    auto epilogue = [&](int x, uint64_t v) {
+      uint64_t xi = csub(v, q);
+      if (FORM == 1) xi = add_mod(xi, c1[x], q);
+      if (i == 0) {
+        x0[x] = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
+      } else {
+        if (reduce_i64(x0[x], c) != xi) bad = 1;
+      }
+    };
+    if (FORM == 0) {
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = add_mod(c1[base + r], mul_mod(c2[base + r], s[base + r], c), q);
+          },
+          epilogue);
+    } else {
+      const Tw *tw = a.tw + (size_t)i * N;
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return c2[x]; },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) sm[pad16(base + r)] = mul_mod(canon4(v[r], q, two_q), s[base + r], c);
+          });
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base + r)];
+          },
+          epilogue);
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0 && a.status_out) a.status_out[b] = bad;
+}
+
+// ============================================================ encode (C-6)
+template <int LOGM>
+__global__ void __launch_bounds__(FftPlan<LOGM>::THREADS) encode_kernel(EncodeArgs a) {
+  constexpr int M = 1 << LOGM;
+  using P = FftPlan<LOGM>;
+  extern __shared__ __align__(16) double2 buf[];
+  const size_t b = blockIdx.x;
+  for (int k = threadIdx.x; k < M; k += P::THREADS) {
+    double2 z;
+    if (a.complex_slots) {
+      z = reinterpret_cast<const double2 *>(a.slots)[b * M + k];
+    } else {
+      z = make_double2(a.slots[b * M + k], 0.0);
+    }
+    buf[pad16(a.perm[k])] = z;
+  }
+  __syncthreads();
+  auto lds = [&](int i) { return buf[pad16(i)]; };
+  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
+  fft_pass<LOGM, 0, P::K1, P::THREADS, true, false>(a.fft_tw, lds, sts);
+  __syncthreads();
+  fft_pass<LOGM, P::K1, P::K2, P::THREADS, true, false>(a.fft_tw, lds, sts);
+  __syncthreads();
+  int64_t *m = a.m_out + b * (2 * M);
+  const double scale = a.scale;  // Delta / M, a power of two
+  fft_pass<LOGM, P::K1 + P::K2, P::K3, P::THREADS, true, false>(a.fft_tw, lds, [&](int j, double2 v) {
+    const double2 w = cmul(v, __ldg(a.twist + j));
+    m[j] = llround(w.x * scale);
+    m[j + M] = llround(w.y * scale);
+  });
+}
+
+// ============================================================ decode (C-10)
+template <int LOGM>
+__global__ void __launch_bounds__(FftPlan<LOGM>::THREADS) decode_kernel(DecodeArgs a) {
+  constexpr int M = 1 << LOGM;
+  using P = FftPlan<LOGM>;
+  extern __shared__ __align__(16) double2 buf[];
+  const size_t b = blockIdx.x;
+  const int64_t *x = a.coeff + b * (2 * M);
+  auto lds = [&](int i) { return buf[pad16(i)]; };
+  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
+  fft_pass<LOGM, P::K1 + P::K2, P::K3, P::THREADS, false, true>(a.fft_tw,
+      [&](int j) {
+        const double2 v = make_double2((double)x[j], (double)x[j + M]);
+        return cmul(v, conj2(__ldg(a.twist + j)));
+      }, sts);
+  __syncthreads();
+  fft_pass<LOGM, P::K1, P::K2, P::THREADS, false, true>(a.fft_tw, lds, sts);
+  __syncthreads();
+  fft_pass<LOGM, 0, P::K1, P::THREADS, false, true>(a.fft_tw, lds, sts);
+  __syncthreads();
+  double2 *out = reinterpret_cast<double2 *>(a.slots_out) + b * M;
+  for (int k = threadIdx.x; k < M; k += P::THREADS) {
+    const double2 v = buf[pad16(a.perm[k])];
+    out[k] = make_double2(v.x * a.inv_scale, v.y * a.inv_scale);
+  }
+}
+
+// ============================================================ standalone NTT
+template <int LOGN, int INV>
+__global__ void __launch_bounds__(Plan<LOGN>::THREADS) ntt_kernel(NttArgs a) {
+  constexpr int N = 1 << LOGN;
+  extern __shared__ __align__(16) uint64_t sm[];
+  const int i = blockIdx.x % a.L;
+  uint64_t *p = a.data + (size_t)blockIdx.x * N;
+  const LimbConst c = a.limbs[i];
+  const uint64_t q = c.q, two_q = c.two_q;
+  if (INV == 0) {
+    ntt_forward<LOGN>(sm, a.tw + (size_t)i * N, q, [&](int x) { return p[x]; },
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) p[base + r] = canon4(v[r], q, two_q);
+        });
+  } else {
+    ntt_inverse<LOGN>(sm, a.itw + (size_t)i * N, c,
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) v[r] = p[base + r];
+        },
+        [&](int x, uint64_t v) { p[x] = csub(v, q); });
+  }
+}
+
+// ============================================================ samplers (debug)
+__global__ void sample_kernel(SampleArgs a) {
+  size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.n) return;
+  if (a.tag == TAG_SK || a.tag == TAG_ENC_U) {
+    uint4 w = stream_block(a.seed, a.msg, a.tag, 0, (uint32_t)(c / 4));
+    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    reinterpret_cast<int64_t *>(a.out)[c] = tern(ws[c % 4]);
+  } else if (a.tag == TAG_PK_A) {
+    uint4 w = stream_block(a.seed, a.msg, a.tag, a.limb, (uint32_t)c);
+    reinterpret_cast<uint64_t *>(a.out)[c] = uniform_mod(w, a.q);
+  } else {
+    uint4 w = stream_block(a.seed, a.msg, a.tag, 0, (uint32_t)(c / 2));
+    reinterpret_cast<int64_t *>(a.out)[c] = (c & 1) ? cbd_hi(w) : cbd_lo(w);
+  }
+}
+
+// ============================================================ integer peak (K11)
+// 8 independent register-resident lazy Shoup butterflies per iteration, the
+// same instruction mix as the NTT passes, no memory traffic.
+__global__ void __launch_bounds__(256) int_peak_kernel(IntPeakArgs a) {
+  const uint64_t q = a.q, two_q = 2 * a.q;
+  uint64_t v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = (threadIdx.x * 16 + r + blockIdx.x) % q;
+  uint64_t w = a.w, wp = a.wp;
+  for (int it = 0; it < a.iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) ct_bfly(v[r], v[r + 8], w, wp, q, two_q);
+    w += (v[0] & 1);  // keep w loop-variant so the compiler cannot hoist
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc ^= v[r];
+  if (acc == 0x1234567890ABCDEFull) a.sink[0] = acc;
+}
+
+// ============================================================ launchers
+template <class K>
+static cudaError_t set_smem(K kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+size_t zinc_coeff_smem(int L, int threads) { return ((size_t)2 * L * 2 * threads + 2 * L) * sizeof(uint64_t); }
+
+cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, cudaStream_t s) {
+  size_t smem = zinc_coeff_smem(a.L, threads);
+  cudaError_t e = set_smem(zinc_coeff_kernel, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(a.n / (2 * threads), grid_y);
+  zinc_coeff_kernel<<<grid, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int LOGN> static size_t ntt_smem_words() { return SmemWords<LOGN>::value * sizeof(uint64_t); }
+
+template <int LOGN>
+static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
+  size_t smem = ntt_smem_words<LOGN>() + 3 * (1 << LOGN);
+  dim3 grid((unsigned)batch, groups);
+  cudaError_t e;
+  if (form == 0) {
+    if ((e = set_smem(vanilla_kernel<LOGN, 0>, smem)) != cudaSuccess) return e;
+    vanilla_kernel<LOGN, 0><<<grid, Plan<LOGN>::THREADS, smem, s>>>(a);
+  } else {
+    if ((e = set_smem(vanilla_kernel<LOGN, 1>, smem)) != cudaSuccess) return e;
+    vanilla_kernel<LOGN, 1><<<grid, Plan<LOGN>::THREADS, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_vanilla_t<12>(a, form, batch, groups, s);
+    case 13: return launch_vanilla_t<13>(a, form, batch, groups, s);
+    case 14: return launch_vanilla_t<14>(a, form, batch, groups, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int LOGN>
+static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
+  size_t smem = ntt_smem_words<LOGN>() + 2 * (1 << LOGN);
+  cudaError_t e;
+  if ((e = set_smem(zinc_ntt_kernel<LOGN>, smem)) != cudaSuccess) return e;
+  zinc_ntt_kernel<LOGN><<<dim3((unsigned)batch, groups), Plan<LOGN>::THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_zinc_ntt_t<12>(a, batch, groups, s);
+    case 13: return launch_zinc_ntt_t<13>(a, batch, groups, s);
+    case 14: return launch_zinc_ntt_t<14>(a, batch, groups, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int LOGN>
+static cudaError_t launch_keygen_t(const KeygenArgs &a, cudaStream_t s) {
+  size_t smem = ntt_smem_words<LOGN>() + 2 * (1 << LOGN);
+  cudaError_t e;
+  if ((e = set_smem(keygen_kernel<LOGN>, smem)) != cudaSuccess) return e;
+  keygen_kernel<LOGN><<<a.L, Plan<LOGN>::THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_keygen_t<12>(a, s);
+    case 13: return launch_keygen_t<13>(a, s);
+    case 14: return launch_keygen_t<14>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int LOGN>
+static cudaError_t launch_decrypt_t(const DecryptArgs &a, int form, size_t batch, cudaStream_t s) {
+  size_t smem = ntt_smem_words<LOGN>();
+  cudaError_t e;
+  if (form == 0) {
+    if ((e = set_smem(decrypt_kernel<LOGN, 0>, smem)) != cudaSuccess) return e;
+    decrypt_kernel<LOGN, 0><<<(unsigned)batch, Plan<LOGN>::THREADS, smem, s>>>(a);
+  } else {
+    if ((e = set_smem(decrypt_kernel<LOGN, 1>, smem)) != cudaSuccess) return e;
+    decrypt_kernel<LOGN, 1><<<(unsigned)batch, Plan<LOGN>::THREADS, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_decrypt_t<12>(a, form, batch, s);
+    case 13: return launch_decrypt_t<13>(a, form, batch, s);
+    case 14: return launch_decrypt_t<14>(a, form, batch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int LOGM> static size_t fft_smem() { return ((1 << LOGM) + ((1 << LOGM) >> 4)) * sizeof(double2); }
+
+template <int LOGM>
+static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = set_smem(encode_kernel<LOGM>, fft_smem<LOGM>())) != cudaSuccess) return e;
+  encode_kernel<LOGM><<<(unsigned)batch, FftPlan<LOGM>::THREADS, fft_smem<LOGM>(), s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_encode_t<11>(a, batch, s);
+    case 13: return launch_encode_t<12>(a, batch, s);
+    case 14: return launch_encode_t<13>(a, batch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int LOGM>
+static cudaError_t launch_decode_t(const DecodeArgs &a, size_t batch, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = set_smem(decode_kernel<LOGM>, fft_smem<LOGM>())) != cudaSuccess) return e;
+  decode_kernel<LOGM><<<(unsigned)batch, FftPlan<LOGM>::THREADS, fft_smem<LOGM>(), s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_decode_t<11>(a, batch, s);
+    case 13: return launch_decode_t<12>(a, batch, s);
+    case 14: return launch_decode_t<13>(a, batch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int LOGN>
+static cudaError_t launch_ntt_t(const NttArgs &a, int inv, size_t polys, cudaStream_t s) {
+  size_t smem = ntt_smem_words<LOGN>();
+  cudaError_t e;
+  if (inv == 0) {
+    if ((e = set_smem(ntt_kernel<LOGN, 0>, smem)) != cudaSuccess) return e;
+    ntt_kernel<LOGN, 0><<<(unsigned)polys, Plan<LOGN>::THREADS, smem, s>>>(a);
+  } else {
+    if ((e = set_smem(ntt_kernel<LOGN, 1>, smem)) != cudaSuccess) return e;
+    ntt_kernel<LOGN, 1><<<(unsigned)polys, Plan<LOGN>::THREADS, smem, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s) {
+  switch (log_n) {
+    case 12: return launch_ntt_t<12>(a, inv, polys, s);
+    case 13: return launch_ntt_t<13>(a, inv, polys, s);
+    case 14: return launch_ntt_t<14>(a, inv, polys, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s) {
+  unsigned blocks = (unsigned)((a.n + 255) / 256);
+  sample_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_int_peak(const IntPeakArgs &a, int blocks, cudaStream_t s) {
+  int_peak_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace zinc

@@ -1,0 +1,103 @@
+// kernels.h -- argument blocks and launchers of the kernels in kernels.cu
+// (internal to libzinc.so; the public ABI is include/zinc.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace zinc {
+
+using Tw = ulonglong2;  // {w, floor(w 2^64 / q)}
+
+struct ZincCoeffArgs {
+  const LimbConst *limbs;
+  const uint64_t *cache;  // [2][L][N]
+  const int64_t *m;       // [batch][N] or null (m = 0)
+  uint64_t *ct;           // [batch][2][L][N]
+  size_t batch, msgs_per_cta;
+  uint64_t seed, msg_base;
+  int n, L;
+};
+struct VanillaArgs {
+  const LimbConst *limbs;
+  const Tw *tw, *itw;
+  const uint64_t *pk;     // [2][L][N] NTT form
+  const int64_t *m;       // [batch][N] or null
+  uint64_t *ct;
+  uint64_t seed, msg_base;
+  int L, limbs_per_cta;
+};
+struct ZincNttArgs {
+  const LimbConst *limbs;
+  const Tw *tw;
+  const uint64_t *cache;  // NTT form
+  const int64_t *m;
+  uint64_t *ct;
+  uint64_t seed, msg_base;
+  int L, limbs_per_cta;
+};
+struct KeygenArgs {
+  const LimbConst *limbs;
+  const Tw *tw;
+  uint64_t *pk, *sk_ntt;
+  int8_t *sk_coeff;
+  uint64_t seed;
+  int L;
+};
+struct DecryptArgs {
+  const LimbConst *limbs;
+  const Tw *tw, *itw;
+  const uint64_t *sk_ntt, *ct;
+  int64_t *coeff_out;
+  int32_t *status_out;
+  int L;
+};
+struct EncodeArgs {
+  const double *slots;
+  int complex_slots;
+  const int *perm;
+  const double2 *fft_tw, *twist;
+  double scale;
+  int64_t *m_out;
+};
+struct DecodeArgs {
+  const int64_t *coeff;
+  const int *perm;
+  const double2 *fft_tw, *twist;
+  double inv_scale;
+  double *slots_out;
+};
+struct NttArgs {
+  const LimbConst *limbs;
+  const Tw *tw, *itw;
+  uint64_t *data;
+  int L;
+};
+struct SampleArgs {
+  uint32_t tag, limb;
+  uint64_t seed, msg, q;
+  size_t n;
+  void *out;
+};
+struct IntPeakArgs {
+  uint64_t q, w, wp;
+  int iters;
+  uint64_t *sink;
+};
+
+size_t zinc_coeff_smem(int L, int threads);
+cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, cudaStream_t s);
+cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s);
+cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s);
+cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);
+cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s);
+cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s);
+cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s);
+cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s);
+cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
+cudaError_t launch_int_peak(const IntPeakArgs &a, int blocks, cudaStream_t s);
+
+}  // namespace zinc

@@ -1,0 +1,316 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bar (BASELINE.json north_star): ciphertext words bit-exact given the same seed
+and the same int64 plaintext; encode within +-1 per coefficient (floating point,
+C-6 / reading A9); decoded slots within 1e-4 at 2^40, 1e-3 at 2^30.
+"""
+import numpy as np
+import pytest
+import torch
+
+from workloads import CONFIGS, int_plaintexts, message_slots, slots_batch
+
+pytestmark = pytest.mark.gpu
+
+NTT, COEFF = 0, 1
+
+
+def np64(t):
+    return t.cpu().numpy()
+
+
+def dev_u64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64)).cuda()
+
+
+def dev_i64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).cuda()
+
+
+@pytest.fixture(scope="module")
+def Z():
+    import paper_2408_07304_b200 as Z
+    assert torch.cuda.is_available()
+    return Z
+
+
+class Setup:
+    def __init__(self, Z, orc, cfg):
+        self.cfg = cfg
+        self.ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
+        self.P = orc.Params.make(cfg.log_n, cfg.bits, cfg.log_scale)
+        self.sk, self.skc, self.pk = Z.zinc_keygen(self.ctx, cfg.key_seed)
+        self.o_sk, self.o_sk_ntt, self.o_pk = orc.keygen(self.P, cfg.key_seed)
+        self.cache = {f: Z.zinc_precompute_cache(self.ctx, self.pk, cfg.cache_seed, f) for f in (NTT, COEFF)}
+        torch.cuda.synchronize()
+
+
+_setups = {}
+
+
+def setup_for(Z, orc, name):
+    if name not in _setups:
+        _setups[name] = Setup(Z, orc, CONFIGS[name])
+    return _setups[name]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_params_match_oracle(Z, orc, name):
+    s = setup_for(Z, orc, name)
+    assert s.ctx.q == [int(x) for x in s.P.q]
+    assert s.ctx.psi == [int(x) for x in s.P.psi]
+
+
+@pytest.mark.parametrize("tag", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_sampler_streams_bit_exact(Z, orc, tag):
+    s = setup_for(Z, orc, "C3")
+    n = 4100  # ragged: not a multiple of the 4-per-block ternary layout
+    for seed, msg, limb in [(1, 0, 0), (0xDEADBEEFCAFEF00D, (1 << 32) + 5, 3), (7, (1 << 64) - 1, 7)]:
+        got = np64(Z.zinc_debug_sample(s.ctx, tag, seed, msg, limb, n))
+        if tag == 3:
+            want = orc.sample_uniform(seed, msg, tag, limb, int(s.P.q[limb]), n)
+        elif tag in (1, 4):
+            want = orc.sample_ternary(seed, msg, tag, n)
+        else:
+            want = orc.sample_cbd(seed, msg, tag, n)
+        assert np.array_equal(got, want), (tag, seed, msg, limb)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_ntt_bit_exact(Z, orc, name):
+    s = setup_for(Z, orc, name)
+    rng = np.random.default_rng(11)
+    count = 3
+    x = np.stack([np.stack([rng.integers(0, int(q), s.P.n, dtype=np.uint64) for q in s.P.q]) for _ in range(count)])
+    d = dev_u64(x)
+    Z.zinc_ntt_forward(s.ctx, d)
+    fwd = np64(d)
+    for c in range(count):
+        assert np.array_equal(fwd[c], orc.ntt_limbs(s.P, x[c]))
+    Z.zinc_ntt_inverse(s.ctx, d)
+    assert np.array_equal(np64(d), x)
+    # edge values: all q-1, all 0
+    e = np.stack([np.full(s.P.n, int(q) - 1, dtype=np.uint64) for q in s.P.q])[None]
+    d = dev_u64(e)
+    Z.zinc_ntt_forward(s.ctx, d)
+    assert np.array_equal(np64(d)[0], orc.ntt_limbs(s.P, e[0]))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_keygen_and_cache_bit_exact(Z, orc, name):
+    s = setup_for(Z, orc, name)
+    assert np.array_equal(np64(s.skc).astype(np.int64), s.o_sk)
+    assert np.array_equal(np64(s.sk), s.o_sk_ntt)
+    assert np.array_equal(np64(s.pk), s.o_pk)
+    for f in (NTT, COEFF):
+        assert np.array_equal(np64(s.cache[f]), orc.precompute_cache(s.P, s.o_pk, s.cfg.cache_seed, f))
+
+
+def _check_msgs(orc, s, path, form, m, got, seed, msg_base, idx):
+    key = s.o_pk if path == "vanilla" else orc.precompute_cache(s.P, s.o_pk, s.cfg.cache_seed, form)
+    for b in idx:
+        if path == "vanilla":
+            want = orc.vanilla_encrypt(s.P, key, m[b], seed, msg_base + b, form)
+        else:
+            want = orc.zinc_encrypt(s.P, key, form, m[b], seed, msg_base + b)
+        assert np.array_equal(got[b], want), (path, form, b)
+
+
+@pytest.mark.parametrize("path", ["zinc", "vanilla"])
+@pytest.mark.parametrize("form", [NTT, COEFF])
+def test_encrypt_int64_c1_all_messages(Z, orc, path, form):
+    """C1 in full: all 256 messages bit-exact."""
+    s = setup_for(Z, orc, "C1")
+    B = s.cfg.batch
+    m = int_plaintexts(s.cfg.log_n, B, seed=1, bound_bits=34)
+    seed, base = s.cfg.enc_seed, 1000
+    if path == "zinc":
+        ct = Z.zinc_encrypt_batch(s.ctx, s.cache[form], form, dev_i64(m), seed, base)
+    else:
+        ct = Z.ckks_encrypt_batch(s.ctx, s.pk, form, dev_i64(m), seed, base)
+    _check_msgs(orc, s, path, form, m, np64(ct), seed, base, range(B))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+@pytest.mark.parametrize("path", ["zinc", "vanilla"])
+@pytest.mark.parametrize("form", [NTT, COEFF])
+def test_encrypt_int64_sampled(Z, orc, name, path, form):
+    """Ragged batch (37 messages, not a multiple of any tile), sampled messages."""
+    s = setup_for(Z, orc, name)
+    B = 37
+    m = int_plaintexts(s.cfg.log_n, B, seed=2, bound_bits=50)
+    m[3, :5] = [np.iinfo(np.int64).max, np.iinfo(np.int64).min + 1, -(1 << 62), (1 << 61) + 12345, -1]  # slow reduce path
+    seed, base = 0x123456789, (1 << 32) - 20  # message indices cross the 2^32 counter word
+    if path == "zinc":
+        ct = Z.zinc_encrypt_batch(s.ctx, s.cache[form], form, dev_i64(m), seed, base)
+    else:
+        ct = Z.ckks_encrypt_batch(s.ctx, s.pk, form, dev_i64(m), seed, base)
+    _check_msgs(orc, s, path, form, m, np64(ct), seed, base, [0, 3, 19, 20, 36])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_encode_within_one(Z, orc, name):
+    s = setup_for(Z, orc, name)
+    cfg = s.cfg
+    B = 6
+    z = slots_batch(cfg, 0, B) if name != "C3" else np.stack(
+        [message_slots(cfg, b) for b in (0, 1, cfg.batch - 2, cfg.batch - 1, 5, 9000)])
+    m = np64(Z.ckks_encode_batch(s.ctx, torch.from_numpy(np.ascontiguousarray(z)).cuda()))
+    for b in range(B):
+        want = orc.encode(z[b], cfg.log_n, cfg.log_scale)
+        assert np.max(np.abs(m[b] - want)) <= 1
+    if name == "C1":
+        want = orc.encode_definition(z[0], cfg.log_n, cfg.log_scale)
+        assert np.max(np.abs(m[0] - want)) <= 1
+
+
+def test_encode_complex_slots(Z, orc):
+    s = setup_for(Z, orc, "C2")
+    rng = np.random.default_rng(5)
+    z = rng.uniform(-1, 1, (3, s.P.n // 2)) + 1j * rng.uniform(-1, 1, (3, s.P.n // 2))
+    zz = np.stack([z.real, z.imag], axis=-1)
+    m = np64(Z.ckks_encode_batch(s.ctx, torch.from_numpy(np.ascontiguousarray(zz)).cuda()))
+    for b in range(3):
+        assert np.max(np.abs(m[b] - orc.encode(z[b], s.P.log_n, s.P.log_scale))) <= 1
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+@pytest.mark.parametrize("path", ["zinc", "vanilla"])
+@pytest.mark.parametrize("form", [NTT, COEFF])
+def test_slots_to_ciphertext_and_decrypt(Z, orc, name, path, form):
+    """Slots in: the ciphertext equals the oracle's encryption of the GPU's encoded m
+    bit for bit; decrypt status 0, coeff = oracle decrypt, slots within tolerance."""
+    s = setup_for(Z, orc, name)
+    cfg = s.cfg
+    B = 12
+    z = slots_batch(cfg, 0, B)
+    zd = torch.from_numpy(z).cuda()
+    m_gpu = np64(Z.ckks_encode_batch(s.ctx, zd))
+    seed = cfg.enc_seed
+    if path == "zinc":
+        ct = Z.zinc_encrypt_batch(s.ctx, s.cache[form], form, zd, seed, 0)
+    else:
+        ct = Z.ckks_encrypt_batch(s.ctx, s.pk, form, zd, seed, 0)
+    got = np64(ct)
+    _check_msgs(orc, s, path, form, m_gpu, got, seed, 0, [0, 7, 11])
+    coeff, status, slots = Z.ckks_decrypt_batch(s.ctx, s.sk, form, ct)
+    assert (np64(status) == 0).all()
+    coeff = np64(coeff)
+    for b in (0, 7, 11):
+        x, st = orc.decrypt(s.P, s.o_sk_ntt, got[b], form)
+        assert st == 0 and np.array_equal(coeff[b], x)
+    err = np.max(np.abs(slots.cpu().numpy() - z))
+    assert err < cfg.tolerance(), err
+
+
+def test_decrypt_wrong_key_flags_crt(Z, orc):
+    s = setup_for(Z, orc, "C1")
+    z = torch.from_numpy(slots_batch(s.cfg, 0, 4)).cuda()
+    ct = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 1, 0)
+    other, _, _ = Z.zinc_keygen(s.ctx, 999)
+    _, status, _ = Z.ckks_decrypt_batch(s.ctx, other, COEFF, ct, slots=False)
+    assert (np64(status) == 1).all()
+
+
+def test_decode_matches_oracle(Z, orc):
+    s = setup_for(Z, orc, "C1")
+    z = torch.from_numpy(slots_batch(s.cfg, 3, 2)).cuda()
+    ct = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z, 4, 0)
+    coeff, status, slots = Z.ckks_decrypt_batch(s.ctx, s.sk, NTT, ct)
+    c = np64(coeff)
+    for b in range(2):
+        want = orc.decode(c[b], s.P.log_n, s.P.log_scale)
+        assert np.max(np.abs(slots[b].cpu().numpy() - want)) < 1e-9
+
+
+def test_forms_related_by_one_ntt(Z, orc):
+    s = setup_for(Z, orc, "C2")
+    m = dev_i64(int_plaintexts(s.cfg.log_n, 5, seed=3))
+    for path in ("zinc", "vanilla"):
+        if path == "zinc":
+            a = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, m, 9, 0)
+            b = Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, m, 9, 0)
+        else:
+            a = Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, m, 9, 0)
+            b = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, m, 9, 0)
+        Z.zinc_ntt_forward(s.ctx, a.view(-1, s.ctx.L, s.ctx.n))
+        assert torch.equal(a, b)
+
+
+def test_sharding_is_bit_identical(Z, orc):
+    """msg_base = global offset: two half-batches equal one batch (any P)."""
+    s = setup_for(Z, orc, "C2")
+    m = dev_i64(int_plaintexts(s.cfg.log_n, 40, seed=4))
+    for fn, key in ((Z.zinc_encrypt_batch, s.cache[COEFF]),):
+        full = fn(s.ctx, key, COEFF, m, 77, 500)
+        a = fn(s.ctx, key, COEFF, m[:13].contiguous(), 77, 500)
+        b = fn(s.ctx, key, COEFF, m[13:].contiguous(), 77, 513)
+        assert torch.equal(full, torch.cat([a, b]))
+    full = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, m, 77, 500)
+    a = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, m[:13].contiguous(), 77, 500)
+    b = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, m[13:].contiguous(), 77, 513)
+    assert torch.equal(full, torch.cat([a, b]))
+
+
+def test_batch_zero_and_bad_arguments(Z, orc):
+    s = setup_for(Z, orc, "C1")
+    m0 = torch.zeros((0, s.ctx.n), dtype=torch.int64, device="cuda")
+    Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, m0, 1, 0, out=s.ctx.empty_ct(0))  # no-op
+    m1 = torch.zeros((1, s.ctx.n), dtype=torch.int64, device="cuda")
+    with pytest.raises(Z.ZincError):
+        Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], 7, m1, 1)           # bad form
+    words = 2 * s.ctx.L * s.ctx.n
+    misaligned = torch.empty((words + 1,), dtype=torch.uint64, device="cuda")[1:]
+    with pytest.raises(Z.ZincError):
+        Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, m1, 1, out=misaligned)
+
+
+def test_host_buffer_api_matches_device_api(Z, orc):
+    s = setup_for(Z, orc, "C1")
+    z = slots_batch(s.cfg, 0, 50)
+    pt_h = torch.from_numpy(z).pin_memory()
+    ct_h = torch.empty((50, 2, s.ctx.L, s.ctx.n), dtype=torch.uint64).pin_memory()
+    Z.zinc_encrypt_batch_host(s.ctx, 0, s.cache[COEFF], COEFF, pt_h, 5, 0, ct_h, chunk=16)
+    dev = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, torch.from_numpy(z).cuda(), 5, 0)
+    assert torch.equal(ct_h, dev.cpu())
+    Z.zinc_encrypt_batch_host(s.ctx, 1, s.pk, NTT, pt_h, 5, 0, ct_h, chunk=7)
+    dev = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, torch.from_numpy(z).cuda(), 5, 0)
+    assert torch.equal(ct_h, dev.cpu())
+
+
+@pytest.mark.parametrize("path", ["zinc", "vanilla"])
+def test_full_size_c3_bench_launch_sampled(Z, orc, path):
+    """BASELINE C3 at full size (16384 messages, the bench's launch configuration):
+    sampled messages bit-exact against the oracle, from int64 plaintexts."""
+    s = setup_for(Z, orc, "C3")
+    B = s.cfg.batch
+    rng = np.random.default_rng(9)
+    m_d = torch.randint(-(1 << 45), 1 << 45, (B, s.ctx.n), dtype=torch.int64, device="cuda",
+                        generator=torch.Generator(device="cuda").manual_seed(9))
+    seed = s.cfg.enc_seed
+    if path == "zinc":
+        ct = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, m_d, seed, 0)
+    else:
+        ct = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, m_d, seed, 0)
+    torch.cuda.synchronize()
+    idx = sorted(set([0, B - 1] + rng.integers(0, B, 4).tolist()))
+    form = COEFF if path == "zinc" else NTT
+    m = {b: m_d[b].cpu().numpy() for b in idx}
+    got = {b: ct[b].cpu().numpy() for b in idx}
+    del ct
+    torch.cuda.empty_cache()
+    key = s.o_pk if path == "vanilla" else orc.precompute_cache(s.P, s.o_pk, s.cfg.cache_seed, form)
+    for b in idx:
+        if path == "vanilla":
+            want = orc.vanilla_encrypt(s.P, key, m[b], seed, b, form)
+        else:
+            want = orc.zinc_encrypt(s.P, key, form, m[b], seed, b)
+        assert np.array_equal(got[b], want), b
+
+
+def test_int_peak_kernel_runs(Z, orc):
+    s = setup_for(Z, orc, "C3")
+    sink = torch.zeros(2, dtype=torch.uint64, device="cuda")
+    bf = Z.zinc_int_peak(s.ctx, 148 * 4, 100, sink)
+    torch.cuda.synchronize()
+    assert bf == 148 * 4 * 256 * 8 * 100
