@@ -167,6 +167,29 @@ zinc_status zinc_encrypt_batch_host(const zinc_ctx *ctx, int path, const uint64_
                                     size_t batch, uint64_t seed, uint64_t msg_base,
                                     uint64_t *ct_host, size_t chunk);
 
+/* Kernel tracing.  Ids of the library's kernels: */
+enum {
+  ZINC_K_ZINC_COEFF = 0, /* Zinc add/inject, COEFF form          */
+  ZINC_K_ZINC_NTT = 1,   /* Zinc, NTT form                        */
+  ZINC_K_VANILLA = 2,    /* vanilla encryption (both forms)       */
+  ZINC_K_KEYGEN = 3,
+  ZINC_K_ENCODE = 4,
+  ZINC_K_DECRYPT = 5,
+  ZINC_K_DECODE = 6,
+  ZINC_K_NTT = 7,
+  ZINC_K_SAMPLE = 8,
+  ZINC_K_INT_PEAK = 9,
+  ZINC_K_COUNT = 10
+};
+/* on != 0: clear the trace and bracket every following kernel launch with CUDA
+ * events recorded on the launch's own stream; on == 0: stop recording. */
+zinc_status zinc_profile_enable(int on);
+/* Wait for the recorded events and return, per kernel id, the summed device
+ * time in ms and the launch count (host arrays of ZINC_K_COUNT). */
+zinc_status zinc_profile_read(double *ms, uint64_t *launches);
+/* Name of kernel id (static string, "?" if out of range). */
+const char *zinc_kernel_name(int id);
+
 /* Number of kernel launches this library issued since the last reset (all
  * threads); used by bench.py's gpu_launches claim. */
 uint64_t zinc_launch_count(void);

@@ -24,7 +24,7 @@ __all__ = [
     "zinc_keygen", "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch",
     "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
     "zinc_debug_sample", "zinc_int_peak", "zinc_encrypt_batch_host", "launch_count",
-    "launch_count_reset", "LIB_PATH", "EXPORTED_SYMBOLS",
+    "launch_count_reset", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
 ]
 
 NTT, COEFF = 0, 1
@@ -39,7 +39,10 @@ EXPORTED_SYMBOLS = (
     "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch", "ckks_decrypt_batch",
     "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse", "zinc_debug_sample", "zinc_int_peak",
     "zinc_encrypt_batch_host", "zinc_launch_count", "zinc_launch_count_reset", "zinc_last_error",
+    "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name",
 )
+KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
+                "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel")
 
 
 class ZincError(RuntimeError):
@@ -64,6 +67,8 @@ _SIGS = {
     "zinc_debug_sample": [_vp, _i32, _u64, _u64, _i32, _sz, _vp, _vp],
     "zinc_int_peak": [_vp, _i32, _i32, _vp, _c.POINTER(_c.c_double), _vp],
     "zinc_encrypt_batch_host": [_vp, _i32, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _sz],
+    "zinc_profile_enable": [_i32],
+    "zinc_profile_read": [_c.POINTER(_c.c_double), _c.POINTER(_u64)],
 }
 
 _lib = None
@@ -82,6 +87,8 @@ def lib() -> ctypes.CDLL:
             f.restype = _c.c_int
         L.zinc_last_error.restype = _c.c_char_p
         L.zinc_last_error.argtypes = []
+        L.zinc_kernel_name.restype = _c.c_char_p
+        L.zinc_kernel_name.argtypes = [_i32]
         L.zinc_launch_count.restype = _u64
         L.zinc_launch_count.argtypes = []
         L.zinc_launch_count_reset.restype = None
@@ -260,6 +267,20 @@ def zinc_encrypt_batch_host(ctx: Context, path: int, key: torch.Tensor, form: in
                                          pt_host.shape[0], seed, msg_base, _ptr(ct_host), chunk),
            "zinc_encrypt_batch_host")
     return ct_host
+
+
+def profile_enable(on: bool = True):
+    """Start (clear) / stop per-kernel CUDA-event tracing inside the library."""
+    _check(lib().zinc_profile_enable(1 if on else 0), "zinc_profile_enable")
+
+
+def profile_read() -> dict:
+    """{kernel name: (total device ms, launches)} since profile_enable(True)."""
+    n = len(KERNEL_NAMES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_uint64 * n)()
+    _check(lib().zinc_profile_read(ms, cnt), "zinc_profile_read")
+    return {KERNEL_NAMES[i]: (float(ms[i]), int(cnt[i])) for i in range(n) if cnt[i]}
 
 
 def launch_count() -> int:

@@ -38,9 +38,55 @@ static zinc_status fail(zinc_status s, const char *fmt, ...) {
     if (_e != cudaSuccess)                                                           \
       return fail(ZINC_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));      \
   } while (0)
-#define LAUNCH(expr)                                                                 \
+// ------------------------------------------------------------------ tracing
+// When enabled, every launch is bracketed by two CUDA events on its stream.
+struct TraceRec { int id; cudaEvent_t a, b; };
+static std::mutex g_trace_mu;
+static std::atomic<int> g_trace_on{0};
+static std::vector<TraceRec> g_trace;
+static std::vector<cudaEvent_t> g_event_pool;
+static double g_trace_ms[ZINC_K_COUNT];
+static uint64_t g_trace_n[ZINC_K_COUNT];
+static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel",
+                                                 "keygen_kernel", "encode_kernel", "decrypt_kernel",
+                                                 "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel"};
+static cudaEvent_t pool_event() {
+  cudaEvent_t e = nullptr;
+  if (!g_event_pool.empty()) {
+    e = g_event_pool.back();
+    g_event_pool.pop_back();
+  } else {
+    cudaEventCreate(&e);
+  }
+  return e;
+}
+struct TraceScope {
+  int id;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  TraceScope(int id_, cudaStream_t s_) : id(id_), s(s_) {
+    if (g_trace_on.load(std::memory_order_relaxed)) {
+      std::lock_guard<std::mutex> l(g_trace_mu);
+      a = pool_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~TraceScope() {
+    if (a) {
+      std::lock_guard<std::mutex> l(g_trace_mu);
+      cudaEvent_t b = pool_event();
+      cudaEventRecord(b, s);
+      g_trace.push_back({id, a, b});
+    }
+  }
+};
+#define LAUNCH(id, stream, expr)                                                     \
   do {                                                                               \
-    cudaError_t _e = (expr);                                                         \
+    cudaError_t _e;                                                                  \
+    {                                                                                \
+      TraceScope _ts((id), (stream));                                                \
+      _e = (expr);                                                                   \
+    }                                                                                \
     g_launches.fetch_add(1, std::memory_order_relaxed);                              \
     if (_e != cudaSuccess)                                                           \
       return fail(ZINC_ECUDA, "launch %s failed: %s", #expr, cudaGetErrorString(_e)); \
@@ -142,6 +188,38 @@ static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 extern "C" {
 
 const char *zinc_last_error(void) { return g_err.c_str(); }
+
+const char *zinc_kernel_name(int id) { return (id >= 0 && id < ZINC_K_COUNT) ? kKernelNames[id] : "?"; }
+
+zinc_status zinc_profile_enable(int on) {
+  std::lock_guard<std::mutex> l(g_trace_mu);
+  if (on) {
+    for (auto &r : g_trace) { g_event_pool.push_back(r.a); g_event_pool.push_back(r.b); }
+    g_trace.clear();
+    for (int i = 0; i < ZINC_K_COUNT; ++i) { g_trace_ms[i] = 0; g_trace_n[i] = 0; }
+  }
+  g_trace_on.store(on ? 1 : 0);
+  return ZINC_OK;
+}
+
+zinc_status zinc_profile_read(double *ms, uint64_t *launches) {
+  std::lock_guard<std::mutex> l(g_trace_mu);
+  for (auto &r : g_trace) {
+    float t = 0;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+      return fail(ZINC_ECUDA, "trace event query failed");
+    g_trace_ms[r.id] += t;
+    g_trace_n[r.id] += 1;
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_trace.clear();
+  for (int i = 0; i < ZINC_K_COUNT; ++i) {
+    if (ms) ms[i] = g_trace_ms[i];
+    if (launches) launches[i] = g_trace_n[i];
+  }
+  return ZINC_OK;
+}
 uint64_t zinc_launch_count(void) { return g_launches.load(); }
 void zinc_launch_count_reset(void) { g_launches.store(0); }
 
@@ -291,7 +369,7 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
   a.twist = c->d_twist;
   a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
   a.m_out = m;
-  LAUNCH(launch_encode(c->log_n, a, batch, s));
+  LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
 
@@ -324,7 +402,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     size_t gy = std::max<size_t>(1, (target + gx - 1) / gx);
     a.msgs_per_cta = (batch + gy - 1) / gy;
     gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
-    LAUNCH(launch_zinc_coeff(a, threads, (int)gy, s));
+    LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, s));
     return ZINC_OK;
   }
   const int lpc = limbs_per_cta(c, batch);
@@ -340,7 +418,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
-    LAUNCH(launch_zinc_ntt(c->log_n, a, batch, groups, s));
+    LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, batch, groups, s));
     return ZINC_OK;
   }
   VanillaArgs a{};
@@ -354,7 +432,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
-  LAUNCH(launch_vanilla(c->log_n, a, form, batch, groups, s));
+  LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, batch, groups, s));
   return ZINC_OK;
 }
 
@@ -406,7 +484,7 @@ zinc_status zinc_keygen(const zinc_ctx *c, uint64_t seed, uint64_t *sk_ntt, int8
   a.sk_coeff = sk_coeff;
   a.seed = seed;
   a.L = c->L;
-  LAUNCH(launch_keygen(c->log_n, a, (cudaStream_t)stream));
+  LAUNCH(ZINC_K_KEYGEN, (cudaStream_t)stream, launch_keygen(c->log_n, a, (cudaStream_t)stream));
   return ZINC_OK;
 }
 
@@ -462,7 +540,11 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
   a.L = c->L;
   st = ZINC_OK;
   {
-    cudaError_t e = launch_decrypt(c->log_n, a, form, batch, s);
+    cudaError_t e;
+    {
+      TraceScope ts(ZINC_K_DECRYPT, s);
+      e = launch_decrypt(c->log_n, a, form, batch, s);
+    }
     g_launches.fetch_add(1);
     if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decrypt launch: %s", cudaGetErrorString(e));
   }
@@ -474,7 +556,11 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
     d.twist = c->d_twist;
     d.inv_scale = ldexp(1.0, -c->log_scale);
     d.slots_out = slots_out;
-    cudaError_t e = launch_decode(c->log_n, d, batch, s);
+    cudaError_t e;
+    {
+      TraceScope ts(ZINC_K_DECODE, s);
+      e = launch_decode(c->log_n, d, batch, s);
+    }
     g_launches.fetch_add(1);
     if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decode launch: %s", cudaGetErrorString(e));
   }
@@ -505,7 +591,7 @@ static zinc_status ntt_dir(const zinc_ctx *c, uint64_t *data, size_t count, int 
   a.itw = c->d_itw;
   a.data = data;
   a.L = c->L;
-  LAUNCH(launch_ntt(c->log_n, a, inv, count * c->L, (cudaStream_t)stream));
+  LAUNCH(ZINC_K_NTT, (cudaStream_t)stream, launch_ntt(c->log_n, a, inv, count * c->L, (cudaStream_t)stream));
   return ZINC_OK;
 }
 zinc_status zinc_ntt_forward(const zinc_ctx *c, uint64_t *data, size_t count, zinc_stream_t stream) {
@@ -532,7 +618,7 @@ zinc_status zinc_debug_sample(const zinc_ctx *c, int tag, uint64_t seed, uint64_
   a.q = c->q[limb];
   a.n = n;
   a.out = out;
-  LAUNCH(launch_sample(a, (cudaStream_t)stream));
+  LAUNCH(ZINC_K_SAMPLE, (cudaStream_t)stream, launch_sample(a, (cudaStream_t)stream));
   return ZINC_OK;
 }
 
@@ -549,7 +635,7 @@ zinc_status zinc_int_peak(const zinc_ctx *c, int blocks, int iters, uint64_t *si
   a.wp = shoup(c->psi[0], c->q[0]);
   a.iters = iters;
   a.sink = sink;
-  LAUNCH(launch_int_peak(a, blocks, (cudaStream_t)stream));
+  LAUNCH(ZINC_K_INT_PEAK, (cudaStream_t)stream, launch_int_peak(a, blocks, (cudaStream_t)stream));
   if (butterflies) *butterflies = (double)blocks * 256.0 * 8.0 * (double)iters;
   return ZINC_OK;
 }

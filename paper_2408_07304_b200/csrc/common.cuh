@@ -63,6 +63,15 @@ ZINC_DEV uint64_t reduce_i64q(int64_t v, uint64_t q, uint64_t mu) {
   return (v < 0 && r != 0) ? q - r : r;
 }
 ZINC_DEV uint64_t reduce_i64(int64_t v, const LimbConst &c) { return reduce_i64q(v, c.q, c.mu64); }
+// Residue of m + e for an int64 plaintext coefficient m and a small error e,
+// exact even when m + e overflows int64 (then both are reduced separately).
+ZINC_DEV uint64_t reduce_m_plus_e(int64_t m, int e, uint64_t q, uint64_t mu) {
+  const int64_t v = (int64_t)((uint64_t)m + (uint64_t)(int64_t)e);
+  const bool ovf = ((m ^ v) & ((int64_t)e ^ v)) < 0;
+  if (!ovf) return reduce_i64q(v, q, mu);
+  const uint64_t r = reduce_i64q(m, q, mu), f = e < 0 ? (uint64_t)((int64_t)q + e) : (uint64_t)e;
+  return csub(r + f, q);
+}
 // Residue of a small signed value |v| < q.
 ZINC_DEV uint64_t reduce_small(int64_t v, uint64_t q) {
   return v < 0 ? (uint64_t)(v + (int64_t)q) : (uint64_t)v;

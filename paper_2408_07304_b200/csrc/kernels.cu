@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
       ulonglong2 mv = ld2_nc(a.m + b * a.n + j);
       m0 = (int64_t)mv.x; m1 = (int64_t)mv.y;
     }
-    const int64_t v0 = m0 + cbd_lo(w1), v1 = m1 + cbd_hi(w1);
+    const int e0 = cbd_lo(w1), e1 = cbd_hi(w1);
     const int f0 = cbd_lo(w2), f1 = cbd_hi(w2);
     uint64_t *out = a.ct + b * 2 * lnn + j;
 #pragma unroll 4
@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
       uint64_t z10, z11, z20, z21;
       ld2(tile + (size_t)i * T + jl, z10, z11);
       ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-      const uint64_t c10 = add_mod(z10, reduce_i64q(v0, q, mu), q);
-      const uint64_t c11 = add_mod(z11, reduce_i64q(v1, q, mu), q);
+      const uint64_t c10 = add_mod(z10, reduce_m_plus_e(m0, e0, q, mu), q);
+      const uint64_t c11 = add_mod(z11, reduce_m_plus_e(m1, e1, q, mu), q);
       const uint64_t c20 = add_mod(z20, reduce_small(f0, q), q);
       const uint64_t c21 = add_mod(z21, reduce_small(f1, q), q);
       st2_cs(out + (size_t)i * a.n, c10, c11);
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(Plan<LOGN>::THREADS) vanilla_kernel(VanillaArg
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if (FORM == 0) {
       ntt_forward<LOGN>(sm, tw, q,
-          [&](int x) { return reduce_i64((int64_t)se1[x] + (m ? m[x] : 0), c); },
+          [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; r += 2) st2(ct0 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(Plan<LOGN>::THREADS) vanilla_kernel(VanillaArg
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base + r)];
           },
           [&](int x, uint64_t v) {
-            uint64_t e = reduce_i64((int64_t)se1[x] + (m ? m[x] : 0), c);
+            uint64_t e = reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64);
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
           });
       ntt_inverse<LOGN>(sm, itw, c,
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(Plan<LOGN>::THREADS) zinc_ntt_kernel(ZincNttAr
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     ntt_forward<LOGN>(sm, tw, q,
-        [&](int x) { return reduce_i64((int64_t)se1[x] + (m ? m[x] : 0), c); },
+        [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
           for (int r = 0; r < 16; r += 2) {
