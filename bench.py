@@ -222,6 +222,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2408_07304_b200 as Z
+    from paper_2408_07304_b200.dist import broadcast_words, max_over_ranks
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -243,8 +244,7 @@ def main():
     bcast_ok = True
     if world > 1:
         torch.cuda.synchronize()
-        for t in (pk, cache[Z.COEFF], cache[Z.NTT]):
-            dist.broadcast(t.view(torch.int64), src=0)
+        broadcast_words([pk, cache[Z.COEFF], cache[Z.NTT]], src=0)
         torch.cuda.synchronize()
         bcast_ok = all(torch.equal(a, b) for a, b in ((pk, pk_local), (cache[0], cache_local[0]),
                                                        (cache[1], cache_local[1])))
@@ -325,10 +325,7 @@ def main():
     clk = clocks.stop()
 
     seg = {p: sum(a.elapsed_time(b) for a, b in ev[p]) / args.steps for p in paths}  # ms per step per path
-    seg_t = torch.tensor([seg[p] for p in paths], dtype=torch.float64, device=ctx.dev())
-    if world > 1:
-        dist.all_reduce(seg_t, op=dist.ReduceOp.MAX)
-    seg = {p: float(v) for p, v in zip(paths, seg_t.tolist())}
+    seg = dict(zip(paths, max_over_ranks([seg[p] for p in paths], device=ctx.dev())))
     total_msgs = B * world
     path_out = {p: {"ct_per_s": total_msgs / (seg[p] / 1e3), "ms": seg[p]} for p in paths}
 
@@ -408,11 +405,9 @@ def main():
             t0 = time.perf_counter()
             Z.zinc_encrypt_batch_host(ctx, 0, cache[Z.COEFF], Z.COEFF, pt_h, cfg.enc_seed, base, ct_h)
             ts.append(time.perf_counter() - t0)
-        tt = torch.tensor([min(ts)], dtype=torch.float64, device=ctx.dev())
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tt = max_over_ranks([min(ts)], device=ctx.dev())[0]
         if rank == 0:
-            result["e2e"] = {"value": Be * world / float(tt.item()), "unit": UNIT,
+            result["e2e"] = {"value": Be * world / tt, "unit": UNIT,
                              "h2d_bytes_per_step": int(pt_h.numel() * 8), "d2h_bytes_per_step": int(ct_h.numel() * 8),
                              "batch_per_gpu": Be, "api": "zinc_encrypt_batch_host (pinned host in/out, 2 streams)",
                              "path": "zinc_coeff", "timer": "host perf_counter around the blocking call, best of "
