@@ -163,6 +163,11 @@ class Context:
         return torch.empty((2, self.L, self.n), dtype=torch.uint64, device=self.dev())
 
 
+def _as_pt(pt: torch.Tensor) -> torch.Tensor:
+    """complex128 slots [B, N/2] travel as their float64 (re, im) view [B, N/2, 2]."""
+    return torch.view_as_real(pt) if pt.is_complex() else pt
+
+
 def _kind_of(pt: torch.Tensor) -> int:
     if pt.dtype == torch.int64:
         return PT_COEFF_I64
@@ -191,6 +196,7 @@ def zinc_precompute_cache(ctx: Context, pk_ntt: torch.Tensor, seed: int, form: i
 def zinc_encrypt_batch(ctx: Context, cache: torch.Tensor, form: int, pt: torch.Tensor, seed: int,
                        msg_base: int = 0, out=None, stream=None):
     """Enc_z (Algorithm 1) of a batch of plaintexts (int64 [B,N] or slots). Returns [B,2,L,N] u64."""
+    pt = _as_pt(pt)
     b = pt.shape[0]
     ct = ctx.empty_ct(b) if out is None else out
     _check(lib().zinc_encrypt_batch(ctx.handle, _ptr(cache), form, _kind_of(pt), _ptr(pt), b, seed, msg_base,
@@ -201,6 +207,7 @@ def zinc_encrypt_batch(ctx: Context, cache: torch.Tensor, form: int, pt: torch.T
 def ckks_encrypt_batch(ctx: Context, pk_ntt: torch.Tensor, form: int, pt: torch.Tensor, seed: int,
                        msg_base: int = 0, out=None, stream=None):
     """Vanilla Enc (Eq. 8, reading A1) of a batch. Returns [B,2,L,N] u64."""
+    pt = _as_pt(pt)
     b = pt.shape[0]
     ct = ctx.empty_ct(b) if out is None else out
     _check(lib().ckks_encrypt_batch(ctx.handle, _ptr(pk_ntt), form, _kind_of(pt), _ptr(pt), b, seed, msg_base,
@@ -223,6 +230,7 @@ def ckks_decrypt_batch(ctx: Context, sk_ntt: torch.Tensor, form: int, ct: torch.
 
 def ckks_encode_batch(ctx: Context, slots: torch.Tensor, out=None, stream=None):
     """Encode slots (C-6). Returns int64 [B,N]."""
+    slots = _as_pt(slots)
     b = slots.shape[0]
     m = torch.empty((b, ctx.n), dtype=torch.int64, device=ctx.dev()) if out is None else out
     _check(lib().ckks_encode_batch(ctx.handle, _kind_of(slots), _ptr(slots), b, _ptr(m), _stream(stream)),
@@ -261,6 +269,7 @@ def zinc_int_peak(ctx: Context, blocks: int, iters: int, sink: torch.Tensor, str
 def zinc_encrypt_batch_host(ctx: Context, path: int, key: torch.Tensor, form: int, pt_host: torch.Tensor,
                             seed: int, msg_base: int, ct_host: torch.Tensor, chunk: int = 256):
     """Host-buffer (end-to-end) encryption: pt_host / ct_host are CPU tensors (pinned for speed)."""
+    pt_host = _as_pt(pt_host)
     if pt_host.is_cuda or ct_host.is_cuda:
         raise ZincError("zinc_encrypt_batch_host takes host tensors")
     _check(lib().zinc_encrypt_batch_host(ctx.handle, path, _ptr(key), form, _kind_of(pt_host), _ptr(pt_host),

@@ -251,7 +251,6 @@ zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scal
   for (int i = 0; i < L; ++i)
     if (limb_bits[i] < 20 || limb_bits[i] > 60)
       return fail(ZINC_EINVAL, "limb %d: %d bits outside [20, 60]", i, limb_bits[i]);
-  if (log_n == 15) return fail(ZINC_EUNSUPPORTED, "N = 2^15 is not implemented yet");
   zinc_ctx *c = new zinc_ctx();
   c->device = device;
   c->log_n = log_n;

@@ -1,0 +1,138 @@
+// k_fft.cu -- CKKS encode (C-6) and decode (C-10): FP64 FFT kernels.
+#include "kcommon.cuh"
+
+namespace zinc {
+
+// ============================================================ encode (C-6)
+// One CTA per message (M = N/2 <= 2^13 complex points in smem), or, at
+// M = 2^14 (N = 2^15), a 2-CTA cluster: CTA r gathers the slots whose
+// bit-reversed position lies in half r, runs the first LOGM-1 DIT stages on
+// its M/2 points, and the last stage (pairs x, x + M/2 with W_M^x) reads both
+// halves over distributed shared memory; CTA r finishes x in [r M/4, (r+1) M/4).
+template <int LOGM>
+__global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS) encode_kernel(EncodeArgs a) {
+  constexpr bool SPLIT = LOGM > 13;
+  constexpr int LL = SPLIT ? LOGM - 1 : LOGM;
+  constexpr int M = 1 << LOGM, ML = 1 << LL;
+  constexpr int TWS = SPLIT ? 2 : 1;
+  using P = FftPlan<LL>;
+  extern __shared__ __align__(16) double2 buf[];
+  const size_t b = blockIdx.x / (SPLIT ? 2 : 1);
+  const int r = SPLIT ? (int)cluster_rank() : 0;
+  for (int k = threadIdx.x; k < M; k += P::THREADS) {
+    const int pos = a.perm[k] - r * ML;
+    if (SPLIT && (unsigned)pos >= (unsigned)ML) continue;
+    double2 z;
+    if (a.complex_slots) {
+      z = reinterpret_cast<const double2 *>(a.slots)[b * M + k];
+    } else {
+      z = make_double2(a.slots[b * M + k], 0.0);
+    }
+    buf[pad16(pos)] = z;
+  }
+  __syncthreads();
+  auto lds = [&](int i) { return buf[pad16(i)]; };
+  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
+  fft_pass<LL, 0, P::K1, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+  __syncthreads();
+  fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+  __syncthreads();
+  int64_t *m = a.m_out + b * (2 * M);
+  const double scale = a.scale;  // Delta / M, a power of two
+  auto emit = [&](int j, double2 v) {
+    const double2 w = cmul(v, __ldg(a.twist + j));
+    m[j] = llround(w.x * scale);
+    m[j + M] = llround(w.y * scale);
+  };
+  if constexpr (!SPLIT) {
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false>(a.fft_tw, lds, emit);
+  } else {
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+    cluster_sync_all();
+    const double2 *h0 = peer_smem(buf, 0), *h1 = peer_smem(buf, 1);
+    for (int x = r * (ML / 2) + threadIdx.x; x < (r + 1) * (ML / 2); x += P::THREADS) {
+      const double2 u = h0[pad16(x)];
+      const double2 t = cmul(h1[pad16(x)], __ldg(a.fft_tw + x));
+      emit(x, cadd(u, t));
+      emit(x + ML, csubd(u, t));
+    }
+    cluster_sync_all();
+  }
+}
+
+// ============================================================ decode (C-10)
+// Mirror image of encode.  Split at M = 2^14: the first DIF stage (pairs j,
+// j + M/2) is computed by each CTA for its half straight from the global
+// coefficients; the remaining stages are an independent M/2-point transform
+// whose bit-reversed outputs are positions [r M/2, (r+1) M/2).
+template <int LOGM>
+__global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS) decode_kernel(DecodeArgs a) {
+  constexpr bool SPLIT = LOGM > 13;
+  constexpr int LL = SPLIT ? LOGM - 1 : LOGM;
+  constexpr int M = 1 << LOGM, ML = 1 << LL;
+  constexpr int TWS = SPLIT ? 2 : 1;
+  using P = FftPlan<LL>;
+  extern __shared__ __align__(16) double2 buf[];
+  const size_t b = blockIdx.x / (SPLIT ? 2 : 1);
+  const int r = SPLIT ? (int)cluster_rank() : 0;
+  const int64_t *x = a.coeff + b * (2 * M);
+  auto lds = [&](int i) { return buf[pad16(i)]; };
+  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
+  auto twisted = [&](int j) {
+    const double2 v = make_double2((double)x[j], (double)x[j + M]);
+    return cmul(v, conj2(__ldg(a.twist + j)));
+  };
+  if constexpr (!SPLIT) {
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, false, true>(a.fft_tw, twisted, sts);
+  } else {
+    for (int j = threadIdx.x; j < ML; j += P::THREADS) {
+      const double2 u = twisted(j), v = twisted(j + ML);
+      buf[pad16(j)] = r == 0 ? cadd(u, v) : cmul(csubd(u, v), conj2(__ldg(a.fft_tw + j)));
+    }
+    __syncthreads();
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, false, true, TWS>(a.fft_tw, lds, sts);
+  }
+  __syncthreads();
+  fft_pass<LL, P::K1, P::K2, P::THREADS, false, true, TWS>(a.fft_tw, lds, sts);
+  __syncthreads();
+  fft_pass<LL, 0, P::K1, P::THREADS, false, true, TWS>(a.fft_tw, lds, sts);
+  __syncthreads();
+  double2 *out = reinterpret_cast<double2 *>(a.slots_out) + b * M;
+  for (int k = threadIdx.x; k < M; k += P::THREADS) {
+    const int pos = a.perm[k] - r * ML;
+    if (SPLIT && (unsigned)pos >= (unsigned)ML) continue;
+    const double2 v = buf[pad16(pos)];
+    out[k] = make_double2(v.x * a.inv_scale, v.y * a.inv_scale);
+  }
+}
+
+template <int LOGM> static size_t fft_smem() {
+  constexpr int LL = LOGM > 13 ? LOGM - 1 : LOGM;
+  return ((1 << LL) + ((1 << LL) >> 4)) * sizeof(double2);
+}
+template <int LOGM>
+static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
+  constexpr int C = LOGM > 13 ? 2 : 1;
+  return launch_ex(encode_kernel<LOGM>, dim3((unsigned)(batch * C)), FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
+                   fft_smem<LOGM>(), C, s, a);
+}
+cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s) {
+#define CALL(K) launch_encode_t<K - 1>(a, batch, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+template <int LOGM>
+static cudaError_t launch_decode_t(const DecodeArgs &a, size_t batch, cudaStream_t s) {
+  constexpr int C = LOGM > 13 ? 2 : 1;
+  return launch_ex(decode_kernel<LOGM>, dim3((unsigned)(batch * C)), FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
+                   fft_smem<LOGM>(), C, s, a);
+}
+cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s) {
+#define CALL(K) launch_decode_t<K - 1>(a, batch, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+
+}  // namespace zinc

@@ -1,0 +1,240 @@
+// k_ntt.cu -- Zinc NTT form, keygen (Eq. 7), decrypt (Eq. 10) and the standalone NTT / INTT.
+#include "kcommon.cuh"
+
+namespace zinc {
+
+// ============================================================ Zinc, NTT form
+// c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2') (two DFTs,
+// no multiplication).
+template <int LOGN>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArgs a) {
+  using G = Geo<LOGN>;
+  constexpr int N = 1 << LOGN;
+  constexpr int THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  int8_t *se1 = reinterpret_cast<int8_t *>(sm + SmemWords<G::LOGL>::value);
+  int8_t *se2 = se1 + N;
+  const size_t b = blockIdx.x / G::CLUSTER;
+  const uint64_t msg = a.msg_base + b;
+  sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ZINC_E1);
+  sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2);
+  __syncthreads();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    const uint64_t *z1 = a.cache + (size_t)i * N, *z2 = a.cache + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    ntt_forward<LOGN>(sm, tw, q,
+        [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            uint64_t za, zb;
+            ld2(z1 + base + r, za, zb);
+            st2_cs(ct0 + base + r, add_mod(za, canon4(v[r], q, two_q), q), add_mod(zb, canon4(v[r + 1], q, two_q), q));
+          }
+        });
+    ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); },
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; r += 2) {
+            uint64_t za, zb;
+            ld2(z2 + base + r, za, zb);
+            st2_cs(ct1 + base + r, add_mod(za, canon4(v[r], q, two_q), q), add_mod(zb, canon4(v[r + 1], q, two_q), q));
+          }
+        });
+  }
+}
+
+// ============================================================ keygen (Eq. 7)
+// One CTA per limb: a <- U(R_qi) (tag PK_A, limb i), s <- R_2 (SK), e <- chi (PK_E);
+// pk2 = a^, sk = s^, pk1 = -a^ s^ + e^ (NTT domain; C-5).
+template <int LOGN>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS) keygen_kernel(KeygenArgs a) {
+  using G = Geo<LOGN>;
+  constexpr int N = 1 << LOGN;
+  constexpr int THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  int8_t *ss = reinterpret_cast<int8_t *>(sm + SmemWords<G::LOGL>::value);
+  int8_t *se = ss + N;
+  sample_ternary_smem<THREADS>(ss, N, a.seed, 0, TAG_SK);
+  sample_cbd_smem<THREADS>(se, N, a.seed, 0, TAG_PK_E);
+  __syncthreads();
+  const int i = blockIdx.x / G::CLUSTER, L = a.L;
+  if (i == 0 && local_off<LOGN>() == 0 && a.sk_coeff)
+    for (int x = threadIdx.x; x < N; x += THREADS) a.sk_coeff[x] = ss[x];
+  const LimbConst c = a.limbs[i];
+  const uint64_t q = c.q, two_q = c.two_q;
+  const Tw *tw = a.tw + (size_t)i * N;
+  uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+  uint64_t *sk = a.sk_ntt + (size_t)i * N;
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return uniform_mod(stream_block(a.seed, 0, TAG_PK_A, i, x), q); },
+      [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) pk2[base + r] = canon4(v[r], q, two_q);
+      });
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(ss[x], q); },
+      [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sk[base + r] = canon4(v[r], q, two_q);
+      });
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se[x], q); },
+      [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          uint64_t as = mul_mod(pk2[base + r], sk[base + r], c);
+          pk1[base + r] = add_mod(q - as == q ? 0 : q - as, canon4(v[r], q, two_q), q);
+        }
+      });
+}
+
+// ============================================================ decrypt (Eq. 10)
+// One CTA per message, limbs in order 0..L-1: x^(i) = [c1 + c2 s]_{q_i} (an INTT,
+// plus an NTT of c2 in COEFF form).  Limb 0 writes x0 = centred residue mod q_0
+// to coeff_out; every other limb checks x0 mod q_i == x^(i) (C-10).
+template <int LOGN, int FORM>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs a) {
+  using G = Geo<LOGN>;
+  constexpr int N = 1 << LOGN;
+  extern __shared__ __align__(16) uint64_t sm[];
+  __shared__ int bad_flag;
+  const size_t b = blockIdx.x / G::CLUSTER;
+  const int loff = local_off<LOGN>();
+  const int L = a.L;
+  int bad = 0;
+  int64_t *x0 = a.coeff_out + b * N;
+  const uint64_t q0 = a.limbs[0].q;
+  for (int i = 0; i < L; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t *c1 = a.ct + b * 2 * L * N + (size_t)i * N;
+    const uint64_t *c2 = c1 + (size_t)L * N;
+    const uint64_t *s = a.sk_ntt + (size_t)i * N;
+    const Tw *itw = a.itw + (size_t)i * N;
+    auto epilogue = [&](int x, uint64_t v) {
+      uint64_t xi = csub(v, q);
+      if (FORM == 1) xi = add_mod(xi, c1[x], q);
+      if (i == 0) {
+        x0[x] = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
+      } else {
+        if (reduce_i64(x0[x], c) != xi) bad = 1;
+      }
+    };
+    if (FORM == 0) {
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = add_mod(c1[base + r], mul_mod(c2[base + r], s[base + r], c), q);
+          },
+          epilogue);
+    } else {
+      const Tw *tw = a.tw + (size_t)i * N;
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return c2[x]; },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon4(v[r], q, two_q), s[base + r], c);
+          });
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
+          },
+          epilogue);
+    }
+  }
+  bad = __syncthreads_or(bad);
+  if constexpr (G::SPLIT) {
+    // the pair's verdict: rank 1 publishes its flag, rank 0 reads it over DSMEM
+    if (threadIdx.x == 0) bad_flag = bad;
+    cluster_sync_all();
+    if (threadIdx.x == 0 && loff == 0 && a.status_out) a.status_out[b] = bad | *peer_smem(&bad_flag, 1);
+    cluster_sync_all();
+  } else {
+    if (threadIdx.x == 0 && a.status_out) a.status_out[b] = bad;
+  }
+}
+
+// ============================================================ standalone NTT
+template <int LOGN, int INV>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS) ntt_kernel(NttArgs a) {
+  constexpr int N = 1 << LOGN;
+  extern __shared__ __align__(16) uint64_t sm[];
+  const size_t poly = blockIdx.x / Geo<LOGN>::CLUSTER;
+  const int i = (int)(poly % a.L);
+  uint64_t *p = a.data + poly * N;
+  const LimbConst c = a.limbs[i];
+  const uint64_t q = c.q, two_q = c.two_q;
+  if (INV == 0) {
+    ntt_forward<LOGN>(sm, a.tw + (size_t)i * N, q, [&](int x) { return p[x]; },
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) p[base + r] = canon4(v[r], q, two_q);
+        });
+  } else {
+    ntt_inverse<LOGN>(sm, a.itw + (size_t)i * N, c,
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int r = 0; r < 16; ++r) v[r] = p[base + r];
+        },
+        [&](int x, uint64_t v) { p[x] = csub(v, q); });
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
+  using G = Geo<LOGN>;
+  const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN);
+  return launch_ex(zinc_ntt_kernel<LOGN>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
+}
+cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
+#define CALL(K) launch_zinc_ntt_t<K>(a, batch, groups, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+template <int LOGN>
+static cudaError_t launch_keygen_t(const KeygenArgs &a, cudaStream_t s) {
+  using G = Geo<LOGN>;
+  const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN);
+  return launch_ex(keygen_kernel<LOGN>, msg_grid<LOGN>(a.L), G::THREADS, smem, G::CLUSTER, s, a);
+}
+cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s) {
+#define CALL(K) launch_keygen_t<K>(a, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+template <int LOGN>
+static cudaError_t launch_decrypt_t(const DecryptArgs &a, int form, size_t batch, cudaStream_t s) {
+  using G = Geo<LOGN>;
+  const size_t smem = ntt_smem_bytes<LOGN>();
+  if (form == 0) return launch_ex(decrypt_kernel<LOGN, 0>, msg_grid<LOGN>(batch), G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(decrypt_kernel<LOGN, 1>, msg_grid<LOGN>(batch), G::THREADS, smem, G::CLUSTER, s, a);
+}
+cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s) {
+#define CALL(K) launch_decrypt_t<K>(a, form, batch, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+template <int LOGN>
+static cudaError_t launch_ntt_t(const NttArgs &a, int inv, size_t polys, cudaStream_t s) {
+  using G = Geo<LOGN>;
+  const size_t smem = ntt_smem_bytes<LOGN>();
+  if (inv == 0) return launch_ex(ntt_kernel<LOGN, 0>, msg_grid<LOGN>(polys), G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(ntt_kernel<LOGN, 1>, msg_grid<LOGN>(polys), G::THREADS, smem, G::CLUSTER, s, a);
+}
+cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s) {
+#define CALL(K) launch_ntt_t<K>(a, inv, polys, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+
+}  // namespace zinc

@@ -1,0 +1,140 @@
+// k_stream.cu -- Zinc add/inject (COEFF form), the debug sampler and the integer-peak microkernel.
+#include "kcommon.cuh"
+
+namespace zinc {
+
+// ============================================================ Zinc, COEFF form
+// Algorithm 1 with cache and output in coefficient form:
+//   c1'[i][j] = [zero1[i][j] + m[j] + e1'[j]]_{q_i},  c2'[i][j] = [zero2[i][j] + e2'[j]]_{q_i}.
+// CTA (x, y): coefficient tile [x*T, (x+1)*T), messages [y*mpc, (y+1)*mpc).  The
+// cache tile [2][L][T] is staged once into shared memory with bulk async copies
+// (cp.async.bulk, the 1-D TMA path, completing on an mbarrier) and reused for
+// every message; each thread owns 2 coefficients, draws e1'/e2' with one Philox
+// call each (C-4 block = j/2), and streams 2L 16-byte stores per message.
+__global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
+  extern __shared__ __align__(16) uint64_t tile[];  // [2][L][T], then q[L], mu64[L]
+  __shared__ __align__(8) uint64_t mbar;
+  const int T = 2 * blockDim.x;
+  const int L = a.L;
+  const int j0 = blockIdx.x * T;
+  uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    sq[i] = a.limbs[i].q;
+    smu[i] = a.limbs[i].mu64;
+  }
+  if (threadIdx.x == 0) {
+    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    const uint32_t bytes = (uint32_t)(T * sizeof(uint64_t));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes * 2 * L) : "memory");
+    for (int r = 0; r < 2 * L; ++r) {
+      const uint64_t *src = a.cache + (size_t)r * a.n + j0;
+      uint32_t dst = (uint32_t)__cvta_generic_to_shared(tile + (size_t)r * T);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
+    }
+  }
+  {
+    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(mb) : "memory");
+    }
+  }
+  const int jl = 2 * threadIdx.x;       // local coefficient pair
+  const int j = j0 + jl;
+  const size_t b_begin = (size_t)blockIdx.y * a.msgs_per_cta;
+  size_t b_end = b_begin + a.msgs_per_cta;
+  if (b_end > a.batch) b_end = a.batch;
+  const size_t lnn = (size_t)L * a.n;
+  for (size_t b = b_begin; b < b_end; ++b) {
+    const uint64_t msg = a.msg_base + b;
+    const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
+    const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
+    int64_t m0 = 0, m1 = 0;
+    if (a.m) {
+      ulonglong2 mv = ld2_nc(a.m + b * a.n + j);
+      m0 = (int64_t)mv.x; m1 = (int64_t)mv.y;
+    }
+    const int e0 = cbd_lo(w1), e1 = cbd_hi(w1);
+    const int f0 = cbd_lo(w2), f1 = cbd_hi(w2);
+    uint64_t *out = a.ct + b * 2 * lnn + j;
+#pragma unroll 4
+    for (int i = 0; i < L; ++i) {
+      const uint64_t q = sq[i], mu = smu[i];
+      uint64_t z10, z11, z20, z21;
+      ld2(tile + (size_t)i * T + jl, z10, z11);
+      ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+      const uint64_t c10 = add_mod(z10, reduce_m_plus_e(m0, e0, q, mu), q);
+      const uint64_t c11 = add_mod(z11, reduce_m_plus_e(m1, e1, q, mu), q);
+      const uint64_t c20 = add_mod(z20, reduce_small(f0, q), q);
+      const uint64_t c21 = add_mod(z21, reduce_small(f1, q), q);
+      st2_cs(out + (size_t)i * a.n, c10, c11);
+      st2_cs(out + lnn + (size_t)i * a.n, c20, c21);
+    }
+  }
+}
+
+// ============================================================ samplers (debug)
+__global__ void sample_kernel(SampleArgs a) {
+  size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.n) return;
+  if (a.tag == TAG_SK || a.tag == TAG_ENC_U) {
+    uint4 w = stream_block(a.seed, a.msg, a.tag, 0, (uint32_t)(c / 4));
+    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    reinterpret_cast<int64_t *>(a.out)[c] = tern(ws[c % 4]);
+  } else if (a.tag == TAG_PK_A) {
+    uint4 w = stream_block(a.seed, a.msg, a.tag, a.limb, (uint32_t)c);
+    reinterpret_cast<uint64_t *>(a.out)[c] = uniform_mod(w, a.q);
+  } else {
+    uint4 w = stream_block(a.seed, a.msg, a.tag, 0, (uint32_t)(c / 2));
+    reinterpret_cast<int64_t *>(a.out)[c] = (c & 1) ? cbd_hi(w) : cbd_lo(w);
+  }
+}
+
+// ============================================================ integer peak (K11)
+// 8 independent register-resident lazy Shoup butterflies per iteration, the
+// same instruction mix as the NTT passes, no memory traffic.
+__global__ void __launch_bounds__(256) int_peak_kernel(IntPeakArgs a) {
+  const uint64_t q = a.q, two_q = 2 * a.q;
+  uint64_t v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = (threadIdx.x * 16 + r + blockIdx.x) % q;
+  uint64_t w = a.w, wp = a.wp;
+  for (int it = 0; it < a.iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) ct_bfly(v[r], v[r + 8], w, wp, q, two_q);
+    w += (v[0] & 1);  // keep w loop-variant so the compiler cannot hoist
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc ^= v[r];
+  if (acc == 0x1234567890ABCDEFull) a.sink[0] = acc;
+}
+
+size_t zinc_coeff_smem(int L, int threads) { return ((size_t)2 * L * 2 * threads + 2 * L) * sizeof(uint64_t); }
+
+cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, cudaStream_t s) {
+  dim3 grid(a.n / (2 * threads), grid_y);
+  return launch_ex(zinc_coeff_kernel, grid, threads, zinc_coeff_smem(a.L, threads), 1, s, a);
+}
+
+cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s) {
+  unsigned blocks = (unsigned)((a.n + 255) / 256);
+  sample_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_int_peak(const IntPeakArgs &a, int blocks, cudaStream_t s) {
+  int_peak_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+
+}  // namespace zinc

@@ -1,0 +1,115 @@
+// k_vanilla.cu -- vanilla encryption (Eq. 8), both forms.
+#include "kcommon.cuh"
+
+namespace zinc {
+
+// ============================================================ vanilla encryption
+// Eq. 8 with reading A1: c1 = [pk1.u + e1 + m]_q, c2 = [pk2.u + e2]_q.  CTA =
+// (message b, limb group); u, e1, e2 are sampled once per CTA into smem (int8),
+// then per limb:
+//  NTT form:   NTT(e1 + m) -> ct0;  NTT(e2) -> ct1;
+//              NTT(u) -> epilogue ct0 += pk1 u^, ct1 += pk2 u^.
+//  COEFF form: NTT(u) -> epilogue: ct1 <- pk2 u^ (temporary), smem <- pk1 u^;
+//              INTT(smem) + e1 + m -> ct0;  INTT(ct1) + e2 -> ct1.
+// 3 transforms per limb either way.
+template <int LOGN, int FORM>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs a) {
+  using G = Geo<LOGN>;
+  constexpr int N = 1 << LOGN;
+  constexpr int THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  uint8_t *su = reinterpret_cast<uint8_t *>(sm + SmemWords<G::LOGL>::value);
+  int8_t *se1 = reinterpret_cast<int8_t *>(su + N / 4), *se2 = se1 + N;
+  const size_t b = blockIdx.x / G::CLUSTER;
+  const int loff = local_off<LOGN>();
+  const uint64_t msg = a.msg_base + b;
+  sample_ternary_packed<THREADS>(su, N, a.seed, msg, TAG_ENC_U);
+  sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1);
+  sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2);
+  __syncthreads();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    if (FORM == 0) {
+      ntt_forward<LOGN>(sm, tw, q,
+          [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) st2(ct0 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
+          });
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) st2(ct1 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
+          });
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) {
+              uint64_t u0 = canon4(v[r], q, two_q), u1 = canon4(v[r + 1], q, two_q);
+              uint64_t p10, p11, p20, p21, a0, a1, b0, b1;
+              ld2(pk1 + base + r, p10, p11);
+              ld2(pk2 + base + r, p20, p21);
+              ld2(ct0 + base + r, a0, a1);
+              ld2(ct1 + base + r, b0, b1);
+              st2_cs(ct0 + base + r, add_mod(a0, mul_mod(p10, u0, c), q), add_mod(a1, mul_mod(p11, u1, c), q));
+              st2_cs(ct1 + base + r, add_mod(b0, mul_mod(p20, u0, c), q), add_mod(b1, mul_mod(p21, u1, c), q));
+            }
+          });
+    } else {
+      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); },
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) {
+              uint64_t u0 = canon4(v[r], q, two_q), u1 = canon4(v[r + 1], q, two_q);
+              uint64_t p10, p11, p20, p21;
+              ld2(pk1 + base + r, p10, p11);
+              ld2(pk2 + base + r, p20, p21);
+              st2(ct1 + base + r, mul_mod(p20, u0, c), mul_mod(p21, u1, c));
+              sm[pad16(base - loff + r)] = mul_mod(p10, u0, c);
+              sm[pad16(base - loff + r + 1)] = mul_mod(p11, u1, c);
+            }
+          });
+      const Tw *itw = a.itw + (size_t)i * N;
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
+          },
+          [&](int x, uint64_t v) {
+            uint64_t e = reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64);
+            __stcs(ct0 + x, add_mod(csub(v, q), e, q));
+          });
+      ntt_inverse<LOGN>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int r = 0; r < 16; r += 2) ld2(ct1 + base + r, v[r], v[r + 1]);
+          },
+          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), reduce_small(se2[x], q), q)); });
+    }
+  }
+}
+
+template <int LOGN>
+static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
+  using G = Geo<LOGN>;
+  const size_t smem = ntt_smem_bytes<LOGN>() + (1 << LOGN) / 4 + 2 * (1 << LOGN);
+  if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(vanilla_kernel<LOGN, 1>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
+}
+cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
+#define CALL(K) launch_vanilla_t<K>(a, form, batch, groups, s)
+  ZINC_LOGN_SWITCH(log_n, CALL)
+#undef CALL
+}
+
+
+}  // namespace zinc

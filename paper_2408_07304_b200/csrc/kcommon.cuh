@@ -1,0 +1,105 @@
+// kcommon.cuh -- helpers shared by the kernel translation units of libzinc.so:
+// the small-sample samplers (C-4), 16-byte global loads/stores, and the
+// cluster-capable launcher.  (Internal; the public ABI is include/zinc.h.)
+#pragma once
+#include <stdint.h>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.h"
+#include "ntt.cuh"
+
+namespace zinc {
+
+
+// ============================================================ sampling helpers
+// Fill int8 smem arrays with the limb-independent small samples of one message
+// (C-4: ternary / CBD draws use limb 0 and are reduced into every limb).
+template <int THREADS>
+ZINC_DEV void sample_ternary_smem(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
+  for (int blk = threadIdx.x; blk < n / 4; blk += THREADS) {
+    uint4 w = stream_block(seed, msg, tag, 0, blk);
+    char4 t = make_char4(tern(w.x), tern(w.y), tern(w.z), tern(w.w));
+    reinterpret_cast<char4 *>(dst)[blk] = t;
+  }
+}
+// Ternary packed 2 bits per coefficient (t + 1 in {0, 1, 2}): N/4 bytes.
+template <int THREADS>
+ZINC_DEV void sample_ternary_packed(uint8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
+  for (int blk = threadIdx.x; blk < n / 4; blk += THREADS) {
+    uint4 w = stream_block(seed, msg, tag, 0, blk);
+    dst[blk] = (uint8_t)((tern(w.x) + 1) | ((tern(w.y) + 1) << 2) | ((tern(w.z) + 1) << 4) | ((tern(w.w) + 1) << 6));
+  }
+}
+ZINC_DEV int tern_at(const uint8_t *p, int x) { return (int)((p[x >> 2] >> ((x & 3) * 2)) & 3u) - 1; }
+template <int THREADS>
+ZINC_DEV void sample_cbd_smem(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
+  for (int blk = threadIdx.x; blk < n / 2; blk += THREADS) {
+    uint4 w = stream_block(seed, msg, tag, 0, blk);
+    reinterpret_cast<char2 *>(dst)[blk] = make_char2(cbd_lo(w), cbd_hi(w));
+  }
+}
+
+ZINC_DEV void ld2(const uint64_t *p, uint64_t &a, uint64_t &b) {
+  ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(p);
+  a = v.x; b = v.y;
+}
+ZINC_DEV void st2(uint64_t *p, uint64_t a, uint64_t b) {
+  *reinterpret_cast<ulonglong2 *>(p) = make_ulonglong2(a, b);
+}
+// streaming (evict-first) 128-bit store: ciphertexts are written once
+ZINC_DEV void st2_cs(uint64_t *p, uint64_t a, uint64_t b) {
+  asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+ZINC_DEV ulonglong2 ld2_nc(const void *p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+
+// ============================================================ launchers
+template <class K>
+inline cudaError_t set_smem(K kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// Launch with an optional thread-block cluster along x (2 for the N = 2^15 split).
+template <class... KArgs, class... Args>
+inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, int threads, size_t smem, int cluster,
+                             cudaStream_t s, Args... args) {
+  cudaError_t e = set_smem(kernel, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  if (cluster > 1) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int LOGN> static size_t ntt_smem_bytes() { return SmemWords<Geo<LOGN>::LOGL>::value * sizeof(uint64_t); }
+template <int LOGN> static dim3 msg_grid(size_t count, int groups = 1) {
+  return dim3((unsigned)(count * Geo<LOGN>::CLUSTER), groups);
+}
+
+#define ZINC_LOGN_SWITCH(log_n, CALL) \
+  switch (log_n) {                    \
+    case 12: return CALL(12);         \
+    case 13: return CALL(13);         \
+    case 14: return CALL(14);         \
+    case 15: return CALL(15);         \
+  }                                   \
+  return cudaErrorInvalidValue;
+
+
+}  // namespace zinc

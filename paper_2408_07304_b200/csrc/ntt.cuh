@@ -38,7 +38,7 @@ struct SmemWords { static constexpr int value = (1 << LOGN) + ((1 << LOGN) >> 4)
 // GROUPED, Store is called once per group as store(base, v) with the 2^K words
 // of the group (T == 1: contiguous words base .. base + 2^K - 1).
 template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, class Load, class Store>
-ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, Load load, Store store) {
+ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, Store store) {
   constexpr int N = 1 << LOGN;
   constexpr int G = 1 << K;
   constexpr int T = N >> (S0 + K);
@@ -56,7 +56,7 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, Load load, Store st
       const int D = G >> (l + 1);
 #pragma unroll
       for (int blk = 0; blk < (1 << l); ++blk) {
-        const Tw w = ldtw(tw + (1 << (S0 + l)) + (beta << l) + blk);
+        const Tw w = ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
         for (int j = 0; j < D; ++j) ct_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
       }
@@ -74,8 +74,8 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, Load load, Store st
 // Load -> [0, 2q); Store gets [0, 2q).  When LAST (S0 == 0), stage 0 multiplies
 // the sum by N^-1 and the difference by N^-1 psi^-brv(1) (folded scaling).
 // With GROUPED, Load is called once per group as load(base, v).
-template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, class Load, class Store>
-ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, Load load, Store store) {
+template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool FOLD = true, class Load, class Store>
+ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Load load, Store store) {
   constexpr int N = 1 << LOGN;
   constexpr int G = 1 << K;
   constexpr int T = N >> (S0 + K);
@@ -95,7 +95,7 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, Load load,
 #pragma unroll
     for (int l = K - 1; l >= 0; --l) {
       const int D = G >> (l + 1);
-      if (S0 == 0 && l == 0) {
+      if (FOLD && S0 == 0 && l == 0) {
         // last stage (single block, twiddle psi^-brv(1)) with N^-1 folded in
 #pragma unroll
         for (int j = 0; j < D; ++j) {
@@ -108,7 +108,7 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, Load load,
       } else {
 #pragma unroll
         for (int blk = 0; blk < (1 << l); ++blk) {
-          const Tw w = ldtw(itw + (1 << (S0 + l)) + (beta << l) + blk);
+          const Tw w = ldtw(itw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
           for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
         }
@@ -128,36 +128,127 @@ template <> struct Plan<12> { static constexpr int THREADS = 256, KA = 4, KB = 4
 template <> struct Plan<13> { static constexpr int THREADS = 256, KA = 5, KB = 4, KC = 4; };
 template <> struct Plan<14> { static constexpr int THREADS = 512, KA = 5, KB = 5, KC = 4; };
 
-// Forward NTT: pass A from `load`, passes B, C through smem; `gstore(base, v[16])`
-// receives each group of 16 contiguous outputs (bit-reversed NTT order, C-3).
+// ---------------------------------------------------------------- geometry
+// N <= 2^14: one CTA holds a whole limb (2^14 words = 128 KiB + padding).
+// N = 2^15: a limb (256 KiB) exceeds a CTA's 227 KB of shared memory, so a
+// 2-CTA thread-block cluster splits it.  Forward (CT, natural input): stage 0
+// pairs j with j + N/2 under one twiddle W[1]; CTA r computes half r of stage 0
+// straight from its loads (X + W Y for r = 0, X - W Y for r = 1) and then runs
+// the remaining stages as an independent N/2-point transform whose stage-s'
+// blocks are the global stage-(s'+1) blocks r 2^s' + beta, i.e. twiddle index
+// (2 + r) 2^s' + beta ("tb" below); its outputs are positions [r N/2, (r+1) N/2)
+// of the bit-reversed result.  Inverse (GS, bit-reversed input): each CTA runs
+// stages LOGN-1 .. 1 on its half, then stage 0 (with N^-1 folded in) exchanges
+// halves through distributed shared memory: CTA r finishes j in
+// [r N/4, (r+1) N/4) from both CTAs' buffers.
+template <int LOGN> struct Geo {
+  static constexpr bool SPLIT = LOGN > 14;
+  static constexpr int LOGL = SPLIT ? LOGN - 1 : LOGN;  // words per CTA = 2^LOGL
+  static constexpr int NL = 1 << LOGL;
+  static constexpr int CLUSTER = SPLIT ? 2 : 1;
+  static constexpr int THREADS = Plan<LOGL>::THREADS;
+};
+
+ZINC_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+ZINC_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Generic pointer to the same shared-memory object in cluster CTA `rank`.
+template <class T>
+ZINC_DEV T *peer_smem(T *p, uint32_t rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;" : "=l"(out) : "l"(p), "r"(rank));
+  return reinterpret_cast<T *>(out);
+}
+// Index offset of this CTA's share of a limb (0 unless split).
+template <int LOGN> ZINC_DEV int local_off() {
+  if constexpr (Geo<LOGN>::SPLIT) return (int)cluster_rank() * Geo<LOGN>::NL;
+  else return 0;
+}
+
+// Forward NTT: pass A from `load(x)` (x a global index, value in [0, 4q)),
+// passes B, C through smem; `gstore(base, v[16])` receives each group of 16
+// contiguous outputs (bit-reversed NTT order, C-3) at global position base.
 template <int LOGN, class Load, class GStore>
 ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GStore gstore) {
-  using P = Plan<LOGN>;
+  using G = Geo<LOGN>;
+  using P = Plan<G::LOGL>;
+  constexpr int LL = G::LOGL;
   constexpr int SB = P::KA, SC = P::KA + P::KB;
-  static_assert(SC + P::KC == LOGN && P::KC == 4, "plan");
+  static_assert(SC + P::KC == LL && P::KC == 4, "plan");
+  auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
+  auto sld = [&](int i) { return sm[pad16(i)]; };
   __syncthreads();  // the previous transform may still read sm
-  ct_pass<LOGN, 0, P::KA, P::THREADS>(tw, q, load, [&](int i, uint64_t v) { sm[pad16(i)] = v; });
-  __syncthreads();
-  ct_pass<LOGN, SB, P::KB, P::THREADS>(tw, q, [&](int i) { return sm[pad16(i)]; },
-                                        [&](int i, uint64_t v) { sm[pad16(i)] = v; });
-  __syncthreads();
-  ct_pass<LOGN, SC, P::KC, P::THREADS, true>(tw, q, [&](int i) { return sm[pad16(i)]; }, gstore);
+  if constexpr (!G::SPLIT) {
+    ct_pass<LL, 0, P::KA, P::THREADS>(tw, q, 1, load, sst);
+    __syncthreads();
+    ct_pass<LL, SB, P::KB, P::THREADS>(tw, q, 1, sld, sst);
+    __syncthreads();
+    ct_pass<LL, SC, P::KC, P::THREADS, true>(tw, q, 1, sld, gstore);
+  } else {
+    const int r = (int)cluster_rank();
+    const Tw w1 = ldtw(tw + 1);
+    const uint64_t two_q = 2 * q;
+    auto load0 = [&](int x) {
+      const uint64_t X = csub(load(x), two_q);
+      const uint64_t t = mul_shoup_lazy(load(x + G::NL), w1.x, w1.y, q);
+      return r == 0 ? X + t : X - t + two_q;
+    };
+    const int tb = 2 + r;
+    ct_pass<LL, 0, P::KA, P::THREADS>(tw, q, tb, load0, sst);
+    __syncthreads();
+    ct_pass<LL, SB, P::KB, P::THREADS>(tw, q, tb, sld, sst);
+    __syncthreads();
+    ct_pass<LL, SC, P::KC, P::THREADS, true>(tw, q, tb, sld,
+        [&](int base, uint64_t (&v)[16]) { gstore(base + r * G::NL, v); });
+  }
 }
 
 // Inverse NTT: `gload(base, v[16])` supplies each group of 16 contiguous inputs
-// in [0, 2q); passes B', A' through smem; `store(idx, v)` gets the natural-order
-// outputs in [0, 2q) at indices o + r*T with lane-consecutive o (coalesced).
+// in [0, 2q) (global position base); `store(idx, v)` gets the natural-order
+// outputs in [0, 2q) at global indices, lane-consecutive (coalesced).  When
+// split, every store happens after both CTAs of the pair consumed their inputs
+// (in-place use is safe).
 template <int LOGN, class GLoad, class Store>
 ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad gload, Store store) {
-  using P = Plan<LOGN>;
+  using G = Geo<LOGN>;
+  using P = Plan<G::LOGL>;
+  constexpr int LL = G::LOGL;
   constexpr int SB = P::KA, SC = P::KA + P::KB;
+  auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
+  auto sld = [&](int i) { return sm[pad16(i)]; };
   __syncthreads();
-  gs_pass<LOGN, SC, P::KC, P::THREADS, true>(itw, c, gload, [&](int i, uint64_t v) { sm[pad16(i)] = v; });
-  __syncthreads();
-  gs_pass<LOGN, SB, P::KB, P::THREADS>(itw, c, [&](int i) { return sm[pad16(i)]; },
-                                        [&](int i, uint64_t v) { sm[pad16(i)] = v; });
-  __syncthreads();
-  gs_pass<LOGN, 0, P::KA, P::THREADS>(itw, c, [&](int i) { return sm[pad16(i)]; }, store);
+  if constexpr (!G::SPLIT) {
+    gs_pass<LL, SC, P::KC, P::THREADS, true>(itw, c, 1, gload, sst);
+    __syncthreads();
+    gs_pass<LL, SB, P::KB, P::THREADS>(itw, c, 1, sld, sst);
+    __syncthreads();
+    gs_pass<LL, 0, P::KA, P::THREADS>(itw, c, 1, sld, store);
+  } else {
+    const int r = (int)cluster_rank();
+    const int tb = 2 + r;
+    gs_pass<LL, SC, P::KC, P::THREADS, true>(itw, c, tb,
+        [&](int base, uint64_t (&v)[16]) { gload(base + r * G::NL, v); }, sst);
+    __syncthreads();
+    gs_pass<LL, SB, P::KB, P::THREADS>(itw, c, tb, sld, sst);
+    __syncthreads();
+    gs_pass<LL, 0, P::KA, P::THREADS, false, false>(itw, c, tb, sld, sst);
+    cluster_sync_all();  // both halves complete and every input consumed
+    const uint64_t *h0 = peer_smem(sm, 0), *h1 = peer_smem(sm, 1);
+    const uint64_t two_q = c.two_q, q = c.q;
+    constexpr int QN = G::NL / 2;
+#pragma unroll 2
+    for (int j = r * QN + threadIdx.x; j < (r + 1) * QN; j += P::THREADS) {
+      const uint64_t X = h0[pad16(j)], Y = h1[pad16(j)];
+      store(j, mul_shoup_lazy(X + Y, c.ninv, c.ninv_sh, q));
+      store(j + G::NL, mul_shoup_lazy(X - Y + two_q, c.ninv_w, c.ninv_w_sh, q));
+    }
+    cluster_sync_all();  // the partner finished reading this CTA's buffer
+  }
 }
 
 }  // namespace zinc

@@ -54,7 +54,7 @@ def setup_for(Z, orc, name):
     return _setups[name]
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_params_match_oracle(Z, orc, name):
     s = setup_for(Z, orc, name)
     assert s.ctx.q == [int(x) for x in s.P.q]
@@ -76,7 +76,7 @@ def test_sampler_streams_bit_exact(Z, orc, tag):
         assert np.array_equal(got, want), (tag, seed, msg, limb)
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_ntt_bit_exact(Z, orc, name):
     s = setup_for(Z, orc, name)
     rng = np.random.default_rng(11)
@@ -96,7 +96,7 @@ def test_ntt_bit_exact(Z, orc, name):
     assert np.array_equal(np64(d)[0], orc.ntt_limbs(s.P, e[0]))
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_keygen_and_cache_bit_exact(Z, orc, name):
     s = setup_for(Z, orc, name)
     assert np.array_equal(np64(s.skc).astype(np.int64), s.o_sk)
@@ -131,7 +131,7 @@ def test_encrypt_int64_c1_all_messages(Z, orc, path, form):
     _check_msgs(orc, s, path, form, m, np64(ct), seed, base, range(B))
 
 
-@pytest.mark.parametrize("name", ["C2", "C3"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
 @pytest.mark.parametrize("path", ["zinc", "vanilla"])
 @pytest.mark.parametrize("form", [NTT, COEFF])
 def test_encrypt_int64_sampled(Z, orc, name, path, form):
@@ -148,7 +148,7 @@ def test_encrypt_int64_sampled(Z, orc, name, path, form):
     _check_msgs(orc, s, path, form, m, np64(ct), seed, base, [0, 3, 19, 20, 36])
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_encode_within_one(Z, orc, name):
     s = setup_for(Z, orc, name)
     cfg = s.cfg
@@ -174,7 +174,7 @@ def test_encode_complex_slots(Z, orc):
         assert np.max(np.abs(m[b] - orc.encode(z[b], s.P.log_n, s.P.log_scale))) <= 1
 
 
-@pytest.mark.parametrize("name", ["C1", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
 @pytest.mark.parametrize("path", ["zinc", "vanilla"])
 @pytest.mark.parametrize("form", [NTT, COEFF])
 def test_slots_to_ciphertext_and_decrypt(Z, orc, name, path, form):
@@ -203,8 +203,9 @@ def test_slots_to_ciphertext_and_decrypt(Z, orc, name, path, form):
     assert err < cfg.tolerance(), err
 
 
-def test_decrypt_wrong_key_flags_crt(Z, orc):
-    s = setup_for(Z, orc, "C1")
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_decrypt_wrong_key_flags_crt(Z, orc, name):
+    s = setup_for(Z, orc, name)
     z = torch.from_numpy(slots_batch(s.cfg, 0, 4)).cuda()
     ct = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 1, 0)
     other, _, _ = Z.zinc_keygen(s.ctx, 999)
@@ -212,8 +213,9 @@ def test_decrypt_wrong_key_flags_crt(Z, orc):
     assert (np64(status) == 1).all()
 
 
-def test_decode_matches_oracle(Z, orc):
-    s = setup_for(Z, orc, "C1")
+@pytest.mark.parametrize("name", ["C1", "C4"])
+def test_decode_matches_oracle(Z, orc, name):
+    s = setup_for(Z, orc, name)
     z = torch.from_numpy(slots_batch(s.cfg, 3, 2)).cuda()
     ct = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z, 4, 0)
     coeff, status, slots = Z.ckks_decrypt_batch(s.ctx, s.sk, NTT, ct)
