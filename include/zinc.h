@@ -195,6 +195,20 @@ const char *zinc_kernel_name(int id);
 uint64_t zinc_launch_count(void);
 void zinc_launch_count_reset(void);
 
+/* Process-wide tuning knobs (launch geometry only; results never change):
+ *  ZINC_TUNE_COEFF_MSGS_PER_CTA   messages per CTA of the COEFF-form Zinc kernel (default 2)
+ *  ZINC_TUNE_ENCODE_CHUNK_BYTES   bytes of int64 plaintexts encoded per chunk when the input is slots
+ *                                 (default 32 MiB: the chunk stays resident in the 126 MB L2)
+ *  ZINC_TUNE_OVERLAP              1: encode chunk k+1 on an internal high-priority stream while the
+ *                                 path kernel of chunk k runs; 0 (default): serial on the caller's stream
+ *  ZINC_TUNE_COEFF_SMEM_PAD       extra bytes of dynamic shared memory requested by the COEFF-form
+ *                                 Zinc kernel (limits how many of its CTAs share an SM with the
+ *                                 overlapped encode; default 0)
+ * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
+enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_OVERLAP = 2,
+       ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_COUNT = 4 };
+zinc_status zinc_tune(int knob, long long value, long long *old_value);
+
 /* Thread-local message for the last non-OK status of this thread. */
 const char *zinc_last_error(void);
 

@@ -24,7 +24,7 @@ __all__ = [
     "zinc_keygen", "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch",
     "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
     "zinc_debug_sample", "zinc_int_peak", "zinc_encrypt_batch_host", "launch_count",
-    "launch_count_reset", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
+    "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_OVERLAP", "TUNE_COEFF_SMEM_PAD", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
 ]
 
 NTT, COEFF = 0, 1
@@ -39,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch", "ckks_decrypt_batch",
     "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse", "zinc_debug_sample", "zinc_int_peak",
     "zinc_encrypt_batch_host", "zinc_launch_count", "zinc_launch_count_reset", "zinc_last_error",
-    "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name",
+    "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name", "zinc_tune",
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
                 "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel")
@@ -69,6 +69,7 @@ _SIGS = {
     "zinc_encrypt_batch_host": [_vp, _i32, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _sz],
     "zinc_profile_enable": [_i32],
     "zinc_profile_read": [_c.POINTER(_c.c_double), _c.POINTER(_u64)],
+    "zinc_tune": [_i32, _c.c_longlong, _c.POINTER(_c.c_longlong)],
 }
 
 _lib = None
@@ -290,6 +291,16 @@ def profile_read() -> dict:
     cnt = (ctypes.c_uint64 * n)()
     _check(lib().zinc_profile_read(ms, cnt), "zinc_profile_read")
     return {KERNEL_NAMES[i]: (float(ms[i]), int(cnt[i])) for i in range(n) if cnt[i]}
+
+
+TUNE_COEFF_MSGS_PER_CTA, TUNE_ENCODE_CHUNK_BYTES, TUNE_OVERLAP, TUNE_COEFF_SMEM_PAD = 0, 1, 2, 3
+
+
+def tune(knob: int, value: int) -> int:
+    """Set a launch-geometry knob (results never change); returns the previous value."""
+    old = ctypes.c_longlong()
+    _check(lib().zinc_tune(knob, value, ctypes.byref(old)), "zinc_tune")
+    return old.value
 
 
 def launch_count() -> int:

@@ -4,6 +4,7 @@
 // Parameter generation here is written independently of oracle/ (different
 // Miller-Rabin base set, table-driven twiddles); tests check both against the
 // SURVEY Appendix A values.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -92,6 +93,9 @@ struct TraceScope {
       return fail(ZINC_ECUDA, "launch %s failed: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
+// ------------------------------------------------------------------ tuning
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}};
+
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
   int device, log_n, n, L, log_scale;
@@ -99,7 +103,7 @@ struct zinc_ctx {
   std::vector<LimbConst> h_limbs;
   LimbConst *d_limbs = nullptr;
   Tw *d_tw = nullptr, *d_itw = nullptr;
-  double2 *d_fft_tw = nullptr, *d_twist = nullptr;
+  double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr;
   int *d_perm = nullptr;
   // host-API pipeline buffers (grow-only, guarded)
   std::mutex host_mu;
@@ -107,6 +111,10 @@ struct zinc_ctx {
   uint64_t *h_ct_d[2] = {nullptr, nullptr};
   size_t h_pt_bytes = 0, h_ct_bytes = 0;
   cudaStream_t h_streams[2] = {nullptr, nullptr};
+  // side stream: slot encodes overlap the previous chunk's path kernel
+  std::mutex side_mu;
+  cudaStream_t side = nullptr;
+  uint64_t qmin = 0;
 };
 
 // ------------------------------------------------------------------ number theory (host)
@@ -221,6 +229,14 @@ zinc_status zinc_profile_read(double *ms, uint64_t *launches) {
   return ZINC_OK;
 }
 uint64_t zinc_launch_count(void) { return g_launches.load(); }
+
+zinc_status zinc_tune(int knob, long long value, long long *old_value) {
+  if (knob < 0 || knob >= ZINC_TUNE_COUNT) return fail(ZINC_EINVAL, "bad tuning knob %d", knob);
+  if (value < 0) return fail(ZINC_EINVAL, "tuning value must be >= 0");
+  const long long prev = g_tune[knob].exchange(value);
+  if (old_value) *old_value = prev;
+  return ZINC_OK;
+}
 void zinc_launch_count_reset(void) { g_launches.store(0); }
 
 zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
@@ -231,7 +247,9 @@ zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
   cudaFree(ctx->d_itw);
   cudaFree(ctx->d_fft_tw);
   cudaFree(ctx->d_twist);
+  cudaFree(ctx->d_fft_tw_h);
   cudaFree(ctx->d_perm);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ctx->h_pt_d[k]);
     cudaFree(ctx->h_ct_d[k]);
@@ -290,12 +308,16 @@ zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scal
   }
   // FFT tables for encode / decode (C-6): M = N/2
   const int M = n / 2, log_m = log_n - 1;
-  std::vector<double2> ftw(M / 2), twist(M);
+  std::vector<double2> ftw(M / 2), twist(M), ftw_h(M / 4);
   std::vector<int> perm(M);
   const long double pi = 3.141592653589793238462643383279502884L;
   for (int e = 0; e < M / 2; ++e) {
     long double ang = -2.0L * pi * (long double)e / (long double)M;
     ftw[e] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  for (int e = 0; e < M / 4; ++e) {  // W_{M/2}^e: the real-slot encode's half-length FFT
+    long double ang = -2.0L * pi * (long double)e / (long double)(M / 2);
+    ftw_h[e] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
   for (int j = 0; j < M; ++j) {
     long double ang = -pi * (long double)j / (long double)n;
@@ -309,9 +331,19 @@ zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scal
   zinc_status st;
   if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(ZINC_ECUDA, "cudaSetDevice(%d) failed", device); }
   if ((st = upload(&c->d_limbs, c->h_limbs)) || (st = upload(&c->d_tw, tw)) || (st = upload(&c->d_itw, itw)) ||
-      (st = upload(&c->d_fft_tw, ftw)) || (st = upload(&c->d_twist, twist)) || (st = upload(&c->d_perm, perm))) {
+      (st = upload(&c->d_fft_tw, ftw)) || (st = upload(&c->d_twist, twist)) || (st = upload(&c->d_perm, perm)) ||
+      (st = upload(&c->d_fft_tw_h, ftw_h))) {
     zinc_ctx_destroy(c);
     return st;
+  }
+  c->qmin = *std::min_element(c->q.begin(), c->q.end());
+  // the side stream gets the highest priority so the block scheduler hands freed
+  // SM slots to the (short) encode CTAs ahead of the streaming kernel's backlog
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
+    zinc_ctx_destroy(c);
+    return fail(ZINC_ECUDA, "side stream creation failed");
   }
   // stream-ordered scratch (slot encodes) comes from the default pool: keep it
   cudaMemPool_t pool;
@@ -366,6 +398,7 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
   a.perm = c->d_perm;
   a.fft_tw = c->d_fft_tw;
   a.twist = c->d_twist;
+  a.fft_tw_h = c->d_fft_tw_h;
   a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
   a.m_out = m;
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
@@ -393,15 +426,14 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.n = c->n;
     a.L = c->L;
+    a.qmin = c->qmin;
     int threads = 256;
-    while (threads > 32 && zinc_coeff_smem(c->L, threads) > 100 * 1024) threads /= 2;
-    const int gx = c->n / (2 * threads);
-    const int per_sm = (int)std::max<size_t>(1, (200 * 1024) / zinc_coeff_smem(c->L, threads));
-    const size_t target = (size_t)148 * per_sm * 2;
-    size_t gy = std::max<size_t>(1, (target + gx - 1) / gx);
-    a.msgs_per_cta = (batch + gy - 1) / gy;
-    gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
-    LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, s));
+    while (threads > 32 && zinc_coeff_smem(c->L, threads) > 72 * 1024) threads /= 2;
+    // grid = coefficient tiles x message groups of `msgs_per_cta` (tuning knob)
+    const size_t mpc = (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load());
+    a.msgs_per_cta = mpc;
+    const size_t gy = (batch + mpc - 1) / mpc;
+    LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, (size_t)g_tune[ZINC_TUNE_COEFF_SMEM_PAD].load(), s));
     return ZINC_OK;
   }
   const int lpc = limbs_per_cta(c, batch);
@@ -437,25 +469,67 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
 
 // Encryption with any plaintext kind: int64 plaintexts go straight to the path
 // kernel; slots are encoded chunk by chunk into stream-ordered scratch sized to
-// stay resident in L2 between the encode and the path kernel.
-static const size_t kEncodeChunkBytes = 32ull << 20;
-static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key, int form, int kind,
+// stay resident in L2 between the encode and the path kernel.  The encodes run
+// on the context's side stream, double-buffered, so chunk k+1 is encoded while
+// the path kernel of chunk k streams its ciphertexts out (events order the
+// buffers; the caller's stream sees the whole call as one ordered operation).
+static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key, int form, int kind,
                                const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
                                cudaStream_t s) {
+  zinc_ctx *c = const_cast<zinc_ctx *>(cc);
   if (kind == ZINC_PT_COEFF_I64) return run_path(c, path, key, form, (const int64_t *)pt, batch, seed, msg_base, ct, s);
   const size_t per_msg = (size_t)c->n * 8;
-  const size_t chunk = std::max<size_t>(1, std::min(batch, kEncodeChunkBytes / per_msg));
+  const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());
+  const size_t chunk = std::max<size_t>(1, std::min(batch, chunk_bytes / per_msg));
+  const bool overlap = g_tune[ZINC_TUNE_OVERLAP].load() != 0 && batch > chunk;
+  const int nbuf = overlap ? 2 : 1;
   int64_t *m = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&m, chunk * per_msg, s));
+  CUDA_TRY(cudaMallocAsync((void **)&m, nbuf * chunk * per_msg, s));
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_stride = (size_t)2 * c->L * c->n;
   zinc_status st = ZINC_OK;
-  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
+  if (!overlap) {
+    for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
+      const size_t cnt = std::min(chunk, batch - off);
+      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m, s);
+      if (st == ZINC_OK) st = run_path(c, path, key, form, m, cnt, seed, msg_base + off, ct + off * ct_stride, s);
+    }
+    cudaFreeAsync(m, s);
+    return st;
+  }
+  std::lock_guard<std::mutex> lock(c->side_mu);
+  cudaEvent_t ev_in, ev_enc[2], ev_use[2];
+  CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_enc[k], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_use[k], cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaEventRecord(ev_in, s));  // inputs and the scratch allocation are ready
+  CUDA_TRY(cudaStreamWaitEvent(c->side, ev_in, 0));
+  size_t k = 0;
+  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
+    const int buf = (int)(k & 1);
     const size_t cnt = std::min(chunk, batch - off);
-    st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m, s);
-    if (st == ZINC_OK) st = run_path(c, path, key, form, m, cnt, seed, msg_base + off, ct + off * ct_stride, s);
+    int64_t *mb = m + (size_t)buf * chunk * c->n;
+    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(c->side, ev_use[buf], 0));  // chunk k-2 consumed mb
+    st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, c->side);
+    if (st != ZINC_OK) break;
+    CUDA_TRY(cudaEventRecord(ev_enc[buf], c->side));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_enc[buf], 0));
+    st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s);
+    if (st != ZINC_OK) break;
+    CUDA_TRY(cudaEventRecord(ev_use[buf], s));
+  }
+  if (st != ZINC_OK) {  // keep the caller's stream ordered after whatever was enqueued on the side stream
+    cudaEventRecord(ev_in, c->side);
+    cudaStreamWaitEvent(s, ev_in, 0);
   }
   cudaFreeAsync(m, s);
+  cudaEventDestroy(ev_in);
+  for (int j = 0; j < 2; ++j) {
+    cudaEventDestroy(ev_enc[j]);
+    cudaEventDestroy(ev_use[j]);
+  }
   return st;
 }
 

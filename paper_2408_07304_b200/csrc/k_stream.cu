@@ -1,4 +1,6 @@
 // k_stream.cu -- Zinc add/inject (COEFF form), the debug sampler and the integer-peak microkernel.
+#include <algorithm>
+
 #include "kcommon.cuh"
 
 namespace zinc {
@@ -11,11 +13,26 @@ namespace zinc {
 // (cp.async.bulk, the 1-D TMA path, completing on an mbarrier) and reused for
 // every message; each thread owns 2 coefficients, draws e1'/e2' with one Philox
 // call each (C-4 block = j/2), and streams 2L 16-byte stores per message.
-__global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
+//
+// Per output word the work is one 64-bit modular add plus a share of the
+// limb-independent prologue, so the kernel stays HBM-bound: v = m + e1' is
+// formed once per coefficient; when |v| < min_i q_i for the whole warp (every
+// CKKS plaintext at these scales) the residue of v mod q_i is v or q_i + v
+// (branch-free), otherwise an exact Barrett path runs.  The next message's m
+// is loaded while the current one is stored (software pipelining).
+ZINC_DEV uint64_t mod_add_signed(uint64_t z, int64_t v, uint64_t q) {
+  // z in [0, q), |v| < q  ->  [z + v]_q
+  const uint64_t r = (uint64_t)v + (q & (uint64_t)(v >> 63));  // v mod q in [0, q)
+  const uint64_t s = z + r;
+  return s >= q ? s - q : s;
+}
+
+template <int LC>
+__global__ void __launch_bounds__(256, 3) zinc_coeff_kernel(ZincCoeffArgs a) {
   extern __shared__ __align__(16) uint64_t tile[];  // [2][L][T], then q[L], mu64[L]
   __shared__ __align__(8) uint64_t mbar;
   const int T = 2 * blockDim.x;
-  const int L = a.L;
+  const int L = LC > 0 ? LC : a.L;
   const int j0 = blockIdx.x * T;
   uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L;
   for (int i = threadIdx.x; i < L; i += blockDim.x) {
@@ -39,6 +56,15 @@ __global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
                    ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
     }
   }
+  const int jl = 2 * threadIdx.x;       // local coefficient pair
+  const int j = j0 + jl;
+  const size_t b_begin = (size_t)blockIdx.y * a.msgs_per_cta;
+  size_t b_end = b_begin + a.msgs_per_cta;
+  if (b_end > a.batch) b_end = a.batch;
+  const size_t lnn = (size_t)L * a.n;
+  // first message's plaintext words, fetched while the tile is in flight
+  ulonglong2 mv = make_ulonglong2(0, 0);
+  if (a.m && b_begin < b_end) mv = ld2_nc(a.m + b_begin * a.n + j);
   {
     uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
     uint32_t done = 0;
@@ -47,36 +73,44 @@ __global__ void __launch_bounds__(256) zinc_coeff_kernel(ZincCoeffArgs a) {
                    : "=r"(done) : "r"(mb) : "memory");
     }
   }
-  const int jl = 2 * threadIdx.x;       // local coefficient pair
-  const int j = j0 + jl;
-  const size_t b_begin = (size_t)blockIdx.y * a.msgs_per_cta;
-  size_t b_end = b_begin + a.msgs_per_cta;
-  if (b_end > a.batch) b_end = a.batch;
-  const size_t lnn = (size_t)L * a.n;
+  const uint64_t qmin = a.qmin;
   for (size_t b = b_begin; b < b_end; ++b) {
     const uint64_t msg = a.msg_base + b;
+    const int64_t m0 = (int64_t)mv.x, m1 = (int64_t)mv.y;
+    if (a.m && b + 1 < b_end) mv = ld2_nc(a.m + (b + 1) * a.n + j);  // prefetch
     const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
     const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
-    int64_t m0 = 0, m1 = 0;
-    if (a.m) {
-      ulonglong2 mv = ld2_nc(a.m + b * a.n + j);
-      m0 = (int64_t)mv.x; m1 = (int64_t)mv.y;
-    }
     const int e0 = cbd_lo(w1), e1 = cbd_hi(w1);
     const int f0 = cbd_lo(w2), f1 = cbd_hi(w2);
     uint64_t *out = a.ct + b * 2 * lnn + j;
-#pragma unroll 4
-    for (int i = 0; i < L; ++i) {
-      const uint64_t q = sq[i], mu = smu[i];
-      uint64_t z10, z11, z20, z21;
-      ld2(tile + (size_t)i * T + jl, z10, z11);
-      ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-      const uint64_t c10 = add_mod(z10, reduce_m_plus_e(m0, e0, q, mu), q);
-      const uint64_t c11 = add_mod(z11, reduce_m_plus_e(m1, e1, q, mu), q);
-      const uint64_t c20 = add_mod(z20, reduce_small(f0, q), q);
-      const uint64_t c21 = add_mod(z21, reduce_small(f1, q), q);
-      st2_cs(out + (size_t)i * a.n, c10, c11);
-      st2_cs(out + lnn + (size_t)i * a.n, c20, c21);
+    // |m| < 2^62 rules out int64 overflow of m + e; then |v| < qmin is the fast path
+    const int64_t v0 = m0 + e0, v1 = m1 + e1;
+    const uint64_t a0 = v0 < 0 ? (uint64_t)0 - (uint64_t)v0 : (uint64_t)v0;
+    const uint64_t a1 = v1 < 0 ? (uint64_t)0 - (uint64_t)v1 : (uint64_t)v1;
+    const bool small = (m0 > -(1ll << 62)) && (m0 < (1ll << 62)) && (m1 > -(1ll << 62)) && (m1 < (1ll << 62)) &&
+                       a0 < qmin && a1 < qmin;
+    if (__all_sync(0xffffffffu, small)) {
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        const uint64_t q = sq[i];
+        uint64_t z10, z11, z20, z21;
+        ld2(tile + (size_t)i * T + jl, z10, z11);
+        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+        st2_cs(out + (size_t)i * a.n, mod_add_signed(z10, v0, q), mod_add_signed(z11, v1, q));
+        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+      }
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < L; ++i) {
+        const uint64_t q = sq[i], mu = smu[i];
+        uint64_t z10, z11, z20, z21;
+        ld2(tile + (size_t)i * T + jl, z10, z11);
+        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+        const uint64_t c10 = add_mod(z10, reduce_m_plus_e(m0, e0, q, mu), q);
+        const uint64_t c11 = add_mod(z11, reduce_m_plus_e(m1, e1, q, mu), q);
+        st2_cs(out + (size_t)i * a.n, c10, c11);
+        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+      }
     }
   }
 }
@@ -120,9 +154,16 @@ __global__ void __launch_bounds__(256) int_peak_kernel(IntPeakArgs a) {
 
 size_t zinc_coeff_smem(int L, int threads) { return ((size_t)2 * L * 2 * threads + 2 * L) * sizeof(uint64_t); }
 
-cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, cudaStream_t s) {
+cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, size_t smem_pad, cudaStream_t s) {
   dim3 grid(a.n / (2 * threads), grid_y);
-  return launch_ex(zinc_coeff_kernel, grid, threads, zinc_coeff_smem(a.L, threads), 1, s, a);
+  const size_t smem = std::min<size_t>(zinc_coeff_smem(a.L, threads) + smem_pad, 227 * 1024);
+  switch (a.L) {
+    case 3: return launch_ex(zinc_coeff_kernel<3>, grid, threads, smem, 1, s, a);
+    case 4: return launch_ex(zinc_coeff_kernel<4>, grid, threads, smem, 1, s, a);
+    case 8: return launch_ex(zinc_coeff_kernel<8>, grid, threads, smem, 1, s, a);
+    case 16: return launch_ex(zinc_coeff_kernel<16>, grid, threads, smem, 1, s, a);
+  }
+  return launch_ex(zinc_coeff_kernel<0>, grid, threads, smem, 1, s, a);
 }
 
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s) {

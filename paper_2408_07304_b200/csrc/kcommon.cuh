@@ -57,6 +57,29 @@ ZINC_DEV ulonglong2 ld2_nc(const void *p) {
   return v;
 }
 
+// ============================================================ TMA bulk copies
+// 1-D bulk async copies global -> shared (cp.async.bulk, the non-tensor TMA
+// path) completing on an mbarrier transaction count.
+ZINC_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+ZINC_DEV void mbar_init(uint64_t *mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+ZINC_DEV void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+ZINC_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mbar)) : "memory");
+}
+ZINC_DEV void mbar_wait(uint64_t *mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
+  }
+}
+
 // ============================================================ launchers
 template <class K>
 inline cudaError_t set_smem(K kernel, size_t bytes) {

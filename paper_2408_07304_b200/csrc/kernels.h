@@ -1,4 +1,4 @@
-// kernels.h -- argument blocks and launchers of the kernels in kernels.cu
+// kernels.h -- argument blocks and launchers of the kernels in k_*.cu
 // (internal to libzinc.so; the public ABI is include/zinc.h).
 #pragma once
 
@@ -19,6 +19,7 @@ struct ZincCoeffArgs {
   uint64_t *ct;           // [batch][2][L][N]
   size_t batch, msgs_per_cta;
   uint64_t seed, msg_base;
+  uint64_t qmin;          // min_i q_i (fast-path bound)
   int n, L;
 };
 struct VanillaArgs {
@@ -60,6 +61,7 @@ struct EncodeArgs {
   int complex_slots;
   const int *perm;
   const double2 *fft_tw, *twist;
+  const double2 *fft_tw_h;  // W_{M/2}^e, e < M/4 (real-slot path)
   double scale;
   int64_t *m_out;
 };
@@ -89,7 +91,7 @@ struct IntPeakArgs {
 };
 
 size_t zinc_coeff_smem(int L, int threads);
-cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, cudaStream_t s);
+cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, size_t smem_pad, cudaStream_t s);
 cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s);
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s);
 cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);

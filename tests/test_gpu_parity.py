@@ -316,3 +316,23 @@ def test_int_peak_kernel_runs(Z, orc):
     bf = Z.zinc_int_peak(s.ctx, 148 * 4, 100, sink)
     torch.cuda.synchronize()
     assert bf == 148 * 4 * 256 * 8 * 100
+
+
+@pytest.mark.parametrize("knobs", [{0: 1, 1: 1 << 20, 2: 1, 3: 0}, {0: 7, 1: 3 << 20, 2: 0, 3: 12 << 10},
+                                   {0: 2, 1: 1 << 20, 2: 1, 3: 12 << 10}])
+def test_tuning_knobs_never_change_results(Z, orc, knobs):
+    """Launch geometry (messages per CTA, encode chunk, side-stream overlap, smem
+    reservation) changes timing only: ciphertexts stay bit-identical."""
+    s = setup_for(Z, orc, "C3")
+    z = torch.from_numpy(slots_batch(s.cfg, 0, 70)).cuda()
+    ref = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 3, 10)
+    ref_v = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z[:9], 3, 10)
+    old = {k: Z.tune(k, v) for k, v in knobs.items()}
+    try:
+        got = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 3, 10)
+        got_v = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z[:9], 3, 10)
+        torch.cuda.synchronize()
+    finally:
+        for k, v in old.items():
+            Z.tune(k, v)
+    assert torch.equal(ref, got) and torch.equal(ref_v, got_v)
