@@ -67,6 +67,12 @@ def bytes_per_ct(cfg, kind="slots"):
     return ct + cfg.n * 8
 
 
+def alu_peak_derived(sm_mhz):
+    """Lazy Shoup butterfly = 13 fma-pipe + 14 alu-pipe instructions; both pipes issue
+    64 lanes/clk/SM (B300_MICROARCH.md: rt_SMSP = 2), so the alu pipe bounds it at 14/64 clk per SM."""
+    return 148 * sm_mhz * 1e6 * 64.0 / 14.0
+
+
 def butterflies_per_ct(cfg, path):
     half = cfg.n // 2 * cfg.log_n
     return (3 if path.startswith("vanilla") else 2) * cfg.L * half
@@ -199,6 +205,54 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- C5: batch sweep + cache precompute
+def c5_sweep(Z, torch, ctx_cache, batches=(1, 16, 256, 4096, 65536), reps=3):
+    """BASELINE C5: N=2^14, 8 x 54-bit, Delta=2^40, uniform slots; latency and ct/s of
+    Zinc (COEFF form) and vanilla (NTT form) per batch size, device time with CUDA
+    events (1 warm-up + `reps` timed, median), and zinc_precompute_cache timed alone."""
+    cfg = CONFIGS["C5"]
+    ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
+    sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
+    out = {"workload": "C5", "batches": {}}
+
+    def timed(fn, n):
+        fn()
+        ts = []
+        for _ in range(n):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    cache = {}
+    for f, name in ((Z.COEFF, "coeff"), (Z.NTT, "ntt")):
+        buf = ctx.empty_key()
+        ms = timed(lambda: Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, f, out=buf), 5)
+        cache[f] = buf
+        out[f"cache_precompute_ms_{name}"] = ms
+    free = torch.cuda.mem_get_info()[0]
+    for B in batches:
+        per = 2 * cfg.L * cfg.n * 8 + cfg.n // 2 * 8
+        if B * per > 0.85 * free:
+            out["batches"][str(B)] = {"skipped": f"needs {B * per / 2**30:.0f} GiB"}
+            continue
+        z = torch.from_numpy(np.ascontiguousarray(slots_batch(cfg, 0, min(B, 4096)))).cuda()
+        if B > z.shape[0]:
+            z = z.repeat((B + z.shape[0] - 1) // z.shape[0], 1)[:B].contiguous()
+        ct = ctx.empty_ct(B)
+        zc = timed(lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, z, cfg.enc_seed, 0, out=ct), reps)
+        vn = timed(lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, z, cfg.enc_seed, 0, out=ct), reps)
+        out["batches"][str(B)] = {"zinc_coeff_ms": zc, "zinc_coeff_ct_per_s": B / (zc / 1e3),
+                                  "vanilla_ntt_ms": vn, "vanilla_ntt_ct_per_s": B / (vn / 1e3)}
+        del ct, z
+        torch.cuda.empty_cache()
+    ctx.close()
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -213,6 +267,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 batch sweep")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -334,7 +389,7 @@ def main():
     if rank == 0:
         bpc = bytes_per_ct(cfg, "slots")
         kbytes = bytes_per_ct(cfg, "int64")
-        zk_ms, zk_n = prof.get("zinc_coeff_kernel", (0.0, 0))
+        zk_ms, zk_n = prof.get("zinc_coeff_kernel", (0.0, 0))  # the dominant kernel of the value path
         roof = None
         if zk_n:
             per_launch_ms = zk_ms / zk_n
@@ -356,10 +411,14 @@ def main():
             if p in seg:
                 kms = prof.get(kname, (0.0, 0))[0]
                 ach = butterflies_per_ct(cfg, p) * B / (seg[p] / 1e3)
-                alu[p] = {"bound": "alu", "kernel": kname, "achieved": ach / 1e9, "peak": int_peak / 1e9,
-                          "unit": "Gbutterfly/s", "frac": ach / int_peak,
+                kach = butterflies_per_ct(cfg, p) * B * args.steps / (kms / 1e3) if kms else ach
+                pd = alu_peak_derived(clk["sm_mhz"] or 1965.0)
+                alu[p] = {"bound": "alu", "kernel": kname, "achieved": kach / 1e9, "peak": int_peak / 1e9,
+                          "unit": "Gbutterfly/s", "frac": kach / int_peak, "achieved_path": ach / 1e9,
+                          "peak_derived": pd / 1e9, "frac_of_derived": kach / pd,
                           "butterflies_per_ct": butterflies_per_ct(cfg, p),
-                          "peak_source": "measured int_peak_kernel (K11), lazy Shoup butterflies"}
+                          "peak_source": "measured int_peak_kernel (K11), lazy Shoup butterflies; peak_derived: "
+                                         "148 SMs x sm_mhz x 64 alu lanes/clk / 14 alu ops per butterfly"}
         result = {
             "metric": METRIC,
             "value": path_out["zinc_coeff"]["ct_per_s"] if "zinc_coeff" in path_out else None,
@@ -388,6 +447,12 @@ def main():
             "validity": validity,
             "broadcast_ok": bcast_ok,
         }
+
+    if rank == 0 and world == 1 and not args.no_c5:
+        del ct
+        torch.cuda.empty_cache()
+        result["c5"] = c5_sweep(Z, torch, None)
+        ct = None
 
     # ---------------- end to end through the host-buffer API
     if not args.no_e2e:

@@ -179,7 +179,8 @@ enum {
   ZINC_K_NTT = 7,
   ZINC_K_SAMPLE = 8,
   ZINC_K_INT_PEAK = 9,
-  ZINC_K_COUNT = 10
+  ZINC_K_ZINC_FUSED = 10, /* encode of chunk k+1 fused with Zinc add/inject of chunk k */
+  ZINC_K_COUNT = 11
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */
@@ -199,8 +200,11 @@ void zinc_launch_count_reset(void);
  *  ZINC_TUNE_COEFF_MSGS_PER_CTA   messages per CTA of the COEFF-form Zinc kernel (default 2)
  *  ZINC_TUNE_ENCODE_CHUNK_BYTES   bytes of int64 plaintexts encoded per chunk when the input is slots
  *                                 (default 32 MiB: the chunk stays resident in the 126 MB L2)
- *  ZINC_TUNE_OVERLAP              1: encode chunk k+1 on an internal high-priority stream while the
- *                                 path kernel of chunk k runs; 0 (default): serial on the caller's stream
+ *  ZINC_TUNE_OVERLAP              how slot encodes meet the COEFF-form Zinc kernel: 0 (default)
+ *                                 serial chunks on the caller's stream; 1: encode chunk k+1 on an
+ *                                 internal high-priority stream; 2: one fused launch per chunk carries
+ *                                 the encode of chunk k+1 and the add/inject of chunk k (real slots,
+ *                                 N <= 2^14, L <= 8; otherwise serial)
  *  ZINC_TUNE_COEFF_SMEM_PAD       extra bytes of dynamic shared memory requested by the COEFF-form
  *                                 Zinc kernel (limits how many of its CTAs share an SM with the
  *                                 overlapped encode; default 0)

@@ -42,7 +42,8 @@ EXPORTED_SYMBOLS = (
     "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name", "zinc_tune",
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
-                "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel")
+                "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
+                "zinc_coeff_encode_kernel")
 
 
 class ZincError(RuntimeError):

@@ -50,7 +50,8 @@ static double g_trace_ms[ZINC_K_COUNT];
 static uint64_t g_trace_n[ZINC_K_COUNT];
 static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel",
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
-                                                 "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel"};
+                                                 "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
+                                                 "zinc_coeff_encode_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -390,6 +391,19 @@ static size_t pt_stride_bytes(const zinc_ctx *c, int kind) {
   return kind == ZINC_PT_COEFF_I64 ? (size_t)c->n * 8 : kind == ZINC_PT_SLOTS_F64 ? (size_t)c->n / 2 * 8 : (size_t)c->n * 8;
 }
 
+static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, int64_t *m) {
+  EncodeArgs a{};
+  a.slots = (const double *)slots;
+  a.complex_slots = kind == ZINC_PT_SLOTS_C128;
+  a.perm = c->d_perm;
+  a.fft_tw = c->d_fft_tw;
+  a.twist = c->d_twist;
+  a.fft_tw_h = c->d_fft_tw_h;
+  a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
+  a.m_out = m;
+  return a;
+}
+
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
                                cudaStream_t s) {
   EncodeArgs a{};
@@ -407,6 +421,23 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
 
 // One encryption path over messages whose int64 plaintexts are at m (or none).
 enum Path { PATH_ZINC = 0, PATH_VANILLA = 1 };
+static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, const int64_t *m, size_t batch,
+                                     uint64_t seed, uint64_t msg_base, uint64_t *ct) {
+  ZincCoeffArgs a{};
+  a.limbs = c->d_limbs;
+  a.cache = cache;
+  a.m = m;
+  a.ct = ct;
+  a.batch = batch;
+  a.seed = seed;
+  a.msg_base = msg_base;
+  a.n = c->n;
+  a.L = c->L;
+  a.qmin = c->qmin;
+  // messages per CTA (tuning knob): grid = coefficient tiles x message groups
+  a.msgs_per_cta = (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load());
+  return a;
+}
 static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
   size_t want = 2 * 148;
   if (batch >= want) return c->L;
@@ -414,25 +445,14 @@ static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
   return (c->L + groups - 1) / groups;
 }
 static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, int form, const int64_t *m,
-                            size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s) {
+                            size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s,
+                            bool m_is_scratch = false) {
   if (path == PATH_ZINC && form == ZINC_FORM_COEFF) {
-    ZincCoeffArgs a{};
-    a.limbs = c->d_limbs;
-    a.cache = key;
-    a.m = m;
-    a.ct = ct;
-    a.batch = batch;
-    a.seed = seed;
-    a.msg_base = msg_base;
-    a.n = c->n;
-    a.L = c->L;
-    a.qmin = c->qmin;
+    ZincCoeffArgs a = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
+    a.discard_m = m_is_scratch ? 1 : 0;
     int threads = 256;
     while (threads > 32 && zinc_coeff_smem(c->L, threads) > 72 * 1024) threads /= 2;
-    // grid = coefficient tiles x message groups of `msgs_per_cta` (tuning knob)
-    const size_t mpc = (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load());
-    a.msgs_per_cta = mpc;
-    const size_t gy = (batch + mpc - 1) / mpc;
+    const size_t gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
     LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, (size_t)g_tune[ZINC_TUNE_COEFF_SMEM_PAD].load(), s));
     return ZINC_OK;
   }
@@ -481,18 +501,45 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
   const size_t per_msg = (size_t)c->n * 8;
   const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());
   const size_t chunk = std::max<size_t>(1, std::min(batch, chunk_bytes / per_msg));
-  const bool overlap = g_tune[ZINC_TUNE_OVERLAP].load() != 0 && batch > chunk;
-  const int nbuf = overlap ? 2 : 1;
+  const long long mode = g_tune[ZINC_TUNE_OVERLAP].load();
+  const bool fused = mode == 2 && path == PATH_ZINC && form == ZINC_FORM_COEFF && kind == ZINC_PT_SLOTS_F64 &&
+                     fused_supported(c->log_n, c->L);
+  const bool overlap = mode == 1 && batch > chunk;
+  const int nbuf = (overlap || (fused && batch > chunk)) ? 2 : 1;
   int64_t *m = nullptr;
   CUDA_TRY(cudaMallocAsync((void **)&m, nbuf * chunk * per_msg, s));
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_stride = (size_t)2 * c->L * c->n;
   zinc_status st = ZINC_OK;
+  if (fused) {
+    // launch k: encode chunk k (k < nch) into m[k % 2] | add/inject chunk k-1 from m[(k-1) % 2]
+    const size_t nch = (batch + chunk - 1) / chunk;
+    for (size_t k = 0; k <= nch && st == ZINC_OK; ++k) {
+      const size_t enc = k < nch ? std::min(chunk, batch - k * chunk) : 0;
+      const size_t zc = k > 0 ? std::min(chunk, batch - (k - 1) * chunk) : 0;
+      int64_t *m_enc = m + (size_t)(k % nbuf) * chunk * c->n;
+      const int64_t *m_z = m + (size_t)((k + nbuf - 1) % nbuf) * chunk * c->n;
+      const EncodeArgs ea = encode_args(c, kind, (const char *)pt + (enc ? k * chunk : 0) * in_stride, m_enc);
+      const size_t zoff = k > 0 ? (k - 1) * chunk : 0;
+      ZincCoeffArgs za = zinc_coeff_args(c, key, m_z, zc, seed, msg_base + zoff, ct + zoff * ct_stride);
+      za.discard_m = 1;
+      const int gy = (int)((zc + za.msgs_per_cta - 1) / za.msgs_per_cta);
+      cudaError_t e;
+      {
+        TraceScope ts(ZINC_K_ZINC_FUSED, s);
+        e = launch_zinc_coeff_encode(c->log_n, za, gy, ea, (int)enc, s);
+      }
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (e != cudaSuccess) st = fail(ZINC_ECUDA, "fused encode/zinc launch: %s", cudaGetErrorString(e));
+    }
+    cudaFreeAsync(m, s);
+    return st;
+  }
   if (!overlap) {
     for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
       const size_t cnt = std::min(chunk, batch - off);
       st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m, s);
-      if (st == ZINC_OK) st = run_path(c, path, key, form, m, cnt, seed, msg_base + off, ct + off * ct_stride, s);
+      if (st == ZINC_OK) st = run_path(c, path, key, form, m, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
     }
     cudaFreeAsync(m, s);
     return st;
@@ -516,7 +563,7 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
     if (st != ZINC_OK) break;
     CUDA_TRY(cudaEventRecord(ev_enc[buf], c->side));
     CUDA_TRY(cudaStreamWaitEvent(s, ev_enc[buf], 0));
-    st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s);
+    st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
     if (st != ZINC_OK) break;
     CUDA_TRY(cudaEventRecord(ev_use[buf], s));
   }

@@ -1,0 +1,107 @@
+// encode_real.cuh -- the real-slot CKKS encode body (S3, C-6), shared by the
+// standalone encode kernel (k_fft.cu) and the encode-fused Zinc kernel (k_fused.cu).
+#pragma once
+
+#include "kcommon.cuh"
+
+namespace zinc {
+
+// ============================================================ encode, real slots
+// Real slots make the FFT input y (y_{h_k} = z_k) real, so the M-point
+// transform Y = FFT_M(y) is Hermitian and is obtained from ONE M/2-point complex
+// FFT of x_h = y_{2h} + i y_{2h+1} (the standard real-input split):
+//   X = FFT_{M/2}(x),  E_j = (X_j + conj X_{M/2-j}) / 2,  O_j = -i (X_j - conj X_{M/2-j}) / 2,
+//   Y_j = E_j + W_M^j O_j,  Y_{j+M/2} = E_j - W_M^j O_j   (j < M/2).
+// Half the FP64 work and half the shared memory of the complex path, and one
+// CTA covers N = 2^15.  Latency is what bounds a one-message-per-CTA FFT, so:
+// the message's slots (64 KiB at N = 2^14) and the W_{M/2} twiddle table arrive
+// by TMA bulk copies on one mbarrier; the slot order g_k = 5^k mod 2N is
+// generated in registers (2N is a power of two) instead of loaded; the FFT
+// reads its twiddles from shared memory.  The twist and rounding to m_j /
+// m_{j+M} are the same as encode_kernel's.
+ZINC_DEV uint32_t pow5_mod_pow2(uint32_t e, uint32_t mask) {
+  uint32_t r = 1, b = 5;
+  for (; e; e >>= 1, b = (b * b) & mask)
+    if (e & 1) r = (r * b) & mask;
+  return r;
+}
+
+// Shared memory bytes of one real-slot encode CTA (FFT buffer + twiddles).
+template <int LOGM> constexpr size_t encode_real_smem() {
+  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + (1 << (LOGM - 1)) / 2) * sizeof(double2);
+}
+
+// One CTA's work: encode message `b`; `buf` is the CTA's dynamic shared memory.
+template <int LOGM>
+ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
+  constexpr int M = 1 << LOGM, LH = LOGM - 1, H = 1 << LH;
+  constexpr int THREADS = 256, PER = M / THREADS;
+  using P = FftPlan<LH>;
+  static_assert(P::THREADS == THREADS, "plan");
+  double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2]
+  double *bufd = reinterpret_cast<double *>(buf);
+  __shared__ __align__(8) uint64_t mbar;
+  const int tid = threadIdx.x;
+  if (tid == 0) mbar_init(&mbar, 1);
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&mbar, (uint32_t)(M * sizeof(double) + (H / 2) * sizeof(double2)));
+    bulk_g2s(buf, a.slots + b * M, M * sizeof(double), &mbar);  // raw slots into the buffer prefix
+    bulk_g2s(stw, a.fft_tw_h, (H / 2) * sizeof(double2), &mbar);
+  }
+  constexpr uint32_t MASK = 4u * M - 1u;  // mod 2N
+  uint32_t g = pow5_mod_pow2((uint32_t)tid, MASK);
+  const uint32_t step = pow5_mod_pow2((uint32_t)THREADS, MASK);
+  mbar_wait(&mbar, 0);
+  double zv[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) zv[i] = bufd[tid + i * THREADS];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const uint32_t h = g >> 2;  // h_k = (g_k - 1) / 4
+    const int pos = (int)(__brev(h >> 1) >> (32 - LH));
+    bufd[2 * pad16(pos) + (h & 1)] = zv[i];
+    g = (g * step) & MASK;
+  }
+  __syncthreads();
+  auto lds = [&](int i) { return buf[pad16(i)]; };
+  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
+  fft_pass<LH, 0, P::K1, THREADS, true, false, 1, true>(stw, lds, sts);
+  __syncthreads();
+  fft_pass<LH, P::K1, P::K2, THREADS, true, false, 1, true>(stw, lds, sts);
+  __syncthreads();
+  fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, true>(stw, lds, sts);
+  __syncthreads();
+  int64_t *m = a.m_out + b * (2 * M);
+  const double scale = a.scale;  // Delta / M
+  constexpr int V = 4;  // independent post-processing iterations per batch
+  static_assert(H % (THREADS * V) == 0, "post tiling");
+#pragma unroll 1
+  for (int j0 = tid; j0 < H; j0 += THREADS * V) {
+    double2 w[V], tw0[V], tw1[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int j = j0 + u * THREADS;
+      w[u] = __ldg(a.fft_tw + j);
+      tw0[u] = __ldg(a.twist + j);
+      tw1[u] = __ldg(a.twist + j + H);
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int j = j0 + u * THREADS;
+      const double2 xj = buf[pad16(j)], xr = conj2(buf[pad16((H - j) & (H - 1))]);
+      const double2 e = make_double2(0.5 * (xj.x + xr.x), 0.5 * (xj.y + xr.y));
+      const double2 d = make_double2(0.5 * (xj.x - xr.x), 0.5 * (xj.y - xr.y));
+      const double2 o = make_double2(d.y, -d.x);  // -i d
+      const double2 t = cmul(o, w[u]);
+      const double2 y0 = cmul(cadd(e, t), tw0[u]), y1 = cmul(csubd(e, t), tw1[u]);
+      m[j] = llround(y0.x * scale);  // plain stores: the path kernel re-reads m from L2
+      m[j + M] = llround(y0.y * scale);
+      m[j + H] = llround(y1.x * scale);
+      m[j + H + M] = llround(y1.y * scale);
+    }
+  }
+}
+
+}  // namespace zinc

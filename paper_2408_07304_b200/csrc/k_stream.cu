@@ -1,118 +1,15 @@
 // k_stream.cu -- Zinc add/inject (COEFF form), the debug sampler and the integer-peak microkernel.
 #include <algorithm>
 
-#include "kcommon.cuh"
+#include "zinc_coeff.cuh"
 
 namespace zinc {
 
 // ============================================================ Zinc, COEFF form
-// Algorithm 1 with cache and output in coefficient form:
-//   c1'[i][j] = [zero1[i][j] + m[j] + e1'[j]]_{q_i},  c2'[i][j] = [zero2[i][j] + e2'[j]]_{q_i}.
-// CTA (x, y): coefficient tile [x*T, (x+1)*T), messages [y*mpc, (y+1)*mpc).  The
-// cache tile [2][L][T] is staged once into shared memory with bulk async copies
-// (cp.async.bulk, the 1-D TMA path, completing on an mbarrier) and reused for
-// every message; each thread owns 2 coefficients, draws e1'/e2' with one Philox
-// call each (C-4 block = j/2), and streams 2L 16-byte stores per message.
-//
-// Per output word the work is one 64-bit modular add plus a share of the
-// limb-independent prologue, so the kernel stays HBM-bound: v = m + e1' is
-// formed once per coefficient; when |v| < min_i q_i for the whole warp (every
-// CKKS plaintext at these scales) the residue of v mod q_i is v or q_i + v
-// (branch-free), otherwise an exact Barrett path runs.  The next message's m
-// is loaded while the current one is stored (software pipelining).
-ZINC_DEV uint64_t mod_add_signed(uint64_t z, int64_t v, uint64_t q) {
-  // z in [0, q), |v| < q  ->  [z + v]_q
-  const uint64_t r = (uint64_t)v + (q & (uint64_t)(v >> 63));  // v mod q in [0, q)
-  const uint64_t s = z + r;
-  return s >= q ? s - q : s;
-}
-
 template <int LC>
 __global__ void __launch_bounds__(256, 3) zinc_coeff_kernel(ZincCoeffArgs a) {
-  extern __shared__ __align__(16) uint64_t tile[];  // [2][L][T], then q[L], mu64[L]
-  __shared__ __align__(8) uint64_t mbar;
-  const int T = 2 * blockDim.x;
-  const int L = LC > 0 ? LC : a.L;
-  const int j0 = blockIdx.x * T;
-  uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L;
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    sq[i] = a.limbs[i].q;
-    smu[i] = a.limbs[i].mu64;
-  }
-  if (threadIdx.x == 0) {
-    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
-    const uint32_t bytes = (uint32_t)(T * sizeof(uint64_t));
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes * 2 * L) : "memory");
-    for (int r = 0; r < 2 * L; ++r) {
-      const uint64_t *src = a.cache + (size_t)r * a.n + j0;
-      uint32_t dst = (uint32_t)__cvta_generic_to_shared(tile + (size_t)r * T);
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
-    }
-  }
-  const int jl = 2 * threadIdx.x;       // local coefficient pair
-  const int j = j0 + jl;
-  const size_t b_begin = (size_t)blockIdx.y * a.msgs_per_cta;
-  size_t b_end = b_begin + a.msgs_per_cta;
-  if (b_end > a.batch) b_end = a.batch;
-  const size_t lnn = (size_t)L * a.n;
-  // first message's plaintext words, fetched while the tile is in flight
-  ulonglong2 mv = make_ulonglong2(0, 0);
-  if (a.m && b_begin < b_end) mv = ld2_nc(a.m + b_begin * a.n + j);
-  {
-    uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
-    uint32_t done = 0;
-    while (!done) {
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done) : "r"(mb) : "memory");
-    }
-  }
-  const uint64_t qmin = a.qmin;
-  for (size_t b = b_begin; b < b_end; ++b) {
-    const uint64_t msg = a.msg_base + b;
-    const int64_t m0 = (int64_t)mv.x, m1 = (int64_t)mv.y;
-    if (a.m && b + 1 < b_end) mv = ld2_nc(a.m + (b + 1) * a.n + j);  // prefetch
-    const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
-    const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
-    const int e0 = cbd_lo(w1), e1 = cbd_hi(w1);
-    const int f0 = cbd_lo(w2), f1 = cbd_hi(w2);
-    uint64_t *out = a.ct + b * 2 * lnn + j;
-    // |m| < 2^62 rules out int64 overflow of m + e; then |v| < qmin is the fast path
-    const int64_t v0 = m0 + e0, v1 = m1 + e1;
-    const uint64_t a0 = v0 < 0 ? (uint64_t)0 - (uint64_t)v0 : (uint64_t)v0;
-    const uint64_t a1 = v1 < 0 ? (uint64_t)0 - (uint64_t)v1 : (uint64_t)v1;
-    const bool small = (m0 > -(1ll << 62)) && (m0 < (1ll << 62)) && (m1 > -(1ll << 62)) && (m1 < (1ll << 62)) &&
-                       a0 < qmin && a1 < qmin;
-    if (__all_sync(0xffffffffu, small)) {
-#pragma unroll
-      for (int i = 0; i < L; ++i) {
-        const uint64_t q = sq[i];
-        uint64_t z10, z11, z20, z21;
-        ld2(tile + (size_t)i * T + jl, z10, z11);
-        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-        st2_cs(out + (size_t)i * a.n, mod_add_signed(z10, v0, q), mod_add_signed(z11, v1, q));
-        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
-      }
-    } else {
-#pragma unroll 1
-      for (int i = 0; i < L; ++i) {
-        const uint64_t q = sq[i], mu = smu[i];
-        uint64_t z10, z11, z20, z21;
-        ld2(tile + (size_t)i * T + jl, z10, z11);
-        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-        const uint64_t c10 = add_mod(z10, reduce_m_plus_e(m0, e0, q, mu), q);
-        const uint64_t c11 = add_mod(z11, reduce_m_plus_e(m1, e1, q, mu), q);
-        st2_cs(out + (size_t)i * a.n, c10, c11);
-        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
-      }
-    }
-  }
+  extern __shared__ __align__(16) uint64_t tile[];
+  zinc_coeff_body<LC>(a, blockIdx.x, blockIdx.y, tile);
 }
 
 // ============================================================ samplers (debug)

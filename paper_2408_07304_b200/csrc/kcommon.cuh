@@ -4,6 +4,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "fft.cuh"
 #include "kernels.h"

@@ -21,6 +21,7 @@ struct ZincCoeffArgs {
   uint64_t seed, msg_base;
   uint64_t qmin;          // min_i q_i (fast-path bound)
   int n, L;
+  int discard_m;          // m is library scratch: discard its L2 lines after reading
 };
 struct VanillaArgs {
   const LimbConst *limbs;
@@ -92,6 +93,11 @@ struct IntPeakArgs {
 
 size_t zinc_coeff_smem(int L, int threads);
 cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, size_t smem_pad, cudaStream_t s);
+// encode chunk k+1 (enc_ctas real-slot messages) fused with Zinc COEFF of chunk k
+// (gy message groups, 256-thread tiles); see k_fused.cu
+bool fused_supported(int log_n, int L);
+cudaError_t launch_zinc_coeff_encode(int log_n, const ZincCoeffArgs &za, int gy, const EncodeArgs &ea, int enc_ctas,
+                                     cudaStream_t s);
 cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s);
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s);
 cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);

@@ -64,7 +64,7 @@ def main():
             Z.tune(Z.TUNE_COEFF_MSGS_PER_CTA, mpc)
             rep("zinc_i64", timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, m, 1, 0, out=ct)),
                 ct_bytes + cfg.n * 8, mpc=mpc, pad_kb=pad)
-        for ov in (0, 1):
+        for ov in (0, 1, 2):
             Z.tune(Z.TUNE_OVERLAP, ov)
             for mb in [int(x) for x in args.chunks_mb.split(",")]:
                 Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, mb << 20)
