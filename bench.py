@@ -411,7 +411,10 @@ def main():
             if p in seg:
                 kms = prof.get(kname, (0.0, 0))[0]
                 ach = butterflies_per_ct(cfg, p) * B / (seg[p] / 1e3)
-                kach = butterflies_per_ct(cfg, p) * B * args.steps / (kms / 1e3) if kms else ach
+                # the kernel serves every path of its family (vanilla: both forms) in the timed region
+                n_paths = sum(1 for q in paths if q.split("_")[0] == p.split("_")[0] and
+                              (q.startswith("vanilla") or q == p))
+                kach = butterflies_per_ct(cfg, p) * B * args.steps * n_paths / (kms / 1e3) if kms else ach
                 pd = alu_peak_derived(clk["sm_mhz"] or 1965.0)
                 alu[p] = {"bound": "alu", "kernel": kname, "achieved": kach / 1e9, "peak": int_peak / 1e9,
                           "unit": "Gbutterfly/s", "frac": kach / int_peak, "achieved_path": ach / 1e9,
