@@ -11,18 +11,25 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArg
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
   constexpr int THREADS = G::THREADS;
+  constexpr bool STW = !G::SPLIT;  // passes A and B read a shared-memory copy of W[0, kSmemTw)
   extern __shared__ __align__(16) uint64_t sm[];
   int8_t *se1 = reinterpret_cast<int8_t *>(sm + SmemWords<G::LOGL>::value);
   int8_t *se2 = se1 + N;
+  Tw *stw = reinterpret_cast<Tw *>(se2 + N);
+  __shared__ __align__(8) uint64_t tw_mbar;
+  TwStager tws{&tw_mbar, 0};
   const size_t b = blockIdx.x / G::CLUSTER;
   const uint64_t msg = a.msg_base + b;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  if constexpr (STW) tws.init();
+  __syncthreads();
+  if constexpr (STW) tws.issue(stw, a.tw + (size_t)lo * N);
   sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ZINC_E1);
   sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2);
   __syncthreads();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const int L = a.L;
-  const int lo = blockIdx.y * a.limbs_per_cta;
-  const int hi = min(L, lo + a.limbs_per_cta);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q, two_q = c.two_q;
@@ -30,25 +37,23 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArg
     const uint64_t *z1 = a.cache + (size_t)i * N, *z2 = a.cache + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    ntt_forward<LOGN>(sm, tw, q,
-        [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
-        [&](int base, uint64_t (&v)[16]) {
-#pragma unroll
-          for (int r = 0; r < 16; r += 2) {
-            uint64_t za, zb;
-            ld2(z1 + base + r, za, zb);
-            st2_cs(ct0 + base + r, add_mod(za, canon4(v[r], q, two_q), q), add_mod(zb, canon4(v[r + 1], q, two_q), q));
-          }
-        });
-    ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); },
-        [&](int base, uint64_t (&v)[16]) {
-#pragma unroll
-          for (int r = 0; r < 16; r += 2) {
-            uint64_t za, zb;
-            ld2(z2 + base + r, za, zb);
-            st2_cs(ct1 + base + r, add_mod(za, canon4(v[r], q, two_q), q), add_mod(zb, canon4(v[r + 1], q, two_q), q));
-          }
-        });
+    if constexpr (STW) tws.wait();
+    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
+                           to_smem<LOGN>(sm), stw);
+    __syncthreads();
+    stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+      const ulonglong2 z = ld2_nc(z1 + x);
+      st2_cs(ct0 + x, add_mod(z.x, canon4(v0, q, two_q), q), add_mod(z.y, canon4(v1, q, two_q), q));
+    });
+    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); }, to_smem<LOGN>(sm), stw);
+    __syncthreads();
+    if constexpr (STW) {
+      if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
+    }
+    stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+      const ulonglong2 z = ld2_nc(z2 + x);
+      st2_cs(ct1 + x, add_mod(z.x, canon4(v0, q, two_q), q), add_mod(z.y, canon4(v1, q, two_q), q));
+    });
   }
 }
 
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) ntt_kernel(NttArgs a) {
 template <int LOGN>
 static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
   using G = Geo<LOGN>;
-  const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN);
+  const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN) + (G::SPLIT ? 0 : kSmemTw * sizeof(Tw));
   return launch_ex(zinc_ntt_kernel<LOGN>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
 }
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {

@@ -20,17 +20,30 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
   extern __shared__ __align__(16) uint64_t sm[];
   uint8_t *su = reinterpret_cast<uint8_t *>(sm + SmemWords<G::LOGL>::value);
   int8_t *se1 = reinterpret_cast<int8_t *>(su + N / 4), *se2 = se1 + N;
+  constexpr bool STW = !G::SPLIT;  // early passes read shared-memory copies of W[0, kSmemTw)
+  Tw *stw = reinterpret_cast<Tw *>(se2 + N), *sitw = stw + kSmemTw;  // sitw: COEFF form only
+  __shared__ __align__(8) uint64_t tw_mbar[2];
+  TwStager tws{&tw_mbar[0], 0}, itws{&tw_mbar[1], 0};
   const size_t b = blockIdx.x / G::CLUSTER;
   const int loff = local_off<LOGN>();
   const uint64_t msg = a.msg_base + b;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  if constexpr (STW) {
+    tws.init();
+    if (FORM == 1) itws.init();
+  }
+  __syncthreads();
+  if constexpr (STW) {
+    tws.issue(stw, a.tw + (size_t)lo * N);
+    if (FORM == 1) itws.issue(sitw, a.itw + (size_t)lo * N);
+  }
   sample_ternary_packed<THREADS>(su, N, a.seed, msg, TAG_ENC_U);
   sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1);
   sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2);
   __syncthreads();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const int L = a.L;
-  const int lo = blockIdx.y * a.limbs_per_cta;
-  const int hi = min(L, lo + a.limbs_per_cta);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q, two_q = c.two_q;
@@ -38,48 +51,51 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
+    if constexpr (STW) tws.wait();
     if (FORM == 0) {
-      ntt_forward<LOGN>(sm, tw, q,
-          [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
-          [&](int base, uint64_t (&v)[16]) {
-#pragma unroll
-            for (int r = 0; r < 16; r += 2) st2(ct0 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
-          });
-      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); },
-          [&](int base, uint64_t (&v)[16]) {
-#pragma unroll
-            for (int r = 0; r < 16; r += 2) st2(ct1 + base + r, canon4(v[r], q, two_q), canon4(v[r + 1], q, two_q));
-          });
-      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); },
-          [&](int base, uint64_t (&v)[16]) {
-#pragma unroll
-            for (int r = 0; r < 16; r += 2) {
-              uint64_t u0 = canon4(v[r], q, two_q), u1 = canon4(v[r + 1], q, two_q);
-              uint64_t p10, p11, p20, p21, a0, a1, b0, b1;
-              ld2(pk1 + base + r, p10, p11);
-              ld2(pk2 + base + r, p20, p21);
-              ld2(ct0 + base + r, a0, a1);
-              ld2(ct1 + base + r, b0, b1);
-              st2_cs(ct0 + base + r, add_mod(a0, mul_mod(p10, u0, c), q), add_mod(a1, mul_mod(p11, u1, c), q));
-              st2_cs(ct1 + base + r, add_mod(b0, mul_mod(p20, u0, c), q), add_mod(b1, mul_mod(p21, u1, c), q));
-            }
-          });
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
+                             to_smem<LOGN>(sm), stw);
+      __syncthreads();
+      stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+        st2(ct0 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
+      });
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); }, to_smem<LOGN>(sm), stw);
+      __syncthreads();
+      stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+        st2(ct1 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
+      });
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
+                             stw);
+      __syncthreads();
+      if constexpr (STW) {
+        if (i + 1 < hi) tws.issue(stw, tw + N);
+      }
+      stream_pairs<LOGN, 2>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+        const uint64_t u0 = canon4(v0, q, two_q), u1 = canon4(v1, q, two_q);
+        const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
+        uint64_t a0, a1, b0, b1;
+        ld2(ct0 + x, a0, a1);
+        ld2(ct1 + x, b0, b1);
+        st2_cs(ct0 + x, add_mod(a0, mul_mod(p1.x, u0, c), q), add_mod(a1, mul_mod(p1.y, u1, c), q));
+        st2_cs(ct1 + x, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
+      });
     } else {
-      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); },
-          [&](int base, uint64_t (&v)[16]) {
-#pragma unroll
-            for (int r = 0; r < 16; r += 2) {
-              uint64_t u0 = canon4(v[r], q, two_q), u1 = canon4(v[r + 1], q, two_q);
-              uint64_t p10, p11, p20, p21;
-              ld2(pk1 + base + r, p10, p11);
-              ld2(pk2 + base + r, p20, p21);
-              st2(ct1 + base + r, mul_mod(p20, u0, c), mul_mod(p21, u1, c));
-              sm[pad16(base - loff + r)] = mul_mod(p10, u0, c);
-              sm[pad16(base - loff + r + 1)] = mul_mod(p11, u1, c);
-            }
-          });
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
+                             stw);
+      __syncthreads();
+      if constexpr (STW) {
+        if (i + 1 < hi) tws.issue(stw, tw + N);
+        itws.wait();
+      }
+      stream_pairs<LOGN, 2>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+        const uint64_t u0 = canon4(v0, q, two_q), u1 = canon4(v1, q, two_q);
+        const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
+        st2(ct1 + x, mul_mod(p2.x, u0, c), mul_mod(p2.y, u1, c));  // temporary: pk2 u^
+        sm[pad16(x - loff)] = mul_mod(p1.x, u0, c);                 // in place: pk1 u^
+        sm[pad16(x - loff + 1)] = mul_mod(p1.y, u1, c);
+      });
       const Tw *itw = a.itw + (size_t)i * N;
-      ntt_inverse<LOGN>(sm, itw, c,
+      ntt_inverse<LOGN, STW>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
@@ -87,13 +103,21 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
           [&](int x, uint64_t v) {
             uint64_t e = reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64);
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
-          });
-      ntt_inverse<LOGN>(sm, itw, c,
+          }, sitw);
+      __syncthreads();  // the inverse's last stores may still read sm (split exchange) -- and ct1 temp visibility
+      load_share<LOGN>(sm, ct1);
+      ntt_inverse<LOGN, STW>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-            for (int r = 0; r < 16; r += 2) ld2(ct1 + base + r, v[r], v[r + 1]);
+            for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
-          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), reduce_small(se2[x], q), q)); });
+          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), reduce_small(se2[x], q), q)); }, sitw);
+      if constexpr (STW) {
+        if (i + 1 < hi) {
+          __syncthreads();  // every thread is past the inverse's smem-twiddle passes
+          itws.issue(sitw, itw + N);
+        }
+      }
     }
   }
 }
@@ -101,7 +125,8 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
 template <int LOGN>
 static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
   using G = Geo<LOGN>;
-  const size_t smem = ntt_smem_bytes<LOGN>() + (1 << LOGN) / 4 + 2 * (1 << LOGN);
+  const size_t twb = G::SPLIT ? 0 : (size_t)(form == 0 ? 1 : 2) * kSmemTw * sizeof(Tw);
+  const size_t smem = ntt_smem_bytes<LOGN>() + (1 << LOGN) / 4 + 2 * (1 << LOGN) + twb;
   if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
   return launch_ex(vanilla_kernel<LOGN, 1>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
 }

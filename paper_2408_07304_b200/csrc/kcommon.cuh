@@ -59,6 +59,55 @@ ZINC_DEV ulonglong2 ld2_nc(const void *p) {
   return v;
 }
 
+// ============================================================ smem epilogues
+// Transform outputs go back into the CTA's own shared-memory buffer (final-pass
+// groups are disjoint and each is read before it is written, so this is safe in
+// place); after a barrier a streaming epilogue walks the buffer in coalesced
+// word pairs.  Decoupling the epilogue's global loads (cache, pk, ct) from the
+// butterflies lets U iterations of 16-byte loads be in flight per thread
+// instead of exposing one L2 round trip per 16-word group.
+template <int LOGN>
+ZINC_DEV auto to_smem(uint64_t *sm) {
+  const int loff = local_off<LOGN>();
+  return [sm, loff](int base, uint64_t (&v)[16]) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = v[r];
+  };
+}
+// f(xg, v0, v1): words xg, xg + 1 (global, xg even) of this CTA's share.
+template <int LOGN, int U = 4, class F>
+ZINC_DEV void stream_pairs(const uint64_t *sm, F f) {
+  constexpr int NL = Geo<LOGN>::NL, THREADS = Geo<LOGN>::THREADS;
+  static_assert(NL % (2 * THREADS * U) == 0, "epilogue tiling");
+  const int loff = local_off<LOGN>();
+#pragma unroll 1
+  for (int x0 = 2 * threadIdx.x; x0 < NL; x0 += 2 * THREADS * U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int x = x0 + u * 2 * THREADS;
+      f(x + loff, sm[pad16(x)], sm[pad16(x + 1)]);
+    }
+  }
+}
+// Coalesced prologue: the CTA's share of a global limb into the smem buffer.
+template <int LOGN, int U = 4>
+ZINC_DEV void load_share(uint64_t *sm, const uint64_t *src) {
+  constexpr int NL = Geo<LOGN>::NL, THREADS = Geo<LOGN>::THREADS;
+  const int loff = local_off<LOGN>();
+#pragma unroll 1
+  for (int x0 = 2 * threadIdx.x; x0 < NL; x0 += 2 * THREADS * U) {
+    ulonglong2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = *reinterpret_cast<const ulonglong2 *>(src + loff + x0 + u * 2 * THREADS);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int x = x0 + u * 2 * THREADS;
+      sm[pad16(x)] = v[u].x;
+      sm[pad16(x + 1)] = v[u].y;
+    }
+  }
+}
+
 // ============================================================ TMA bulk copies
 // 1-D bulk async copies global -> shared (cp.async.bulk, the non-tensor TMA
 // path) completing on an mbarrier transaction count.
@@ -81,6 +130,29 @@ ZINC_DEV void mbar_wait(uint64_t *mbar, uint32_t parity) {
                  : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
   }
 }
+
+// Twiddle-table entries [0, kSmemTw) of one limb, staged into shared memory by
+// one TMA bulk copy on a dedicated mbarrier (one phase per staged limb).
+struct TwStager {
+  uint64_t *mbar;
+  uint32_t phase;
+  ZINC_DEV void init() {
+    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    phase = 0;
+  }
+  // caller: every thread of the CTA has finished reading dst (a barrier precedes)
+  ZINC_DEV void issue(Tw *dst, const Tw *src) {
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(mbar, (uint32_t)(kSmemTw * sizeof(Tw)));
+      bulk_g2s(dst, src, (uint32_t)(kSmemTw * sizeof(Tw)), mbar);
+    }
+  }
+  ZINC_DEV void wait() {
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+  }
+};
 
 // ============================================================ launchers
 template <class K>

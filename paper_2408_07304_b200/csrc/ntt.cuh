@@ -37,7 +37,9 @@ struct SmemWords { static constexpr int value = (1 << LOGN) + ((1 << LOGN) >> 4)
 // Load(idx) -> uint64 in [0, 4q); Store(idx, v) with v in [0, 4q).  With
 // GROUPED, Store is called once per group as store(base, v) with the 2^K words
 // of the group (T == 1: contiguous words base .. base + 2^K - 1).
-template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, class Load, class Store>
+// SMEM_TW: `tw` points to a shared-memory copy of the table (the early passes'
+// indices are all < kSmemTw).
+template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool SMEM_TW = false, class Load, class Store>
 ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, Store store) {
   constexpr int N = 1 << LOGN;
   constexpr int G = 1 << K;
@@ -56,7 +58,7 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
       const int D = G >> (l + 1);
 #pragma unroll
       for (int blk = 0; blk < (1 << l); ++blk) {
-        const Tw w = ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
+        const Tw w = SMEM_TW ? tw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
         for (int j = 0; j < D; ++j) ct_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
       }
@@ -74,7 +76,8 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
 // Load -> [0, 2q); Store gets [0, 2q).  When LAST (S0 == 0), stage 0 multiplies
 // the sum by N^-1 and the difference by N^-1 psi^-brv(1) (folded scaling).
 // With GROUPED, Load is called once per group as load(base, v).
-template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool FOLD = true, class Load, class Store>
+template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool FOLD = true, bool SMEM_TW = false,
+          class Load, class Store>
 ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Load load, Store store) {
   constexpr int N = 1 << LOGN;
   constexpr int G = 1 << K;
@@ -108,7 +111,7 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Lo
       } else {
 #pragma unroll
         for (int blk = 0; blk < (1 << l); ++blk) {
-          const Tw w = ldtw(itw + (tb << (S0 + l)) + (beta << l) + blk);
+          const Tw w = SMEM_TW ? itw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(itw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
           for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
         }
@@ -173,8 +176,12 @@ template <int LOGN> ZINC_DEV int local_off() {
 // Forward NTT: pass A from `load(x)` (x a global index, value in [0, 4q)),
 // passes B, C through smem; `gstore(base, v[16])` receives each group of 16
 // contiguous outputs (bit-reversed NTT order, C-3) at global position base.
-template <int LOGN, class Load, class GStore>
-ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GStore gstore) {
+// Entries of the twiddle tables the early passes touch (stages < SB + KB <= 10):
+// kernels may stage them in shared memory (STW) and pass the copy as `stw`.
+constexpr int kSmemTw = 1024;
+
+template <int LOGN, bool STW = false, class Load, class GStore>
+ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GStore gstore, const Tw *stw = nullptr) {
   using G = Geo<LOGN>;
   using P = Plan<G::LOGL>;
   constexpr int LL = G::LOGL;
@@ -183,10 +190,11 @@ ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GSt
   auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
   auto sld = [&](int i) { return sm[pad16(i)]; };
   __syncthreads();  // the previous transform may still read sm
+  static_assert(!STW || (!G::SPLIT && (1 << (SC)) <= kSmemTw), "smem twiddles cover passes A and B");
   if constexpr (!G::SPLIT) {
-    ct_pass<LL, 0, P::KA, P::THREADS>(tw, q, 1, load, sst);
+    ct_pass<LL, 0, P::KA, P::THREADS, false, STW>(STW ? stw : tw, q, 1, load, sst);
     __syncthreads();
-    ct_pass<LL, SB, P::KB, P::THREADS>(tw, q, 1, sld, sst);
+    ct_pass<LL, SB, P::KB, P::THREADS, false, STW>(STW ? stw : tw, q, 1, sld, sst);
     __syncthreads();
     ct_pass<LL, SC, P::KC, P::THREADS, true>(tw, q, 1, sld, gstore);
   } else {
@@ -213,8 +221,9 @@ ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GSt
 // outputs in [0, 2q) at global indices, lane-consecutive (coalesced).  When
 // split, every store happens after both CTAs of the pair consumed their inputs
 // (in-place use is safe).
-template <int LOGN, class GLoad, class Store>
-ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad gload, Store store) {
+template <int LOGN, bool STW = false, class GLoad, class Store>
+ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad gload, Store store,
+                          const Tw *sitw = nullptr) {
   using G = Geo<LOGN>;
   using P = Plan<G::LOGL>;
   constexpr int LL = G::LOGL;
@@ -222,12 +231,13 @@ ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad
   auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
   auto sld = [&](int i) { return sm[pad16(i)]; };
   __syncthreads();
+  static_assert(!STW || (!G::SPLIT && (1 << (SC)) <= kSmemTw), "smem twiddles cover passes B' and A'");
   if constexpr (!G::SPLIT) {
     gs_pass<LL, SC, P::KC, P::THREADS, true>(itw, c, 1, gload, sst);
     __syncthreads();
-    gs_pass<LL, SB, P::KB, P::THREADS>(itw, c, 1, sld, sst);
+    gs_pass<LL, SB, P::KB, P::THREADS, false, true, STW>(STW ? sitw : itw, c, 1, sld, sst);
     __syncthreads();
-    gs_pass<LL, 0, P::KA, P::THREADS>(itw, c, 1, sld, store);
+    gs_pass<LL, 0, P::KA, P::THREADS, false, true, STW>(STW ? sitw : itw, c, 1, sld, store);
   } else {
     const int r = (int)cluster_rank();
     const int tb = 2 + r;
