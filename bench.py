@@ -68,9 +68,11 @@ def bytes_per_ct(cfg, kind="slots"):
 
 
 def alu_peak_derived(sm_mhz):
-    """Lazy Shoup butterfly = 13 fma-pipe + 14 alu-pipe instructions; both pipes issue
-    64 lanes/clk/SM (B300_MICROARCH.md: rt_SMSP = 2), so the alu pipe bounds it at 14/64 clk per SM."""
-    return 148 * sm_mhz * 1e6 * 64.0 / 14.0
+    """The lazy Shoup butterfly as compiled (SASS of int_peak_kernel): 14.9 fma-pipe
+    (IMAD family) + 15.0 alu-pipe instructions, 30 issue slots.  Both pipes take 64 lanes/clk/SM
+    (B300_MICROARCH.md: rt_SMSP = 2) and issue is 128 lanes/clk/SM, so 15/64 clk per butterfly
+    per SM bounds it: 148 x f_sm x 64 / 15."""
+    return 148 * sm_mhz * 1e6 * 64.0 / 15.0
 
 
 def butterflies_per_ct(cfg, path):
@@ -253,6 +255,58 @@ def c5_sweep(Z, torch, ctx_cache, batches=(1, 16, 256, 4096, 65536), reps=3):
     return out
 
 
+def _timed(torch, fn, n):
+    fn()
+    ts = []
+    for _ in range(n):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def other_configs(Z, torch, names=("C1", "C2", "C4"), reps=2):
+    """The other BASELINE configs on one GPU (parity-tested in tests/): ct/s of the four
+    encryption paths from slots and of batched decrypt+decode, device
+    time with CUDA events (1 warm-up + `reps`, median).  Each config's full batch."""
+    out = {}
+    for name in names:
+        cfg = CONFIGS[name]
+        ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
+        sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
+        cache = {f: Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, f) for f in (Z.COEFF, Z.NTT)}
+        B = cfg.batch
+        z = slots_batch(cfg, 0, B)
+        if cfg.complex_slots:
+            z = np.stack([z.real, z.imag], axis=-1)
+        zd = torch.from_numpy(np.ascontiguousarray(z)).cuda()
+        ct = ctx.empty_ct(B)
+        r = {"N": cfg.n, "L": cfg.L, "batch": B}
+        for pname, fn in (
+                ("zinc_coeff", lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, zd, cfg.enc_seed, 0, out=ct)),
+                ("zinc_ntt", lambda: Z.zinc_encrypt_batch(ctx, cache[Z.NTT], Z.NTT, zd, cfg.enc_seed, 0, out=ct)),
+                ("vanilla_ntt", lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, zd, cfg.enc_seed, 0, out=ct)),
+                ("vanilla_coeff", lambda: Z.ckks_encrypt_batch(ctx, pk, Z.COEFF, zd, cfg.enc_seed, 0, out=ct))):
+            ms = _timed(torch, fn, reps)
+            r[pname] = {"ms": ms, "ct_per_s": B / (ms / 1e3)}
+        # f1: batched decrypt + decode of the last (vanilla COEFF) ciphertexts, checked
+        ms = _timed(torch, lambda: Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct), reps)
+        _, st, zz = Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct[:64])
+        ref = slots_batch(cfg, 0, min(B, 64))
+        err = float(np.max(np.abs(zz.cpu().numpy() - ref)))
+        r["decrypt_decode_coeff"] = {"ms": ms, "ct_per_s": B / (ms / 1e3), "max_abs_err_64": err,
+                                     "crt_ok": int(st.sum().item()) == 0, "tolerance": cfg.tolerance()}
+        r["ok"] = r["decrypt_decode_coeff"]["crt_ok"] and err < cfg.tolerance()
+        out[name] = r
+        del ct, zd
+        ctx.close()
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -268,6 +322,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 batch sweep")
+    ap.add_argument("--no-others", action="store_true", help="skip the C1/C2/C4 single-GPU lines")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -421,7 +476,7 @@ def main():
                           "peak_derived": pd / 1e9, "frac_of_derived": kach / pd,
                           "butterflies_per_ct": butterflies_per_ct(cfg, p),
                           "peak_source": "measured int_peak_kernel (K11), lazy Shoup butterflies; peak_derived: "
-                                         "148 SMs x sm_mhz x 64 alu lanes/clk / 14 alu ops per butterfly"}
+                                         "148 SMs x sm_mhz x 64 lanes/clk / 15 fma- or alu-pipe ops per butterfly"}
         result = {
             "metric": METRIC,
             "value": path_out["zinc_coeff"]["ct_per_s"] if "zinc_coeff" in path_out else None,
@@ -451,11 +506,24 @@ def main():
             "broadcast_ok": bcast_ok,
         }
 
+    if rank == 0 and "vanilla_coeff" in paths:
+        # batched decrypt + decode (Eq. 10, CRT check on every limb) of the
+        # step's last output (vanilla COEFF form), device-timed like the paths
+        dms = _timed(torch, lambda: Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct), 3)
+        result["decrypt_decode"] = {"form": "COEFF", "ms": dms, "ct_per_s": B / (dms / 1e3),
+                                    "transforms_per_ct": 2 * cfg.L,
+                                    "note": "x = c1 + c2 s on every limb (NTT + INTT per limb), CRT check, FP64 decode"}
     if rank == 0 and world == 1 and not args.no_c5:
         del ct
         torch.cuda.empty_cache()
         result["c5"] = c5_sweep(Z, torch, None)
         ct = None
+    if rank == 0 and world == 1 and not args.no_others:
+        if ct is not None:
+            del ct
+            ct = None
+            torch.cuda.empty_cache()
+        result["other_configs"] = other_configs(Z, torch)
 
     # ---------------- end to end through the host-buffer API
     if not args.no_e2e:
