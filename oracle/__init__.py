@@ -84,6 +84,13 @@ def _declare(L):
         "orc_zinc_encrypt": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_int, _i64p, _c.c_uint64, _c.c_uint64, _u64p]),
         "orc_decrypt": (_c.c_int, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _u64p, _c.c_int, _i64p, _u64p]),
         "orc_ntt_limbs": (None, [_u64p, _c.c_int, _c.c_int, _u64p, _u64p]),
+        "orc_keygen_scaled": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _c.c_uint64, _c.c_int64, _i64p, _u64p, _u64p]),
+        "orc_bfv_delta_mod": (_c.c_uint64, [_c.c_int, _u64p, _c.c_uint64, _c.c_int]),
+        "orc_plaintext_residues": (None, [_c.c_int, _c.c_uint64, _c.c_int, _c.c_int, _u64p, _i64p, _u64p]),
+        "orc_encrypt_general_explicit": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _u64p, _i64p, _i64p, _i64p, _c.c_int64, _c.c_int, _u64p]),
+        "orc_encrypt_scheme": (None, [_c.c_int, _c.c_uint64, _c.c_int, _c.c_int, _u64p, _u64p, _u64p, _i64p, _c.c_uint64, _c.c_uint64, _c.c_int, _u64p]),
+        "orc_precompute_cache_scheme": (None, [_c.c_int, _c.c_uint64, _c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_uint64, _c.c_int, _u64p]),
+        "orc_zinc_encrypt_scheme": (None, [_c.c_int, _c.c_uint64, _c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_int, _i64p, _c.c_uint64, _c.c_uint64, _u64p]),
         "orc_intt_limbs": (None, [_u64p, _c.c_int, _c.c_int, _u64p, _u64p]),
     }
     for name, (res, args) in sig.items():
@@ -317,3 +324,88 @@ def counters():
     t = ctypes.c_uint64(); p = ctypes.c_uint64()
     lib().orc_counters_get(ctypes.byref(t), ctypes.byref(p))
     return int(t.value), int(p.value)
+
+
+# ---------------------------------------------------------------- BFV / BGV (section 4.2)
+CKKS, BFV, BGV = 0, 1, 2
+
+
+def keygen_scheme(P: Params, seed: int, scheme: int, t: int = 0):
+    """Gen with BGV's t-scaled key error (reading A17); CKKS / BFV equal `keygen`."""
+    sk = np.zeros(P.n, dtype=np.int64)
+    sk_ntt = np.zeros((P.L, P.n), dtype=np.uint64)
+    pk = np.zeros((2, P.L, P.n), dtype=np.uint64)
+    lib().orc_keygen_scaled(*P._args(), seed, t if scheme == BGV else 1, _p(sk, _i64p), _p(sk_ntt, _u64p),
+                            _p(pk, _u64p))
+    return sk, sk_ntt, pk
+
+
+def bfv_delta_mod(P: Params, t: int):
+    return [int(lib().orc_bfv_delta_mod(P.L, _p(P.q, _u64p), t, i)) for i in range(P.L)]
+
+
+def plaintext_residues(P: Params, scheme: int, t: int, m) -> np.ndarray:
+    m = _i64(m)
+    out = np.zeros((P.L, P.n), dtype=np.uint64)
+    lib().orc_plaintext_residues(scheme, t, P.log_n, P.L, _p(P.q, _u64p), _p(m, _i64p), _p(out, _u64p))
+    return out
+
+
+def encrypt_general_explicit(P: Params, pk, pt_res, u, e1, e2, es: int, form: int) -> np.ndarray:
+    pk, pt_res, u, e1, e2 = _u64(pk), _u64(pt_res), _i64(u), _i64(e1), _i64(e2)
+    ct = np.zeros((2, P.L, P.n), dtype=np.uint64)
+    lib().orc_encrypt_general_explicit(*P._args(), _p(pk, _u64p), _p(pt_res, _u64p), _p(u, _i64p), _p(e1, _i64p),
+                                       _p(e2, _i64p), es, form, _p(ct, _u64p))
+    return ct
+
+
+def encrypt_scheme(P: Params, scheme: int, t: int, pk, m, seed: int, msg: int, form: int) -> np.ndarray:
+    pk, m = _u64(pk), _i64(m)
+    ct = np.zeros((2, P.L, P.n), dtype=np.uint64)
+    lib().orc_encrypt_scheme(scheme, t, *P._args(), _p(pk, _u64p), _p(m, _i64p), seed, msg, form, _p(ct, _u64p))
+    return ct
+
+
+def precompute_cache_scheme(P: Params, scheme: int, t: int, pk, cache_seed: int, form: int) -> np.ndarray:
+    pk = _u64(pk)
+    cache = np.zeros((2, P.L, P.n), dtype=np.uint64)
+    lib().orc_precompute_cache_scheme(scheme, t, *P._args(), _p(pk, _u64p), cache_seed, form, _p(cache, _u64p))
+    return cache
+
+
+def zinc_encrypt_scheme(P: Params, scheme: int, t: int, cache, form: int, m, seed: int, msg: int) -> np.ndarray:
+    cache, m = _u64(cache), _i64(m)
+    ct = np.zeros((2, P.L, P.n), dtype=np.uint64)
+    lib().orc_zinc_encrypt_scheme(scheme, t, *P._args(), _p(cache, _u64p), form, _p(m, _i64p), seed, msg,
+                                  _p(ct, _u64p))
+    return ct
+
+
+def crt_centered(P: Params, x_limbs) -> list:
+    """x in (-Q/2, Q/2] from its residues [L][N] (plain big-integer CRT, Python ints)."""
+    q = [int(v) for v in P.q]
+    Q = 1
+    for v in q:
+        Q *= v
+    coef = []
+    for i, qi in enumerate(q):
+        Qi = Q // qi
+        coef.append(Qi * pow(Qi % qi, -1, qi))
+    out = []
+    xl = [[int(v) for v in row] for row in np.asarray(x_limbs)]
+    for j in range(P.n):
+        x = sum(xl[i][j] * coef[i] for i in range(P.L)) % Q
+        out.append(x - Q if x > Q // 2 else x)
+    return out, Q
+
+
+def decrypt_scheme(P: Params, scheme: int, t: int, sk_ntt, ct, form: int) -> np.ndarray:
+    """BFV: m = round(t.x/Q) mod t; BGV: m = x mod t; x = [c1 + c2.sk]_Q centred
+    (Eq. 10 with the decoders of the original schemes)."""
+    _, _, xl = decrypt(P, sk_ntt, ct, form, want_limbs=True)
+    xs, Q = crt_centered(P, xl)
+    if scheme == BFV:
+        m = [((2 * t * x + Q) // (2 * Q)) % t for x in xs]  # round half up of t x / Q
+    else:
+        m = [x % t for x in xs]
+    return np.array(m, dtype=np.int64)

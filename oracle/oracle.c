@@ -469,8 +469,17 @@ void orc_decode_fft(const int64_t *x, int log_n, int log_scale, double *z_re, do
 /* a <- R_q, e <- chi; pk1 = [-a.sk + e]_q, pk2 = a.  Stored in NTT form.    */
 /* Outputs: sk_coeff [N] (int64 in {-1,0,1}), sk_ntt [L][N], pk_ntt [2][L][N]*/
 /* ------------------------------------------------------------------------ */
+/* e_scale = 1 (CKKS, BFV) or t (BGV, reading A17: pk1 = [-a.sk + t.e]_q). */
+void orc_keygen_scaled(int log_n, int num_limbs, const uint64_t *q, const uint64_t *psi,
+                       uint64_t seed, int64_t e_scale, int64_t *sk_coeff, uint64_t *sk_ntt,
+                       uint64_t *pk_ntt);
 void orc_keygen(int log_n, int num_limbs, const uint64_t *q, const uint64_t *psi, uint64_t seed,
                 int64_t *sk_coeff, uint64_t *sk_ntt, uint64_t *pk_ntt) {
+  orc_keygen_scaled(log_n, num_limbs, q, psi, seed, 1, sk_coeff, sk_ntt, pk_ntt);
+}
+void orc_keygen_scaled(int log_n, int num_limbs, const uint64_t *q, const uint64_t *psi,
+                       uint64_t seed, int64_t e_scale, int64_t *sk_coeff, uint64_t *sk_ntt,
+                       uint64_t *pk_ntt) {
   uint64_t n = 1ull << log_n;
   int64_t *e = (int64_t *)malloc(sizeof(int64_t) * n);
   uint64_t *a = (uint64_t *)malloc(sizeof(uint64_t) * n);
@@ -483,7 +492,7 @@ void orc_keygen(int log_n, int num_limbs, const uint64_t *q, const uint64_t *psi
     orc_sample_uniform(seed, 0, TAG_PK_A, (uint32_t)i, qi, (int)n, a);
     for (uint64_t j = 0; j < n; j++) {
       s_l[j] = residue_i64(sk_coeff[j], qi);
-      e_l[j] = residue_i64(e[j], qi);
+      e_l[j] = residue_i64(e[j] * e_scale, qi);
     }
     orc_ntt(a, log_n, qi, psi[i]);
     orc_ntt(s_l, log_n, qi, psi[i]);
@@ -678,6 +687,125 @@ int orc_decrypt(int log_n, int num_limbs, const uint64_t *q, const uint64_t *psi
   if (x_limbs) memcpy(x_limbs, x, sizeof(uint64_t) * n * (uint64_t)num_limbs);
   free(x); free(t);
   return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Scheme variants, PAPER.md:319-343 (section 4.2).  The plaintext space is  */
+/* Z_t/(X^N+1); a plaintext coefficient is taken as its residue m mod t in   */
+/* [0, t) (reading A18).                                                     */
+/*   BFV, Eq. 12:  c1 = [pk1.u + e1 + Delta.m]_Q, Delta = floor(Q/t);        */
+/*                 Zinc "without modification".               */
+/*   BGV, Eq. 13:  c1 = [pk1.u + t.e1 + m]_Q, c2 = [pk2.u + t.e2]_Q;          */
+/*                 Zinc adds t.e1', t.e2'.                     */
+/* (c2 uses pk2, reading A1, as for CKKS.)  scheme: 0 CKKS, 1 BFV, 2 BGV.    */
+/* ------------------------------------------------------------------------ */
+static uint64_t mod_t(int64_t m, uint64_t t) {
+  i128 r = (i128)m % (i128)t;
+  if (r < 0) r += (i128)t;
+  return (uint64_t)r;
+}
+/* Delta mod q_i with Delta = floor(Q/t), Q = prod q_k, exactly and without big
+ * integers: Q = Delta.t + (Q mod t) and q_i | Q give
+ * Delta = -(Q mod t) . t^{-1}  (mod q_i). */
+uint64_t orc_bfv_delta_mod(int num_limbs, const uint64_t *q, uint64_t t, int i) {
+  uint64_t qmod_t = 1 % t;
+  for (int k = 0; k < num_limbs; k++) qmod_t = (uint64_t)(((u128)qmod_t * (q[k] % t)) % t);
+  uint64_t tinv = powmod(t % q[i], q[i] - 2, q[i]); /* q_i prime, t < q_i */
+  return mulmod(submod(0, qmod_t % q[i], q[i]), tinv, q[i]);
+}
+/* Residues [L][N] of the scheme's plaintext term: CKKS m; BFV Delta.(m mod t); BGV m mod t. */
+void orc_plaintext_residues(int scheme, uint64_t t, int log_n, int num_limbs, const uint64_t *q,
+                            const int64_t *m, uint64_t *out) {
+  uint64_t n = 1ull << log_n;
+  for (int i = 0; i < num_limbs; i++) {
+    uint64_t delta = scheme == 1 ? orc_bfv_delta_mod(num_limbs, q, t, i) : 1;
+    for (uint64_t j = 0; j < n; j++) {
+      uint64_t v;
+      if (scheme == 0) v = residue_i64(m[j], q[i]);
+      else v = mulmod(delta, mod_t(m[j], t) % q[i], q[i]);
+      out[(uint64_t)i * n + j] = v;
+    }
+  }
+}
+/* General explicit encryption: c1 = [pk1.u + es.e1 + pt]_q, c2 = [pk2.u + es.e2]_q
+ * with pt given as residues [L][N] and es the error scale (1, or t for BGV). */
+void orc_encrypt_general_explicit(int log_n, int num_limbs, const uint64_t *q,
+                                  const uint64_t *psi, const uint64_t *pk_ntt,
+                                  const uint64_t *pt_res, const int64_t *u, const int64_t *e1,
+                                  const int64_t *e2, int64_t es, int form, uint64_t *ct) {
+  uint64_t n = 1ull << log_n;
+  int64_t *zero = (int64_t *)calloc(n, sizeof(int64_t));
+  int64_t *se1 = (int64_t *)malloc(sizeof(int64_t) * n);
+  int64_t *se2 = (int64_t *)malloc(sizeof(int64_t) * n);
+  for (uint64_t j = 0; j < n; j++) {
+    se1[j] = e1[j] * es;
+    se2[j] = e2[j] * es;
+  }
+  /* Eq. 8 structure with m = 0, then + pt (same ring element in either form) */
+  orc_vanilla_encrypt_explicit(log_n, num_limbs, q, psi, pk_ntt, zero, u, se1, se2, form, ct);
+  uint64_t *p = (uint64_t *)malloc(sizeof(uint64_t) * n);
+  for (int i = 0; i < num_limbs; i++) {
+    memcpy(p, pt_res + (uint64_t)i * n, sizeof(uint64_t) * n);
+    if (form == 0) orc_ntt(p, log_n, q[i], psi[i]);
+    for (uint64_t j = 0; j < n; j++) ct[(uint64_t)i * n + j] = addmod(ct[(uint64_t)i * n + j], p[j], q[i]);
+  }
+  free(zero); free(se1); free(se2); free(p);
+}
+void orc_encrypt_scheme(int scheme, uint64_t t, int log_n, int num_limbs, const uint64_t *q,
+                        const uint64_t *psi, const uint64_t *pk_ntt, const int64_t *m,
+                        uint64_t seed, uint64_t msg, int form, uint64_t *ct) {
+  uint64_t n = 1ull << log_n;
+  int64_t *u = (int64_t *)malloc(sizeof(int64_t) * n);
+  int64_t *e1 = (int64_t *)malloc(sizeof(int64_t) * n);
+  int64_t *e2 = (int64_t *)malloc(sizeof(int64_t) * n);
+  uint64_t *pt = (uint64_t *)malloc(sizeof(uint64_t) * n * (uint64_t)num_limbs);
+  orc_sample_ternary(seed, msg, TAG_ENC_U, (int)n, u);
+  orc_sample_cbd(seed, msg, TAG_ENC_E1, (int)n, e1);
+  orc_sample_cbd(seed, msg, TAG_ENC_E2, (int)n, e2);
+  orc_plaintext_residues(scheme, t, log_n, num_limbs, q, m, pt);
+  orc_encrypt_general_explicit(log_n, num_limbs, q, psi, pk_ntt, pt, u, e1, e2,
+                               scheme == 2 ? (int64_t)t : 1, form, ct);
+  free(u); free(e1); free(e2); free(pt);
+}
+/* Cache of a scheme: its Enc(0), msg = 2^64 - 1. */
+void orc_precompute_cache_scheme(int scheme, uint64_t t, int log_n, int num_limbs,
+                                 const uint64_t *q, const uint64_t *psi, const uint64_t *pk_ntt,
+                                 uint64_t cache_seed, int form, uint64_t *cache) {
+  uint64_t n = 1ull << log_n;
+  int64_t *zero = (int64_t *)calloc(n, sizeof(int64_t));
+  orc_encrypt_scheme(scheme, t, log_n, num_limbs, q, psi, pk_ntt, zero, cache_seed, UINT64_MAX,
+                     form, cache);
+  free(zero);
+}
+/* Zinc of a scheme: Algorithm 1 with the plaintext term of the scheme (line 1)
+ * and, for BGV, the injected errors scaled by t (line 3). */
+void orc_zinc_encrypt_scheme(int scheme, uint64_t t, int log_n, int num_limbs, const uint64_t *q,
+                             const uint64_t *psi, const uint64_t *cache, int form,
+                             const int64_t *m, uint64_t seed, uint64_t msg, uint64_t *ct) {
+  uint64_t n = 1ull << log_n;
+  int64_t *e1p = (int64_t *)malloc(sizeof(int64_t) * n);
+  int64_t *e2p = (int64_t *)malloc(sizeof(int64_t) * n);
+  uint64_t *pt = (uint64_t *)malloc(sizeof(uint64_t) * n * (uint64_t)num_limbs);
+  uint64_t *ep = (uint64_t *)malloc(sizeof(uint64_t) * n);
+  orc_sample_cbd(seed, msg, TAG_ZINC_E1, (int)n, e1p); /* line 2 */
+  orc_sample_cbd(seed, msg, TAG_ZINC_E2, (int)n, e2p);
+  orc_plaintext_residues(scheme, t, log_n, num_limbs, q, m, pt);
+  int64_t es = scheme == 2 ? (int64_t)t : 1;
+  for (int i = 0; i < num_limbs; i++) {
+    uint64_t qi = q[i];
+    uint64_t *p = pt + (uint64_t)i * n;
+    uint64_t *c1 = ct + (uint64_t)i * n;
+    uint64_t *c2 = ct + ((uint64_t)num_limbs + i) * n;
+    const uint64_t *z1 = cache + (uint64_t)i * n;
+    const uint64_t *z2 = cache + ((uint64_t)num_limbs + i) * n;
+    for (uint64_t j = 0; j < n; j++) ep[j] = residue_i64(e1p[j] * es, qi);
+    if (form == 0) { orc_ntt(p, log_n, qi, psi[i]); orc_ntt(ep, log_n, qi, psi[i]); }
+    for (uint64_t j = 0; j < n; j++) c1[j] = addmod(addmod(z1[j], p[j], qi), ep[j], qi);
+    for (uint64_t j = 0; j < n; j++) ep[j] = residue_i64(e2p[j] * es, qi);
+    if (form == 0) orc_ntt(ep, log_n, qi, psi[i]);
+    for (uint64_t j = 0; j < n; j++) c2[j] = addmod(z2[j], ep[j], qi);
+  }
+  free(e1p); free(e2p); free(pt); free(ep);
 }
 
 /* Plain helpers exposed for tests: forward/inverse NTT of [L][N] in place. */
