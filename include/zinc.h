@@ -78,6 +78,25 @@ zinc_status zinc_ctx_create(int log_n, int num_limbs, const int *limb_bits, int 
                             int device, zinc_ctx **out);
 zinc_status zinc_ctx_destroy(zinc_ctx *ctx);
 
+/* Scheme of a context (section 4.2). */
+typedef enum { ZINC_SCHEME_CKKS = 0, ZINC_SCHEME_BFV = 1, ZINC_SCHEME_BGV = 2 } zinc_scheme;
+
+/* zinc_ctx_create for a scheme.  CKKS: as zinc_ctx_create (plain_modulus ignored).
+ * BFV (Eq. 12): c1 = [pk1.u + e1 + Delta.m]_Q, Delta = floor(Q/t), Q = prod q_i; Zinc
+ *   unchanged.  BGV (Eq. 13): c1 = [pk1.u + t.e1 + m]_Q, c2 = [pk2.u + t.e2]_Q;
+ *   keygen uses the t-scaled key error pk1 = [-a.sk + t.e]_Q (reading A17) and Zinc injects
+ *   t.e1', t.e2'.  plain_modulus t: 2 <= t < 2^32 and t < every q_i, else
+ *   ZINC_EINVAL / ZINC_EPARAMS; log_scale is ignored for BFV / BGV.  Plaintexts of BFV / BGV
+ *   contexts are int64 coefficients (kind ZINC_PT_COEFF_I64 only); the library uses each
+ *   coefficient's residue m mod t in [0, t) (reading A18).  ckks_decrypt_batch on such a
+ *   context writes m in [0, t) to coeff_out (BGV: from limb 0 with the CRT status as for
+ *   CKKS; BFV: round(t.x/Q) mod t from every limb, status 0) and needs slots_out == NULL. */
+zinc_status zinc_ctx_create_scheme(int log_n, int num_limbs, const int *limb_bits, int scheme,
+                                   uint64_t plain_modulus, int log_scale, int device,
+                                   zinc_ctx **out);
+/* Scheme and plaintext modulus of a context (host pointers, each may be NULL). */
+zinc_status zinc_ctx_scheme(const zinc_ctx *ctx, int *scheme, uint64_t *plain_modulus);
+
 /* Host copies of the moduli q_i and roots psi_i (arrays of L, host pointers). */
 zinc_status zinc_ctx_moduli(const zinc_ctx *ctx, uint64_t *q_out, uint64_t *psi_out);
 /* N, L, log_scale of the context (host pointers, each may be NULL). */
@@ -180,7 +199,8 @@ enum {
   ZINC_K_SAMPLE = 8,
   ZINC_K_INT_PEAK = 9,
   ZINC_K_ZINC_FUSED = 10, /* encode of chunk k+1 fused with Zinc add/inject of chunk k */
-  ZINC_K_COUNT = 11
+  ZINC_K_BFV_SCALE = 11, /* BFV decryption: round(t.x/Q) mod t from the RNS residues */
+  ZINC_K_COUNT = 12
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */

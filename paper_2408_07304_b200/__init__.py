@@ -28,6 +28,7 @@ __all__ = [
 ]
 
 NTT, COEFF = 0, 1
+CKKS, BFV, BGV = 0, 1, 2
 PT_COEFF_I64, PT_SLOTS_F64, PT_SLOTS_C128 = 0, 1, 2
 PATH_ZINC, PATH_VANILLA = 0, 1
 
@@ -39,11 +40,12 @@ EXPORTED_SYMBOLS = (
     "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch", "ckks_decrypt_batch",
     "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse", "zinc_debug_sample", "zinc_int_peak",
     "zinc_encrypt_batch_host", "zinc_launch_count", "zinc_launch_count_reset", "zinc_last_error",
-    "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name", "zinc_tune",
+    "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name", "zinc_tune", "zinc_ctx_create_scheme",
+    "zinc_ctx_scheme",
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
                 "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                "zinc_coeff_encode_kernel")
+                "zinc_coeff_encode_kernel", "bfv_scale_kernel")
 
 
 class ZincError(RuntimeError):
@@ -71,6 +73,8 @@ _SIGS = {
     "zinc_profile_enable": [_i32],
     "zinc_profile_read": [_c.POINTER(_c.c_double), _c.POINTER(_u64)],
     "zinc_tune": [_i32, _c.c_longlong, _c.POINTER(_c.c_longlong)],
+    "zinc_ctx_create_scheme": [_i32, _i32, _c.POINTER(_c.c_int), _i32, _u64, _i32, _i32, _c.POINTER(_vp)],
+    "zinc_ctx_scheme": [_vp, _c.POINTER(_c.c_int), _c.POINTER(_u64)],
 }
 
 _lib = None
@@ -123,13 +127,16 @@ def _stream(stream=None):
 
 class Context:
     """A zinc_ctx: ring degree 2^log_n, RNS primes of the given bit sizes (C-1),
-    scale 2^log_scale, bound to CUDA device `device`."""
+    scale 2^log_scale, bound to CUDA device `device`; `scheme` CKKS (default),
+    BFV or BGV with plaintext modulus `t`."""
 
-    def __init__(self, log_n: int, bits, log_scale: int, device: int = 0):
+    def __init__(self, log_n: int, bits, log_scale: int, device: int = 0, scheme: int = 0, t: int = 0):
         arr = (ctypes.c_int * len(bits))(*[int(b) for b in bits])
         h = ctypes.c_void_p()
         torch.cuda.init()
-        _check(lib().zinc_ctx_create(log_n, len(bits), arr, log_scale, device, ctypes.byref(h)), "zinc_ctx_create")
+        _check(lib().zinc_ctx_create_scheme(log_n, len(bits), arr, scheme, t, log_scale, device, ctypes.byref(h)),
+               "zinc_ctx_create_scheme")
+        self.scheme, self.t = scheme, t
         self._h = h
         self.log_n, self.L, self.log_scale, self.device = log_n, len(bits), log_scale, device
         self.n = 1 << log_n
@@ -223,6 +230,7 @@ def ckks_decrypt_batch(ctx: Context, sk_ntt: torch.Tensor, form: int, ct: torch.
     b = ct.shape[0]
     coeff = torch.empty((b, ctx.n), dtype=torch.int64, device=ctx.dev())
     status = torch.empty((b,), dtype=torch.int32, device=ctx.dev())
+    slots = slots and ctx.scheme == CKKS  # BFV / BGV: coeff = m in [0, t), no slots
     z = torch.empty((b, ctx.n // 2, 2), dtype=torch.float64, device=ctx.dev()) if slots else None
     _check(lib().ckks_decrypt_batch(ctx.handle, _ptr(sk_ntt), form, _ptr(ct), b, _ptr(z), _ptr(coeff), _ptr(status),
                                     _stream(stream)), "ckks_decrypt_batch")

@@ -51,7 +51,7 @@ static uint64_t g_trace_n[ZINC_K_COUNT];
 static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel",
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
                                                  "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                                                 "zinc_coeff_encode_kernel"};
+                                                 "zinc_coeff_encode_kernel", "bfv_scale_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -100,6 +100,8 @@ static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0},
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
   int device, log_n, n, L, log_scale;
+  int scheme = ZINC_SCHEME_CKKS;
+  uint64_t t = 0;  // plaintext modulus (BFV, BGV)
   std::vector<uint64_t> q, psi;
   std::vector<LimbConst> h_limbs;
   LimbConst *d_limbs = nullptr;
@@ -262,7 +264,16 @@ zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
 
 zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scale, int device,
                             zinc_ctx **out) {
+  return zinc_ctx_create_scheme(log_n, L, limb_bits, ZINC_SCHEME_CKKS, 0, log_scale, device, out);
+}
+
+zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int scheme, uint64_t plain_modulus,
+                                   int log_scale, int device, zinc_ctx **out) {
   if (!out || !limb_bits) return fail(ZINC_EINVAL, "null argument");
+  if (scheme != ZINC_SCHEME_CKKS && scheme != ZINC_SCHEME_BFV && scheme != ZINC_SCHEME_BGV)
+    return fail(ZINC_EINVAL, "bad scheme %d", scheme);
+  if (scheme != ZINC_SCHEME_CKKS && (plain_modulus < 2 || plain_modulus >= (1ull << 32)))
+    return fail(ZINC_EINVAL, "plain modulus %llu outside [2, 2^32)", (unsigned long long)plain_modulus);
   *out = nullptr;
   if (log_n < 12 || log_n > 15) return fail(ZINC_EINVAL, "log_n %d outside [12, 15]", log_n);
   if (L < 1 || L > 32) return fail(ZINC_EINVAL, "num_limbs %d outside [1, 32]", L);
@@ -272,6 +283,8 @@ zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scal
       return fail(ZINC_EINVAL, "limb %d: %d bits outside [20, 60]", i, limb_bits[i]);
   zinc_ctx *c = new zinc_ctx();
   c->device = device;
+  c->scheme = scheme;
+  c->t = scheme == ZINC_SCHEME_CKKS ? 0 : plain_modulus;
   c->log_n = log_n;
   c->n = 1 << log_n;
   c->L = L;
@@ -279,6 +292,8 @@ zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scal
   if (!gen_primes(log_n, L, limb_bits, c->q)) { delete c; return fail(ZINC_EPARAMS, "no prime found"); }
   for (int i = 1; i < L; ++i)
     if (c->q[i] > c->q[0]) { delete c; return fail(ZINC_EPARAMS, "limb 0 must hold the largest prime (C-10)"); }
+  for (int i = 0; i < L; ++i)
+    if (c->t && c->t >= c->q[i]) { delete c; return fail(ZINC_EPARAMS, "plain modulus must be below every q_i"); }
   const int n = c->n;
   std::vector<Tw> tw((size_t)L * n), itw((size_t)L * n);
   c->psi.resize(L);
@@ -306,6 +321,31 @@ zinc_status zinc_ctx_create(int log_n, int L, const int *limb_bits, int log_scal
     lc.ninv_sh = shoup(lc.ninv, q);
     lc.ninv_w = mulm(lc.ninv, itw[(size_t)i * n + 1].x, q);
     lc.ninv_w_sh = shoup(lc.ninv_w, q);
+    // scheme constants (section 4.2)
+    lc.scheme = (uint32_t)scheme;
+    if (c->t) {
+      const uint64_t t = c->t;
+      lc.t = t;
+      lc.t_mu = (uint64_t)(((u128)1 << 64) / t);
+      // Delta = floor(Q/t) mod q_i = -(Q mod t) t^-1 mod q_i  (Q = Delta t + (Q mod t), q_i | Q)
+      uint64_t qmod_t = 1 % t;
+      for (int k = 0; k < L; ++k) qmod_t = (uint64_t)((u128)qmod_t * (c->q[k] % t) % t);
+      const uint64_t tinv = powm(t, q - 2, q);
+      lc.delta = mulm((q - qmod_t % q) % q, tinv, q);
+      lc.delta_sh = shoup(lc.delta, q);
+      // BFV decryption: t Q~_i / q_i = I_i + F_i with Q~_i = (Q/q_i)^-1 mod q_i
+      uint64_t qt = 1;
+      for (int k = 0; k < L; ++k)
+        if (k != i) qt = mulm(qt, c->q[k] % q, q);
+      const uint64_t qtilde = powm(qt, q - 2, q);
+      const u128 num = (u128)t * qtilde;
+      uint64_t ip = (uint64_t)(num / q);
+      const u128 rem = num % q;
+      u128 f = ((rem << 64) + q / 2) / q;  // round(F_i 2^64)
+      if (f >> 64) { f = 0; ip += 1; }
+      lc.dec_i = ip % t;
+      lc.dec_f = (uint64_t)f;
+    }
   }
   // FFT tables for encode / decode (C-6): M = N/2
   const int M = n / 2, log_m = log_n - 1;
@@ -362,6 +402,13 @@ zinc_status zinc_ctx_moduli(const zinc_ctx *ctx, uint64_t *q_out, uint64_t *psi_
     if (q_out) q_out[i] = ctx->q[i];
     if (psi_out) psi_out[i] = ctx->psi[i];
   }
+  return ZINC_OK;
+}
+
+zinc_status zinc_ctx_scheme(const zinc_ctx *ctx, int *scheme, uint64_t *plain_modulus) {
+  if (!ctx) return fail(ZINC_EINVAL, "null ctx");
+  if (scheme) *scheme = ctx->scheme;
+  if (plain_modulus) *plain_modulus = ctx->t;
   return ZINC_OK;
 }
 
@@ -585,6 +632,8 @@ static zinc_status check_encrypt(const zinc_ctx *c, const uint64_t *key, int for
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_form(form)) || (st = check_kind(kind)) || (st = check_ptrs({key, pt, ct}))) return st;
+  if (c->scheme != ZINC_SCHEME_CKKS && kind != ZINC_PT_COEFF_I64)
+    return fail(ZINC_EINVAL, "BFV / BGV contexts take integer plaintext coefficients (ZINC_PT_COEFF_I64)");
   if (cudaSetDevice(c->device) != cudaSuccess) return fail(ZINC_ECUDA, "cudaSetDevice failed");
   return ZINC_OK;
 }
@@ -645,6 +694,8 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
   if ((st = check_form(form)) || (st = check_ptrs({sk_ntt, ct}))) return st;
   for (const void *p : {(const void *)slots_out, (const void *)coeff_out, (const void *)status_out})
     if (p && ((uintptr_t)p & 7u)) return fail(ZINC_EINVAL, "output pointer misaligned");
+  if (c->scheme != ZINC_SCHEME_CKKS && slots_out)
+    return fail(ZINC_EINVAL, "BFV / BGV decryption has no slot decoding (slots_out must be NULL)");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = (cudaStream_t)stream;
   int64_t *x = coeff_out;
@@ -658,6 +709,11 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
   a.coeff_out = x;
   a.status_out = status_out;
   a.L = c->L;
+  uint64_t *xl = nullptr;
+  if (c->scheme == ZINC_SCHEME_BFV) {
+    CUDA_TRY(cudaMallocAsync((void **)&xl, batch * (size_t)c->L * c->n * 8, s));
+    a.xl_out = xl;
+  }
   st = ZINC_OK;
   {
     cudaError_t e;
@@ -668,6 +724,18 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
     g_launches.fetch_add(1);
     if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decrypt launch: %s", cudaGetErrorString(e));
   }
+  if (st == ZINC_OK && c->scheme == ZINC_SCHEME_BFV) {
+    BfvScaleArgs f{};
+    f.limbs = c->d_limbs;
+    f.xl = xl;
+    f.m_out = x;
+    f.batch = batch;
+    f.n = c->n;
+    f.L = c->L;
+    LAUNCH(ZINC_K_BFV_SCALE, s, launch_bfv_scale(f, s));
+    if (status_out) CUDA_TRY(cudaMemsetAsync(status_out, 0, batch * sizeof(int32_t), s));
+  }
+  if (xl) cudaFreeAsync(xl, s);
   if (st == ZINC_OK && slots_out) {
     DecodeArgs d{};
     d.coeff = x;

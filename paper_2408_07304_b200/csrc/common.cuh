@@ -25,7 +25,17 @@ struct LimbConst {
   uint64_t ninv_sh;  // Shoup companion of ninv
   uint64_t ninv_w;   // N^-1 * psi^-brv(1) mod q (last GS stage, folded scaling)
   uint64_t ninv_w_sh;
+  // scheme (section 4.2): the same in every limb's entry
+  uint32_t scheme;   // SCHEME_CKKS / SCHEME_BFV / SCHEME_BGV
+  uint32_t pad2;
+  uint64_t t;        // plaintext modulus (BFV, BGV), 2 <= t < 2^32
+  uint64_t t_mu;     // floor(2^64 / t)
+  uint64_t delta;    // BFV: floor(Q/t) mod q;  Shoup companion below
+  uint64_t delta_sh;
+  uint64_t dec_i;    // BFV decrypt: floor(t Q~_i / q_i) mod t, Q~_i = (Q/q_i)^-1 mod q_i
+  uint64_t dec_f;    // BFV decrypt: round(frac(t Q~_i / q_i) 2^64)
 };
+enum : uint32_t { SCHEME_CKKS = 0, SCHEME_BFV = 1, SCHEME_BGV = 2 };
 
 // Random stream tags (C-4).
 enum Tag : uint32_t {
@@ -75,6 +85,29 @@ ZINC_DEV uint64_t reduce_m_plus_e(int64_t m, int e, uint64_t q, uint64_t mu) {
 // Residue of a small signed value |v| < q.
 ZINC_DEV uint64_t reduce_small(int64_t v, uint64_t q) {
   return v < 0 ? (uint64_t)(v + (int64_t)q) : (uint64_t)v;
+}
+
+// ------------------------------------------------------------------ schemes
+// m mod t in [0, t) for any int64 m (t < 2^32, t_mu = floor(2^64 / t)).
+ZINC_DEV uint64_t mod_t(int64_t m, uint64_t t, uint64_t t_mu) {
+  const uint64_t a = m < 0 ? (uint64_t)0 - (uint64_t)m : (uint64_t)m;
+  uint64_t r = a - __umul64hi(a, t_mu) * t;  // [0, 2t)
+  r = csub(r, t);
+  return (m < 0 && r != 0) ? t - r : r;
+}
+// Residue of the scheme's c1 plaintext-plus-error term for plaintext coefficient
+// m and error e: CKKS m + e (Eq. 8); BFV Delta (m mod t) + e (Eq. 12);
+// BGV (m mod t) + t e (Eq. 13).
+ZINC_DEV uint64_t pt_plus_e(int64_t m, int e, const LimbConst &c) {
+  if (c.scheme == SCHEME_CKKS) return reduce_m_plus_e(m, e, c.q, c.mu64);
+  const uint64_t mt = mod_t(m, c.t, c.t_mu);
+  if (c.scheme == SCHEME_BFV)
+    return add_mod(csub(mul_shoup_lazy(mt, c.delta, c.delta_sh, c.q), c.q), reduce_small(e, c.q), c.q);
+  return reduce_i64q((int64_t)mt + (int64_t)c.t * e, c.q, c.mu64);
+}
+// Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).
+ZINC_DEV uint64_t err_term(int e, const LimbConst &c) {
+  return c.scheme == SCHEME_BGV ? reduce_i64q((int64_t)c.t * e, c.q, c.mu64) : reduce_small(e, c.q);
 }
 
 // Forward Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> [0, 4q).

@@ -38,14 +38,14 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArg
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
-    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
+    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e(m ? m[x] : 0, se1[x], c); },
                            to_smem<LOGN>(sm), stw);
     __syncthreads();
     stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
       const ulonglong2 z = ld2_nc(z1 + x);
       st2_cs(ct0 + x, add_mod(z.x, canon4(v0, q, two_q), q), add_mod(z.y, canon4(v1, q, two_q), q));
     });
-    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); }, to_smem<LOGN>(sm), stw);
+    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term(se2[x], c); }, to_smem<LOGN>(sm), stw);
     __syncthreads();
     if constexpr (STW) {
       if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) keygen_kernel(KeygenArgs a
 #pragma unroll
         for (int r = 0; r < 16; ++r) sk[base + r] = canon4(v[r], q, two_q);
       });
-  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(se[x], q); },
+  ntt_forward<LOGN>(sm, tw, q, [&](int x) { return err_term(se[x], c); },  // BGV: t e (reading A17)
       [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
@@ -102,7 +102,10 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) keygen_kernel(KeygenArgs a
 // ============================================================ decrypt (Eq. 10)
 // One CTA per message, limbs in order 0..L-1: x^(i) = [c1 + c2 s]_{q_i} (an INTT,
 // plus an NTT of c2 in COEFF form).  Limb 0 writes x0 = centred residue mod q_0
-// to coeff_out; every other limb checks x0 mod q_i == x^(i) (C-10).
+// to coeff_out; every other limb checks x0 mod q_i == x^(i) (C-10).  BGV then
+// replaces x0 by m = x0 mod t (Eq. 13's decoder; valid while |x| < q_0 / 2, the
+// same condition as CKKS's check).  BFV needs every residue: each limb's x^(i)
+// goes to a scratch [B][L][N] and bfv_scale_kernel forms round(t x / Q) mod t.
 template <int LOGN, int FORM>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs a) {
   using G = Geo<LOGN>;
@@ -125,11 +128,16 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs
     auto epilogue = [&](int x, uint64_t v) {
       uint64_t xi = csub(v, q);
       if (FORM == 1) xi = add_mod(xi, c1[x], q);
+      if (c.scheme == SCHEME_BFV) {
+        a.xl_out[(b * L + i) * N + x] = xi;
+        return;
+      }
       if (i == 0) {
         x0[x] = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
       } else {
         if (reduce_i64(x0[x], c) != xi) bad = 1;
       }
+      if (c.scheme == SCHEME_BGV && i == L - 1) x0[x] = (int64_t)mod_t(x0[x], c.t, c.t_mu);
     };
     if (FORM == 0) {
       ntt_inverse<LOGN>(sm, itw, c,
@@ -163,6 +171,32 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs
   } else {
     if (threadIdx.x == 0 && a.status_out) a.status_out[b] = bad;
   }
+}
+
+// ============================================================ BFV decryption scaling
+// m = round(t x / Q) mod t from the residues x_i = x mod q_i (Eq. 12's decoder):
+// with Q~_i = (Q/q_i)^-1 mod q_i, t x / Q = sum_i x_i t Q~_i / q_i - t k, so mod t
+// only the sum matters.  t Q~_i / q_i = I_i + F_i; the integer parts enter mod t,
+// the fractions as 64-bit fixed point f_i = round(F_i 2^64): the 128-bit sum's
+// high word (mod t) plus a rounding bit from the low word.  The fixed-point
+// error is < sum_i x_i / 2^65 <= L q / 2^65 (<= 1/8 at L = 4, 60-bit q), far
+// inside the 1/2 rounding margin for a decryptable ciphertext.
+__global__ void __launch_bounds__(256) bfv_scale_kernel(BfvScaleArgs a) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= a.batch * (size_t)a.n) return;
+  const size_t b = idx / a.n, j = idx % a.n;
+  const uint64_t t = a.limbs[0].t, tmu = a.limbs[0].t_mu;
+  uint64_t lo = 0, hi = 0, ip = 0;  // hi, ip kept mod t
+  for (int i = 0; i < a.L; ++i) {
+    const uint64_t x = a.xl[(b * a.L + i) * a.n + j];
+    const LimbConst &c = a.limbs[i];
+    const uint64_t plo = x * c.dec_f, phi = __umul64hi(x, c.dec_f);
+    const uint64_t nlo = lo + plo;
+    hi = (hi + mod_t((int64_t)phi, t, tmu) + (nlo < lo ? 1 : 0)) % t;
+    lo = nlo;
+    ip = (ip + mod_t((int64_t)x, t, tmu) * c.dec_i) % t;
+  }
+  a.m_out[idx] = (int64_t)((ip + hi + (lo >> 63)) % t);
 }
 
 // ============================================================ standalone NTT
@@ -222,6 +256,12 @@ static cudaError_t launch_decrypt_t(const DecryptArgs &a, int form, size_t batch
   if (form == 0) return launch_ex(decrypt_kernel<LOGN, 0>, msg_grid<LOGN>(batch), G::THREADS, smem, G::CLUSTER, s, a);
   return launch_ex(decrypt_kernel<LOGN, 1>, msg_grid<LOGN>(batch), G::THREADS, smem, G::CLUSTER, s, a);
 }
+cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s) {
+  const size_t n = a.batch * (size_t)a.n;
+  bfv_scale_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s) {
 #define CALL(K) launch_decrypt_t<K>(a, form, batch, s)
   ZINC_LOGN_SWITCH(log_n, CALL)

@@ -4,7 +4,8 @@
 namespace zinc {
 
 // ============================================================ vanilla encryption
-// Eq. 8 with reading A1: c1 = [pk1.u + e1 + m]_q, c2 = [pk2.u + e2]_q.  CTA =
+// Eq. 8 with reading A1: c1 = [pk1.u + e1 + m]_q, c2 = [pk2.u + e2]_q (BFV Eq. 12 /
+// BGV Eq. 13 through pt_plus_e / err_term).  CTA =
 // (message b, limb group); u, e1, e2 are sampled once per CTA into smem (int8),
 // then per limb:
 //  NTT form:   NTT(e1 + m) -> ct0;  NTT(e2) -> ct1;
@@ -53,13 +54,13 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
     if (FORM == 0) {
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64); },
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e(m ? m[x] : 0, se1[x], c); },
                              to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         st2(ct0 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
       });
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(se2[x], q); }, to_smem<LOGN>(sm), stw);
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term(se2[x], c); }, to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         st2(ct1 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
           [&](int x, uint64_t v) {
-            uint64_t e = reduce_m_plus_e(m ? m[x] : 0, se1[x], c.q, c.mu64);
+            uint64_t e = pt_plus_e(m ? m[x] : 0, se1[x], c);
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
           }, sitw);
       __syncthreads();  // the inverse's last stores may still read sm (split exchange) -- and ct1 temp visibility
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
-          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), reduce_small(se2[x], q), q)); }, sitw);
+          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), err_term(se2[x], c), q)); }, sitw);
       if constexpr (STW) {
         if (i + 1 < hi) {
           __syncthreads();  // every thread is past the inverse's smem-twiddle passes

@@ -55,7 +55,15 @@ struct DecryptArgs {
   const uint64_t *sk_ntt, *ct;
   int64_t *coeff_out;
   int32_t *status_out;
+  uint64_t *xl_out;       // BFV: residues [B][L][N] for bfv_scale_kernel
   int L;
+};
+struct BfvScaleArgs {
+  const LimbConst *limbs;
+  const uint64_t *xl;     // [B][L][N]
+  int64_t *m_out;         // [B][N], m in [0, t)
+  size_t batch;
+  int n, L;
 };
 struct EncodeArgs {
   const double *slots;
@@ -102,6 +110,7 @@ cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t bat
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s);
 cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);
 cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s);
+cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s);
 cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s);
 cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s);
 cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s);

@@ -36,11 +36,15 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   const int T = 2 * blockDim.x;
   const int L = LC > 0 ? LC : a.L;
   const int j0 = tile_x * T;
-  uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L;
+  uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L, *sdel = smu + L, *sdelsh = sdel + L;
   for (int i = threadIdx.x; i < L; i += blockDim.x) {
     sq[i] = a.limbs[i].q;
     smu[i] = a.limbs[i].mu64;
+    sdel[i] = a.limbs[i].delta;
+    sdelsh[i] = a.limbs[i].delta_sh;
   }
+  const uint32_t scheme = a.limbs[0].scheme;
+  const uint64_t tpl = a.limbs[0].t, tmu = a.limbs[0].t_mu;
   if (threadIdx.x == 0) {
     uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
@@ -85,17 +89,45 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
     const int e0 = cbd_lo(w1), e1 = cbd_hi(w1);
     const int f0 = cbd_lo(w2), f1 = cbd_hi(w2);
     uint64_t *out = a.ct + b * 2 * lnn + j;
-    // |m| < 2^62 rules out int64 overflow of m + e; then |v| < qmin is the fast path
-    const int64_t v0 = m0 + e0, v1 = m1 + e1;
-    // the library's own encode scratch is dead once read: drop its L2 lines
-    // without a write-back (saves the 128 KiB/message the dirty lines would
-    // otherwise cost in HBM writes when evicted).  Lanes 8r..8r+7 share a line.
-    if (a.discard_m && (threadIdx.x & 7) == 0)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.n + j) : "memory");
+    if (scheme == SCHEME_BFV) {
+      // Eq. 12, Zinc "without modification": c1' = zero1 + Delta (m mod t) + e1' (per limb)
+      const uint64_t mt0 = mod_t(m0, tpl, tmu), mt1 = mod_t(m1, tpl, tmu);
+#pragma unroll 1
+      for (int i = 0; i < L; ++i) {
+        const uint64_t q = sq[i];
+        uint64_t z10, z11, z20, z21;
+        ld2(tile + (size_t)i * T + jl, z10, z11);
+        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+        const uint64_t d0 = csub(mul_shoup_lazy(mt0, sdel[i], sdelsh[i], q), q);
+        const uint64_t d1 = csub(mul_shoup_lazy(mt1, sdel[i], sdelsh[i], q), q);
+        st2_cs(out + (size_t)i * a.n, mod_add_signed(add_mod(z10, d0, q), e0, q),
+               mod_add_signed(add_mod(z11, d1, q), e1, q));
+        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+      }
+      // the library's own encode scratch is dead once read (the stores above consumed it):
+      // drop its L2 lines without a write-back.  Lanes 8r..8r+7 share a 128-byte line.
+      if (a.discard_m && (threadIdx.x & 7) == 0)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.n + j) : "memory");
+      continue;
+    }
+    // CKKS: v = m + e1' (|m| < 2^62 rules out int64 overflow); BGV (Eq. 13): v = (m mod t) +
+    // t e1', g = t e2'.  Either way v is limb-independent and |v| < qmin is the fast path.
+    int64_t v0, v1, g0 = f0, g1 = f1;
+    bool in_range = true;
+    if (scheme == SCHEME_BGV) {
+      v0 = (int64_t)mod_t(m0, tpl, tmu) + (int64_t)tpl * e0;
+      v1 = (int64_t)mod_t(m1, tpl, tmu) + (int64_t)tpl * e1;
+      g0 = (int64_t)tpl * f0;
+      g1 = (int64_t)tpl * f1;
+    } else {
+      v0 = m0 + e0;
+      v1 = m1 + e1;
+      in_range = (m0 > -(1ll << 62)) && (m0 < (1ll << 62)) && (m1 > -(1ll << 62)) && (m1 < (1ll << 62));
+    }
     const uint64_t a0 = v0 < 0 ? (uint64_t)0 - (uint64_t)v0 : (uint64_t)v0;
     const uint64_t a1 = v1 < 0 ? (uint64_t)0 - (uint64_t)v1 : (uint64_t)v1;
-    const bool small = (m0 > -(1ll << 62)) && (m0 < (1ll << 62)) && (m1 > -(1ll << 62)) && (m1 < (1ll << 62)) &&
-                       a0 < qmin && a1 < qmin;
+    const uint64_t ag = (uint64_t)(g0 < 0 ? -g0 : g0) | (uint64_t)(g1 < 0 ? -g1 : g1);
+    const bool small = in_range && a0 < qmin && a1 < qmin && ag < qmin;
     if (__all_sync(0xffffffffu, small)) {
 #pragma unroll
       for (int i = 0; i < L; ++i) {
@@ -104,21 +136,24 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
         ld2(tile + (size_t)i * T + jl, z10, z11);
         ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
         st2_cs(out + (size_t)i * a.n, mod_add_signed(z10, v0, q), mod_add_signed(z11, v1, q));
-        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, g0, q), mod_add_signed(z21, g1, q));
       }
     } else {
 #pragma unroll 1
       for (int i = 0; i < L; ++i) {
-        const uint64_t q = sq[i], mu = smu[i];
+        const LimbConst &c = a.limbs[i];
+        const uint64_t q = c.q;
         uint64_t z10, z11, z20, z21;
         ld2(tile + (size_t)i * T + jl, z10, z11);
         ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-        const uint64_t c10 = add_mod(z10, reduce_m_plus_e(m0, e0, q, mu), q);
-        const uint64_t c11 = add_mod(z11, reduce_m_plus_e(m1, e1, q, mu), q);
-        st2_cs(out + (size_t)i * a.n, c10, c11);
-        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+        st2_cs(out + (size_t)i * a.n, add_mod(z10, pt_plus_e(m0, e0, c), q), add_mod(z11, pt_plus_e(m1, e1, c), q));
+        st2_cs(out + lnn + (size_t)i * a.n, add_mod(z20, err_term(f0, c), q), add_mod(z21, err_term(f1, c), q));
       }
     }
+    // the library's own encode scratch is dead once read (the stores above consumed it):
+    // drop its L2 lines without a write-back.  Lanes 8r..8r+7 share a 128-byte line.
+    if (a.discard_m && (threadIdx.x & 7) == 0)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.n + j) : "memory");
   }
 }
 
