@@ -277,6 +277,7 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
   *out = nullptr;
   if (log_n < 12 || log_n > 15) return fail(ZINC_EINVAL, "log_n %d outside [12, 15]", log_n);
   if (L < 1 || L > 32) return fail(ZINC_EINVAL, "num_limbs %d outside [1, 32]", L);
+  if (scheme != ZINC_SCHEME_CKKS) log_scale = 1;  // unused by BFV / BGV
   if (log_scale < 1 || log_scale > 60) return fail(ZINC_EINVAL, "log_scale %d outside [1, 60]", log_scale);
   for (int i = 0; i < L; ++i)
     if (limb_bits[i] < 20 || limb_bits[i] > 60)

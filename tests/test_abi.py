@@ -43,6 +43,12 @@ def test_argument_validation_without_gpu():
     assert lib.zinc_keygen(None, 1, None, None, None, None) == -1
     assert lib.zinc_encrypt_batch(None, None, 0, 0, None, 1, 0, 0, None, None) == -1
     assert lib.ckks_decrypt_batch(None, None, 0, None, 1, None, None, None, None) == -1
+    # scheme validation happens before any device work
+    assert lib.zinc_ctx_create_scheme(12, 3, bits, 3, 65537, 0, 0, ctypes.byref(h)) == -1    # bad scheme
+    assert b"scheme" in lib.zinc_last_error()
+    assert lib.zinc_ctx_create_scheme(12, 3, bits, 1, 1, 0, 0, ctypes.byref(h)) == -1        # t < 2
+    assert lib.zinc_ctx_create_scheme(12, 3, bits, 2, 1 << 32, 0, 0, ctypes.byref(h)) == -1  # t >= 2^32
+    assert b"plain modulus" in lib.zinc_last_error()
     lib.zinc_launch_count_reset()
     assert lib.zinc_launch_count() == 0
 
