@@ -517,7 +517,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
-    LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, batch, groups, s));
+    LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, c->scheme != ZINC_SCHEME_CKKS, batch, groups, s));
     return ZINC_OK;
   }
   VanillaArgs a{};
@@ -531,7 +531,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
-  LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, batch, groups, s));
+  LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, c->scheme != ZINC_SCHEME_CKKS, batch, groups, s));
   return ZINC_OK;
 }
 

@@ -98,16 +98,19 @@ ZINC_DEV uint64_t mod_t(int64_t m, uint64_t t, uint64_t t_mu) {
 // Residue of the scheme's c1 plaintext-plus-error term for plaintext coefficient
 // m and error e: CKKS m + e (Eq. 8); BFV Delta (m mod t) + e (Eq. 12);
 // BGV (m mod t) + t e (Eq. 13).
+// INTS = false compiles the CKKS term only (the kernels' CKKS instantiations).
+template <bool INTS = true>
 ZINC_DEV uint64_t pt_plus_e(int64_t m, int e, const LimbConst &c) {
-  if (c.scheme == SCHEME_CKKS) return reduce_m_plus_e(m, e, c.q, c.mu64);
+  if (!INTS || c.scheme == SCHEME_CKKS) return reduce_m_plus_e(m, e, c.q, c.mu64);
   const uint64_t mt = mod_t(m, c.t, c.t_mu);
   if (c.scheme == SCHEME_BFV)
     return add_mod(csub(mul_shoup_lazy(mt, c.delta, c.delta_sh, c.q), c.q), reduce_small(e, c.q), c.q);
   return reduce_i64q((int64_t)mt + (int64_t)c.t * e, c.q, c.mu64);
 }
 // Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).
+template <bool INTS = true>
 ZINC_DEV uint64_t err_term(int e, const LimbConst &c) {
-  return c.scheme == SCHEME_BGV ? reduce_i64q((int64_t)c.t * e, c.q, c.mu64) : reduce_small(e, c.q);
+  return (INTS && c.scheme == SCHEME_BGV) ? reduce_i64q((int64_t)c.t * e, c.q, c.mu64) : reduce_small(e, c.q);
 }
 
 // Forward Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> [0, 4q).

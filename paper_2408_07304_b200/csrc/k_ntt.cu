@@ -6,7 +6,7 @@ namespace zinc {
 // ============================================================ Zinc, NTT form
 // c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2') (two DFTs,
 // no multiplication).
-template <int LOGN>
+template <int LOGN, bool INTS>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArgs a) {
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
@@ -38,14 +38,14 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArg
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
-    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e(m ? m[x] : 0, se1[x], c); },
+    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
                            to_smem<LOGN>(sm), stw);
     __syncthreads();
     stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
       const ulonglong2 z = ld2_nc(z1 + x);
       st2_cs(ct0 + x, add_mod(z.x, canon4(v0, q, two_q), q), add_mod(z.y, canon4(v1, q, two_q), q));
     });
-    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term(se2[x], c); }, to_smem<LOGN>(sm), stw);
+    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
     __syncthreads();
     if constexpr (STW) {
       if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
@@ -226,13 +226,15 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) ntt_kernel(NttArgs a) {
 }
 
 template <int LOGN>
-static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
+static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, bool ints, size_t batch, int groups, cudaStream_t s) {
   using G = Geo<LOGN>;
   const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN) + (G::SPLIT ? 0 : kSmemTw * sizeof(Tw));
-  return launch_ex(zinc_ntt_kernel<LOGN>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
+  const dim3 grid = msg_grid<LOGN>(batch, groups);
+  if (ints) return launch_ex(zinc_ntt_kernel<LOGN, true>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(zinc_ntt_kernel<LOGN, false>, grid, G::THREADS, smem, G::CLUSTER, s, a);
 }
-cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, size_t batch, int groups, cudaStream_t s) {
-#define CALL(K) launch_zinc_ntt_t<K>(a, batch, groups, s)
+cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, bool ints, size_t batch, int groups, cudaStream_t s) {
+#define CALL(K) launch_zinc_ntt_t<K>(a, ints, batch, groups, s)
   ZINC_LOGN_SWITCH(log_n, CALL)
 #undef CALL
 }

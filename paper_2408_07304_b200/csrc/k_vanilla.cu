@@ -13,7 +13,7 @@ namespace zinc {
 //  COEFF form: NTT(u) -> epilogue: ct1 <- pk2 u^ (temporary), smem <- pk1 u^;
 //              INTT(smem) + e1 + m -> ct0;  INTT(ct1) + e2 -> ct1.
 // 3 transforms per limb either way.
-template <int LOGN, int FORM>
+template <int LOGN, int FORM, bool INTS>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs a) {
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
@@ -54,13 +54,13 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
     if (FORM == 0) {
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e(m ? m[x] : 0, se1[x], c); },
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
                              to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         st2(ct0 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
       });
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term(se2[x], c); }, to_smem<LOGN>(sm), stw);
+      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         st2(ct1 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
           [&](int x, uint64_t v) {
-            uint64_t e = pt_plus_e(m ? m[x] : 0, se1[x], c);
+            uint64_t e = pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c);
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
           }, sitw);
       __syncthreads();  // the inverse's last stores may still read sm (split exchange) -- and ct1 temp visibility
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
-          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), err_term(se2[x], c), q)); }, sitw);
+          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[x], c), q)); }, sitw);
       if constexpr (STW) {
         if (i + 1 < hi) {
           __syncthreads();  // every thread is past the inverse's smem-twiddle passes
@@ -124,15 +124,22 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
 }
 
 template <int LOGN>
-static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
+static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, bool ints, size_t batch, int groups,
+                                    cudaStream_t s) {
   using G = Geo<LOGN>;
   const size_t twb = G::SPLIT ? 0 : (size_t)(form == 0 ? 1 : 2) * kSmemTw * sizeof(Tw);
   const size_t smem = ntt_smem_bytes<LOGN>() + (1 << LOGN) / 4 + 2 * (1 << LOGN) + twb;
-  if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
-  return launch_ex(vanilla_kernel<LOGN, 1>, msg_grid<LOGN>(batch, groups), G::THREADS, smem, G::CLUSTER, s, a);
+  const dim3 grid = msg_grid<LOGN>(batch, groups);
+  if (ints) {
+    if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0, true>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+    return launch_ex(vanilla_kernel<LOGN, 1, true>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  }
+  if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0, false>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(vanilla_kernel<LOGN, 1, false>, grid, G::THREADS, smem, G::CLUSTER, s, a);
 }
-cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, size_t batch, int groups, cudaStream_t s) {
-#define CALL(K) launch_vanilla_t<K>(a, form, batch, groups, s)
+cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, bool ints, size_t batch, int groups,
+                           cudaStream_t s) {
+#define CALL(K) launch_vanilla_t<K>(a, form, ints, batch, groups, s)
   ZINC_LOGN_SWITCH(log_n, CALL)
 #undef CALL
 }
