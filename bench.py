@@ -513,6 +513,14 @@ def main():
         result["decrypt_decode"] = {"form": "COEFF", "ms": dms, "ct_per_s": B / (dms / 1e3),
                                     "transforms_per_ct": 2 * cfg.L,
                                     "note": "x = c1 + c2 s on every limb (NTT + INTT per limb), CRT check, FP64 decode"}
+    if rank == 0:
+        # aggregation of the whole batch (Eq. 2, HBM-bound read of every ciphertext)
+        agg = ctx.empty_key()
+        ams = _timed(torch, lambda: Z.zinc_ct_sum_batch(ctx, ct, out=agg), 3)
+        rb = B * 2 * cfg.L * cfg.n * 8
+        result["aggregate"] = {"ms": ams, "ct_per_s": B / (ams / 1e3), "GBps": rb / (ams / 1e3) / 1e9,
+                               "frac_hbm": rb / (ams / 1e3) / 1e9 / peak, "batch": B,
+                               "note": "zinc_ct_sum_batch over the step's last output (read 2 L N 8 B per ct)"}
     if rank == 0 and world == 1 and not args.no_c5:
         del ct
         torch.cuda.empty_cache()

@@ -149,6 +149,17 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *ctx, const uint64_t *sk_ntt, zinc
                                const uint64_t *ct, size_t batch, double *slots_out,
                                int64_t *coeff_out, int32_t *status_out, zinc_stream_t stream);
 
+/* ---- Eq. 2: batched (+) and aggregation -------------------- */
+
+/* out_b = [x_b + y_b]_q componentwise for b < batch; ciphertexts uint64[batch][2][L][N]
+ * in one form (either: the NTT is linear); out may alias x or y.  Dec(out_b) = m_x + m_y
+ * (+ noise) in every scheme. */
+zinc_status zinc_ct_add_batch(const zinc_ctx *ctx, const uint64_t *x, const uint64_t *y,
+                              size_t batch, uint64_t *out, zinc_stream_t stream);
+/* Aggregation: out = [sum_b ct_b]_q, one ciphertext uint64[2][L][N] (batch 0 -> zero). */
+zinc_status zinc_ct_sum_batch(const zinc_ctx *ctx, const uint64_t *ct, size_t batch,
+                              uint64_t *out, zinc_stream_t stream);
+
 /* ---- support / test exports ---------------------------------------------- */
 
 /* Encode slots (kind SLOTS_F64 or SLOTS_C128) to int64[batch][N] per C-6. */
@@ -200,7 +211,9 @@ enum {
   ZINC_K_INT_PEAK = 9,
   ZINC_K_ZINC_FUSED = 10, /* encode of chunk k+1 fused with Zinc add/inject of chunk k */
   ZINC_K_BFV_SCALE = 11, /* BFV decryption: round(t.x/Q) mod t from the RNS residues */
-  ZINC_K_COUNT = 12
+  ZINC_K_CT_ADD = 12,    /* batched ciphertext addition (Eq. 2) */
+  ZINC_K_CT_SUM = 13,    /* aggregation of a batch */
+  ZINC_K_COUNT = 14
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */

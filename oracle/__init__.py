@@ -84,6 +84,8 @@ def _declare(L):
         "orc_zinc_encrypt": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_int, _i64p, _c.c_uint64, _c.c_uint64, _u64p]),
         "orc_decrypt": (_c.c_int, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _u64p, _c.c_int, _i64p, _u64p]),
         "orc_ntt_limbs": (None, [_u64p, _c.c_int, _c.c_int, _u64p, _u64p]),
+        "orc_ct_add": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_uint64, _u64p]),
+        "orc_ct_sum": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _c.c_uint64, _u64p]),
         "orc_keygen_scaled": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _c.c_uint64, _c.c_int64, _i64p, _u64p, _u64p]),
         "orc_bfv_delta_mod": (_c.c_uint64, [_c.c_int, _u64p, _c.c_uint64, _c.c_int]),
         "orc_plaintext_residues": (None, [_c.c_int, _c.c_uint64, _c.c_int, _c.c_int, _u64p, _i64p, _u64p]),
@@ -409,3 +411,20 @@ def decrypt_scheme(P: Params, scheme: int, t: int, sk_ntt, ct, form: int) -> np.
     else:
         m = [x % t for x in xs]
     return np.array(m, dtype=np.int64)
+
+
+# ---------------------------------------------------------------- Eq. 2: batched (+) and aggregation
+def ct_add(P: Params, a, b) -> np.ndarray:
+    a, b = _u64(a), _u64(b)
+    out = np.zeros_like(a)
+    count = a.size // (2 * P.L * P.n)
+    lib().orc_ct_add(P.log_n, P.L, _p(P.q, _u64p), _p(a, _u64p), _p(b, _u64p), count, _p(out, _u64p))
+    return out
+
+
+def ct_sum(P: Params, ct) -> np.ndarray:
+    ct = _u64(ct)
+    out = np.zeros((2, P.L, P.n), dtype=np.uint64)
+    count = ct.size // (2 * P.L * P.n)
+    lib().orc_ct_sum(P.log_n, P.L, _p(P.q, _u64p), _p(ct, _u64p), count, _p(out, _u64p))
+    return out

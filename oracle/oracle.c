@@ -808,6 +808,33 @@ void orc_zinc_encrypt_scheme(int scheme, uint64_t t, int log_n, int num_limbs, c
   free(e1p); free(e2p); free(pt); free(ep);
 }
 
+/* ------------------------------------------------------------------------ */
+/* Eq. 2: Enc(a) (+) Enc(b) is the componentwise sum, and   */
+/* aggregation of a batch is the repeated sum.  Either form (the NTT is      */
+/* linear).  ct arrays [count][2][L][N].                                     */
+/* ------------------------------------------------------------------------ */
+void orc_ct_add(int log_n, int num_limbs, const uint64_t *q, const uint64_t *a, const uint64_t *b,
+                uint64_t count, uint64_t *out) {
+  uint64_t n = 1ull << log_n;
+  for (uint64_t k = 0; k < count; k++)
+    for (int c = 0; c < 2; c++)
+      for (int i = 0; i < num_limbs; i++)
+        for (uint64_t j = 0; j < n; j++) {
+          uint64_t w = ((k * 2 + c) * (uint64_t)num_limbs + i) * n + j;
+          out[w] = addmod(a[w], b[w], q[i]);
+        }
+}
+void orc_ct_sum(int log_n, int num_limbs, const uint64_t *q, const uint64_t *ct, uint64_t count,
+                uint64_t *out) {
+  uint64_t n = 1ull << log_n, words = 2ull * num_limbs * n;
+  for (uint64_t w = 0; w < words; w++) out[w] = 0;
+  for (uint64_t k = 0; k < count; k++)
+    for (uint64_t w = 0; w < words; w++) {
+      int i = (int)((w / n) % (uint64_t)num_limbs);
+      out[w] = addmod(out[w], ct[k * words + w], q[i]);
+    }
+}
+
 /* Plain helpers exposed for tests: forward/inverse NTT of [L][N] in place. */
 void orc_ntt_limbs(uint64_t *a, int log_n, int num_limbs, const uint64_t *q, const uint64_t *psi) {
   uint64_t n = 1ull << log_n;

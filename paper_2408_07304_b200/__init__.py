@@ -23,7 +23,7 @@ __all__ = [
     "NTT", "COEFF", "PT_COEFF_I64", "PT_SLOTS_F64", "PT_SLOTS_C128", "ZincError", "Context", "lib",
     "zinc_keygen", "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch",
     "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
-    "zinc_debug_sample", "zinc_int_peak", "zinc_encrypt_batch_host", "launch_count",
+    "zinc_debug_sample", "zinc_int_peak", "zinc_ct_add_batch", "zinc_ct_sum_batch", "zinc_encrypt_batch_host", "launch_count",
     "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_OVERLAP", "TUNE_COEFF_SMEM_PAD", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
 ]
 
@@ -41,11 +41,11 @@ EXPORTED_SYMBOLS = (
     "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse", "zinc_debug_sample", "zinc_int_peak",
     "zinc_encrypt_batch_host", "zinc_launch_count", "zinc_launch_count_reset", "zinc_last_error",
     "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name", "zinc_tune", "zinc_ctx_create_scheme",
-    "zinc_ctx_scheme",
+    "zinc_ctx_scheme", "zinc_ct_add_batch", "zinc_ct_sum_batch",
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
                 "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                "zinc_coeff_encode_kernel", "bfv_scale_kernel")
+                "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel")
 
 
 class ZincError(RuntimeError):
@@ -75,6 +75,8 @@ _SIGS = {
     "zinc_tune": [_i32, _c.c_longlong, _c.POINTER(_c.c_longlong)],
     "zinc_ctx_create_scheme": [_i32, _i32, _c.POINTER(_c.c_int), _i32, _u64, _i32, _i32, _c.POINTER(_vp)],
     "zinc_ctx_scheme": [_vp, _c.POINTER(_c.c_int), _c.POINTER(_u64)],
+    "zinc_ct_add_batch": [_vp, _vp, _vp, _sz, _vp, _vp],
+    "zinc_ct_sum_batch": [_vp, _vp, _sz, _vp, _vp],
 }
 
 _lib = None
@@ -246,6 +248,22 @@ def ckks_encode_batch(ctx: Context, slots: torch.Tensor, out=None, stream=None):
     _check(lib().ckks_encode_batch(ctx.handle, _kind_of(slots), _ptr(slots), b, _ptr(m), _stream(stream)),
            "ckks_encode_batch")
     return m
+
+
+def zinc_ct_add_batch(ctx: Context, x: torch.Tensor, y: torch.Tensor, out=None, stream=None):
+    """Eq. 2: [x + y]_q for ciphertext batches [B,2,L,N]."""
+    out = torch.empty_like(x) if out is None else out
+    _check(lib().zinc_ct_add_batch(ctx.handle, _ptr(x), _ptr(y), x.shape[0], _ptr(out), _stream(stream)),
+           "zinc_ct_add_batch")
+    return out
+
+
+def zinc_ct_sum_batch(ctx: Context, ct: torch.Tensor, out=None, stream=None):
+    """Aggregation: the sum of a ciphertext batch [B,2,L,N] -> [2,L,N]."""
+    out = ctx.empty_key() if out is None else out
+    _check(lib().zinc_ct_sum_batch(ctx.handle, _ptr(ct), ct.shape[0], _ptr(out), _stream(stream)),
+           "zinc_ct_sum_batch")
+    return out
 
 
 def zinc_ntt_forward(ctx: Context, data: torch.Tensor, stream=None):

@@ -51,7 +51,8 @@ static uint64_t g_trace_n[ZINC_K_COUNT];
 static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel",
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
                                                  "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                                                 "zinc_coeff_encode_kernel", "bfv_scale_kernel"};
+                                                 "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel",
+                                                 "ct_sum_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -755,6 +756,42 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
   }
   if (!coeff_out) cudaFreeAsync(x, s);
   return st;
+}
+
+zinc_status zinc_ct_add_batch(const zinc_ctx *c, const uint64_t *x, const uint64_t *y, size_t batch, uint64_t *out,
+                              zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (batch == 0) return ZINC_OK;
+  zinc_status st;
+  if ((st = check_ptrs({x, y, out}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CtAddArgs a{};
+  a.limbs = c->d_limbs;
+  a.a = x;
+  a.b = y;
+  a.out = out;
+  a.words = batch * 2 * (size_t)c->L * c->n;
+  a.log_n = c->log_n;
+  a.L = c->L;
+  LAUNCH(ZINC_K_CT_ADD, (cudaStream_t)stream, launch_ct_add(a, (cudaStream_t)stream));
+  return ZINC_OK;
+}
+
+zinc_status zinc_ct_sum_batch(const zinc_ctx *c, const uint64_t *ct, size_t batch, uint64_t *out,
+                              zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  zinc_status st;
+  if ((st = check_ptrs({ct, out}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CtSumArgs a{};
+  a.limbs = c->d_limbs;
+  a.ct = ct;
+  a.out = out;
+  a.batch = batch;  // batch 0 writes the zero ciphertext
+  a.log_n = c->log_n;
+  a.L = c->L;
+  LAUNCH(ZINC_K_CT_SUM, (cudaStream_t)stream, launch_ct_sum(a, (cudaStream_t)stream));
+  return ZINC_OK;
 }
 
 zinc_status ckks_encode_batch(const zinc_ctx *c, zinc_pt_kind kind, const void *slots, size_t batch, int64_t *m_out,

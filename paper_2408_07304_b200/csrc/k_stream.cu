@@ -12,6 +12,60 @@ __global__ void __launch_bounds__(256, 3) zinc_coeff_kernel(ZincCoeffArgs a) {
   zinc_coeff_body<LC>(a, blockIdx.x, blockIdx.y, tile);
 }
 
+// ============================================================ Eq. 2: batched (+) and aggregation
+// out = [a + b]_q word by word over [count][2][L][N] (either form: the NTT is
+// linear).  16-byte loads/stores; the limb of word w is (w / N) mod L.
+__global__ void __launch_bounds__(256) ct_add_kernel(CtAddArgs a) {
+  const size_t pairs = a.words / 2;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += (size_t)gridDim.x * blockDim.x) {
+    const size_t w = 2 * p;
+    const uint64_t q = __ldg(&a.limbs[(w >> a.log_n) % a.L].q);
+    const ulonglong2 x = ld2_nc(a.a + w), y = ld2_nc(a.b + w);
+    st2_cs(a.out + w, add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
+  }
+}
+// out = [sum_b ct_b]_q: one thread per word pair of the [2][L][N] result, walking
+// the batch with U independent 16-byte loads in flight (HBM-bound read of the
+// whole batch, one write).
+__global__ void __launch_bounds__(256) ct_sum_kernel(CtSumArgs a) {
+  const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t words = (size_t)2 * a.L << a.log_n;
+  if (2 * p >= words) return;
+  const size_t w = 2 * p;
+  const uint64_t q = __ldg(&a.limbs[(w >> a.log_n) % a.L].q);
+  uint64_t s0 = 0, s1 = 0;
+  constexpr int U = 8;
+  size_t b = 0;
+  for (; b + U <= a.batch; b += U) {
+    ulonglong2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld2_nc(a.ct + (b + u) * words + w);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      s0 = add_mod(s0, v[u].x, q);
+      s1 = add_mod(s1, v[u].y, q);
+    }
+  }
+  for (; b < a.batch; ++b) {
+    const ulonglong2 v = ld2_nc(a.ct + b * words + w);
+    s0 = add_mod(s0, v.x, q);
+    s1 = add_mod(s1, v.y, q);
+  }
+  st2(a.out + w, s0, s1);
+}
+
+cudaError_t launch_ct_add(const CtAddArgs &a, cudaStream_t s) {
+  const size_t pairs = a.words / 2;
+  const unsigned blocks = (unsigned)std::min<size_t>((pairs + 255) / 256, 148 * 16);
+  ct_add_kernel<<<blocks, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_ct_sum(const CtSumArgs &a, cudaStream_t s) {
+  const size_t pairs = ((size_t)2 * a.L << a.log_n) / 2;
+  ct_sum_kernel<<<(unsigned)((pairs + 255) / 256), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 // ============================================================ samplers (debug)
 __global__ void sample_kernel(SampleArgs a) {
   size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -87,6 +87,20 @@ struct NttArgs {
   uint64_t *data;
   int L;
 };
+struct CtAddArgs {
+  const LimbConst *limbs;
+  const uint64_t *a, *b;
+  uint64_t *out;
+  size_t words;           // count * 2 * L * N
+  int log_n, L;
+};
+struct CtSumArgs {
+  const LimbConst *limbs;
+  const uint64_t *ct;     // [batch][2][L][N]
+  uint64_t *out;          // [2][L][N]
+  size_t batch;
+  int log_n, L;
+};
 struct SampleArgs {
   uint32_t tag, limb;
   uint64_t seed, msg, q;
@@ -116,6 +130,8 @@ cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStre
 cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s);
 cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s);
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
+cudaError_t launch_ct_add(const CtAddArgs &a, cudaStream_t s);
+cudaError_t launch_ct_sum(const CtSumArgs &a, cudaStream_t s);
 cudaError_t launch_int_peak(const IntPeakArgs &a, int blocks, cudaStream_t s);
 
 }  // namespace zinc

@@ -336,3 +336,24 @@ def test_tuning_knobs_never_change_results(Z, orc, knobs):
         for k, v in old.items():
             Z.tune(k, v)
     assert torch.equal(ref, got) and torch.equal(ref_v, got_v)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_ct_add_and_sum_bit_exact_and_decrypt(Z, orc, name):
+    """Eq. 2 kernels: batched (+) and aggregation bit-exact against
+    the oracle; the aggregate of k Zinc ciphertexts decrypts to the sum of the slots."""
+    s = setup_for(Z, orc, name)
+    cfg = s.cfg
+    k = 7
+    z = slots_batch(cfg, 0, k)
+    zc = np.stack([z.real, z.imag], axis=-1) if cfg.complex_slots else z
+    cts = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, torch.from_numpy(np.ascontiguousarray(zc)).cuda(), 9, 0)
+    a, b = cts[:3].contiguous(), cts[3:6].contiguous()
+    got_add = Z.zinc_ct_add_batch(s.ctx, a, b)
+    assert np.array_equal(got_add.cpu().numpy(), orc.ct_add(s.P, a.cpu().numpy(), b.cpu().numpy()))
+    tot = Z.zinc_ct_sum_batch(s.ctx, cts)
+    assert np.array_equal(tot.cpu().numpy(), orc.ct_sum(s.P, cts.cpu().numpy()))
+    assert not Z.zinc_ct_sum_batch(s.ctx, cts[:0]).any()                      # empty batch -> zero
+    _, st, zz = Z.ckks_decrypt_batch(s.ctx, s.sk, COEFF, tot[None].contiguous())
+    assert int(st.sum()) == 0
+    assert np.max(np.abs(zz[0].cpu().numpy() - z.sum(axis=0))) < k * cfg.tolerance()

@@ -260,3 +260,30 @@ def test_transform_accounting(orc, small):
     orc.counters_reset()
     orc.zinc_encrypt(P, cache_n, 0, m, 1, 1)
     assert orc.counters() == (3 * P.L, 0)
+
+
+def test_ct_add_and_sum_match_big_integer_sums(orc, small):
+    """orc_ct_add / orc_ct_sum against Python big-integer sums reduced mod q_i."""
+    P = small[0]
+    rng = np.random.default_rng(12)
+    cts = np.stack([np.stack([np.stack([rng.integers(0, int(q), P.n, dtype=np.uint64) for q in P.q])
+                              for _ in range(2)]) for _ in range(5)])
+    q = np.array([int(v) for v in P.q], dtype=object)[None, None, :, None]
+    add = (cts[:2].astype(object) + cts[2:4].astype(object)) % q
+    assert np.array_equal(orc.ct_add(P, cts[:2], cts[2:4]), add.astype(np.uint64))
+    tot = cts.astype(object).sum(axis=0) % q[0]
+    assert np.array_equal(orc.ct_sum(P, cts), tot.astype(np.uint64))
+
+
+def test_aggregation_decrypts_to_the_slot_sum(orc, c1):
+    """Eq. 2 repeated: Dec(sum of k Zinc encryptions) = sum of the k plaintexts + noise."""
+    P, sk, sk_ntt, pk = c1
+    from workloads import slots_batch
+    cache = orc.precompute_cache(P, pk, 3, orc.COEFF)
+    z = slots_batch(C1, 0, 6)
+    cts = np.stack([orc.zinc_encrypt(P, cache, orc.COEFF, orc.encode(z[k], P.log_n, P.log_scale), 4, k)
+                    for k in range(6)])
+    x, st = orc.decrypt(P, sk_ntt, orc.ct_sum(P, cts), orc.COEFF)
+    assert st == 0
+    err = np.max(np.abs(orc.decode(x, P.log_n, P.log_scale) - z.sum(axis=0)))
+    assert err < 6 * C1.tolerance()
