@@ -781,7 +781,7 @@ zinc_status zinc_ct_sum_batch(const zinc_ctx *c, const uint64_t *ct, size_t batc
                               zinc_stream_t stream) {
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
-  if ((st = check_ptrs({ct, out}))) return st;
+  if ((st = check_ptrs({out})) || (batch && (st = check_ptrs({ct})))) return st;
   CUDA_TRY(cudaSetDevice(c->device));
   CtSumArgs a{};
   a.limbs = c->d_limbs;
