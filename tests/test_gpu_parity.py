@@ -353,7 +353,7 @@ def test_ct_add_and_sum_bit_exact_and_decrypt(Z, orc, name):
     assert np.array_equal(got_add.cpu().numpy(), orc.ct_add(s.P, a.cpu().numpy(), b.cpu().numpy()))
     tot = Z.zinc_ct_sum_batch(s.ctx, cts)
     assert np.array_equal(tot.cpu().numpy(), orc.ct_sum(s.P, cts.cpu().numpy()))
-    assert not Z.zinc_ct_sum_batch(s.ctx, cts[:0]).any()                      # empty batch -> zero
+    assert not Z.zinc_ct_sum_batch(s.ctx, cts[:0]).cpu().numpy().any()        # empty batch -> zero
     _, st, zz = Z.ckks_decrypt_batch(s.ctx, s.sk, COEFF, tot[None].contiguous())
     assert int(st.sum()) == 0
     assert np.max(np.abs(zz[0].cpu().numpy() - z.sum(axis=0))) < k * cfg.tolerance()
