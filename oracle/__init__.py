@@ -84,6 +84,8 @@ def _declare(L):
         "orc_zinc_encrypt": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_int, _i64p, _c.c_uint64, _c.c_uint64, _u64p]),
         "orc_decrypt": (_c.c_int, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _u64p, _c.c_int, _i64p, _u64p]),
         "orc_ntt_limbs": (None, [_u64p, _c.c_int, _c.c_int, _u64p, _u64p]),
+        "orc_encode_fft_i128": (None, [_f64p, _f64p, _c.c_int, _c.c_int, _i64p]),
+        "orc_decode_fft_i128": (None, [_i64p, _c.c_int, _c.c_int, _f64p, _f64p]),
         "orc_ct_add": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _u64p, _c.c_uint64, _u64p]),
         "orc_ct_sum": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _c.c_uint64, _u64p]),
         "orc_keygen_scaled": (None, [_c.c_int, _c.c_int, _u64p, _u64p, _c.c_uint64, _c.c_int64, _i64p, _u64p, _u64p]),
@@ -428,3 +430,59 @@ def ct_sum(P: Params, ct) -> np.ndarray:
     count = ct.size // (2 * P.L * P.n)
     lib().orc_ct_sum(P.log_n, P.L, _p(P.q, _u64p), _p(ct, _u64p), count, _p(out, _u64p))
     return out
+
+
+# ---------------------------------------------------------------- wide plaintexts (f3: Delta = 2^55)
+def encode_i128(z, log_n: int, log_scale: int) -> np.ndarray:
+    """C-6 encode with 128-bit coefficients: int64[N][2] (lo, hi) pairs."""
+    re, im = _slots(z)
+    m = np.zeros((1 << log_n, 2), dtype=np.int64)
+    lib().orc_encode_fft_i128(_p(re, _f64p), _p(im, _f64p), log_n, log_scale, _p(m, _i64p))
+    return m
+
+
+def decode_i128(x, log_n: int, log_scale: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.int64)
+    re = np.zeros(1 << (log_n - 1)); im = np.zeros_like(re)
+    lib().orc_decode_fft_i128(_p(x, _i64p), log_n, log_scale, _p(re, _f64p), _p(im, _f64p))
+    return re + 1j * im
+
+
+def i128_to_int(m) -> list:
+    """int64[N][2] (lo, hi) pairs -> Python ints."""
+    m = np.asarray(m, dtype=np.int64)
+    return [int(hi) * (1 << 64) + (int(lo) & ((1 << 64) - 1)) for lo, hi in m]
+
+
+def int_to_i128(v) -> np.ndarray:
+    out = np.zeros((len(v), 2), dtype=np.int64)
+    for j, x in enumerate(v):
+        lo = x & ((1 << 64) - 1)
+        out[j, 0] = lo - (1 << 64) if lo >= (1 << 63) else lo
+        out[j, 1] = x >> 64
+    return out
+
+
+def residues_of_ints(P: Params, v) -> np.ndarray:
+    """[L][N] canonical residues of Python-int plaintext coefficients."""
+    return np.array([[x % int(q) for x in v] for q in P.q], dtype=np.uint64)
+
+
+def decrypt_wide(P: Params, sk_ntt, ct, form: int):
+    """Eq. 10 with a two-limb CRT: x in (-q0 q1 / 2, q0 q1 / 2] from limbs 0 and 1 (Python
+    ints), status 0 iff x mod q_i matches every other limb.  Returns (x ints, status)."""
+    _, _, xl = decrypt(P, sk_ntt, ct, form, want_limbs=True)
+    q0, q1 = int(P.q[0]), int(P.q[1])
+    Q2 = q0 * q1
+    inv = pow(q0, -1, q1)
+    xs, st = [], 0
+    for j in range(P.n):
+        x0, x1 = int(xl[0][j]), int(xl[1][j])
+        x = x0 + q0 * (((x1 - x0) * inv) % q1)
+        if x > Q2 // 2:
+            x -= Q2
+        for i in range(2, P.L):
+            if x % int(P.q[i]) != int(xl[i][j]):
+                st = 1
+        xs.append(x)
+    return xs, st

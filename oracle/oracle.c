@@ -438,6 +438,70 @@ void orc_encode_fft(const double *z_re, const double *z_im, int log_n, int log_s
   free(re); free(im);
 }
 
+/* Wide plaintexts (the paper's own parameters: Delta = 2^55
+ * makes |m_j| exceed 2^63 for the paper's value ranges).  Coefficient j is the
+ * 128-bit integer hi.2^64 + lo, stored as int64 pairs m[2j] = lo, m[2j+1] = hi. */
+static void ld_to_i128(long double r, int64_t *out) {
+  /* r integral; long double carries 64 significant bits, so both parts are exact */
+  long double hi = floorl(ldexpl(r, -64));
+  long double lo = r - ldexpl(hi, 64); /* [0, 2^64) */
+  out[0] = (int64_t)(uint64_t)lo;
+  out[1] = (int64_t)hi;
+}
+static long double i128_to_ld(const int64_t *x) {
+  return ldexpl((long double)x[1], 64) + (long double)(uint64_t)x[0];
+}
+/* C-6 encode with 128-bit integer output: the same transform as orc_encode_fft,
+ * rounded half away from zero into m[2N] (lo, hi pairs). */
+void orc_encode_fft_i128(const double *z_re, const double *z_im, int log_n, int log_scale,
+                         int64_t *m) {
+  uint64_t n = 1ull << log_n, two_n = 2 * n, M = n / 2;
+  long double *re = (long double *)calloc(M, sizeof(long double));
+  long double *im = (long double *)calloc(M, sizeof(long double));
+  uint64_t gk = 1;
+  for (uint64_t k = 0; k < M; k++) {
+    uint64_t h = (gk - 1) / 4;
+    re[h] = (long double)z_re[k];
+    im[h] = z_im ? (long double)z_im[k] : 0.0L;
+    gk = (gk * 5) % two_n;
+  }
+  fft_ld(re, im, M, -1);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  long double scale = ldexpl(1.0L, log_scale) / (long double)M;
+  for (uint64_t j = 0; j < M; j++) {
+    long double ang = -pi * (long double)j / (long double)n;
+    long double cr = cosl(ang), ci = sinl(ang);
+    ld_to_i128(roundl((re[j] * cr - im[j] * ci) * scale), m + 2 * j);
+    ld_to_i128(roundl((re[j] * ci + im[j] * cr) * scale), m + 2 * (j + M));
+  }
+  free(re); free(im);
+}
+/* C-10 decode of a 128-bit integer polynomial x[2N] (lo, hi pairs). */
+void orc_decode_fft_i128(const int64_t *x, int log_n, int log_scale, double *z_re,
+                         double *z_im) {
+  uint64_t n = 1ull << log_n, two_n = 2 * n, M = n / 2;
+  long double *re = (long double *)malloc(sizeof(long double) * M);
+  long double *im = (long double *)malloc(sizeof(long double) * M);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (uint64_t j = 0; j < M; j++) {
+    long double ang = pi * (long double)j / (long double)n;
+    long double cr = cosl(ang), ci = sinl(ang);
+    long double vr = i128_to_ld(x + 2 * j), vi = i128_to_ld(x + 2 * (j + M));
+    re[j] = vr * cr - vi * ci;
+    im[j] = vr * ci + vi * cr;
+  }
+  fft_ld(re, im, M, +1);
+  long double inv_scale = ldexpl(1.0L, -log_scale);
+  uint64_t gk = 1;
+  for (uint64_t k = 0; k < M; k++) {
+    uint64_t h = (gk - 1) / 4;
+    z_re[k] = (double)(re[h] * inv_scale);
+    z_im[k] = (double)(im[h] * inv_scale);
+    gk = (gk * 5) % two_n;
+  }
+  free(re); free(im);
+}
+
 /* Decode in O(N log N): z_k = (1/Delta) sum_j v_j zeta^j exp(+2 pi i h_k j / M)
  * with v_j = x_j + i x_{j+M}. */
 void orc_decode_fft(const int64_t *x, int log_n, int log_scale, double *z_re, double *z_im) {
