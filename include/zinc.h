@@ -62,7 +62,12 @@ typedef enum { ZINC_FORM_NTT = 0, ZINC_FORM_COEFF = 1 } zinc_form;
  * (the bit-exact contract); SLOTS_F64: double[B][N/2] real slots;
  * SLOTS_C128: double[B][N/2][2] complex slots (re, im).  Slots are encoded per
  * C-6 (canonical embedding, scale 2^log_scale) inside the library. */
-typedef enum { ZINC_PT_COEFF_I64 = 0, ZINC_PT_SLOTS_F64 = 1, ZINC_PT_SLOTS_C128 = 2 } zinc_pt_kind;
+typedef enum {
+  ZINC_PT_COEFF_I64 = 0,
+  ZINC_PT_SLOTS_F64 = 1,
+  ZINC_PT_SLOTS_C128 = 2,
+  ZINC_PT_COEFF_I128 = 3 /* int64[B][N][2]: coefficient j = hi 2^64 + lo with (lo, hi) at [j][0], [j][1] */
+} zinc_pt_kind;
 
 /* ---- context ------------------------------------------------------------ */
 
@@ -160,9 +165,22 @@ zinc_status zinc_ct_add_batch(const zinc_ctx *ctx, const uint64_t *x, const uint
 zinc_status zinc_ct_sum_batch(const zinc_ctx *ctx, const uint64_t *ct, size_t batch,
                               uint64_t *out, zinc_stream_t stream);
 
+/* Wide decryption (f3): x = [c1 + c2.sk]_Q recovered in (-q0 q1 / 2, q0 q1 / 2] from limbs 0
+ * and 1 by CRT, CRT-checked on every other limb (status 1 on a mismatch); coeff128_out
+ * (int64[B][N][2], may be NULL) receives x, slots_out (may be NULL) its decoding.  Needs
+ * L >= 2 and |m + v| < q0 q1 / 2. */
+zinc_status ckks_decrypt_batch_wide(const zinc_ctx *ctx, const uint64_t *sk_ntt, zinc_form form,
+                                    const uint64_t *ct, size_t batch, double *slots_out,
+                                    int64_t *coeff128_out, int32_t *status_out,
+                                    zinc_stream_t stream);
+
 /* ---- support / test exports ---------------------------------------------- */
 
 /* Encode slots (kind SLOTS_F64 or SLOTS_C128) to int64[batch][N] per C-6. */
+zinc_status ckks_encode_batch_wide(const zinc_ctx *ctx, zinc_pt_kind kind, const void *slots,
+                                   size_t batch, int64_t *m_out /* [batch][N][2] */,
+                                   zinc_stream_t stream);
+/* (ckks_encode_batch_wide: the same, into 128-bit coefficients; ckks_encode_batch below.) */
 zinc_status ckks_encode_batch(const zinc_ctx *ctx, zinc_pt_kind kind, const void *slots,
                               size_t batch, int64_t *m_out, zinc_stream_t stream);
 
@@ -213,7 +231,9 @@ enum {
   ZINC_K_BFV_SCALE = 11, /* BFV decryption: round(t.x/Q) mod t from the RNS residues */
   ZINC_K_CT_ADD = 12,    /* batched ciphertext addition (Eq. 2) */
   ZINC_K_CT_SUM = 13,    /* aggregation of a batch */
-  ZINC_K_COUNT = 14
+  ZINC_K_LIFT = 14,      /* 128-bit plaintexts -> RNS residues */
+  ZINC_K_PT_ADD = 15,    /* c1 += plaintext residues */
+  ZINC_K_COUNT = 16
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */

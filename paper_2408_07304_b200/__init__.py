@@ -29,7 +29,7 @@ __all__ = [
 
 NTT, COEFF = 0, 1
 CKKS, BFV, BGV = 0, 1, 2
-PT_COEFF_I64, PT_SLOTS_F64, PT_SLOTS_C128 = 0, 1, 2
+PT_COEFF_I64, PT_SLOTS_F64, PT_SLOTS_C128, PT_COEFF_I128 = 0, 1, 2, 3
 PATH_ZINC, PATH_VANILLA = 0, 1
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libzinc.so")
@@ -41,11 +41,12 @@ EXPORTED_SYMBOLS = (
     "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse", "zinc_debug_sample", "zinc_int_peak",
     "zinc_encrypt_batch_host", "zinc_launch_count", "zinc_launch_count_reset", "zinc_last_error",
     "zinc_profile_enable", "zinc_profile_read", "zinc_kernel_name", "zinc_tune", "zinc_ctx_create_scheme",
-    "zinc_ctx_scheme", "zinc_ct_add_batch", "zinc_ct_sum_batch",
+    "zinc_ctx_scheme", "zinc_ct_add_batch", "zinc_ct_sum_batch", "ckks_encode_batch_wide", "ckks_decrypt_batch_wide",
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
                 "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel")
+                "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel", "lift_kernel",
+                "pt_add_kernel")
 
 
 class ZincError(RuntimeError):
@@ -77,6 +78,8 @@ _SIGS = {
     "zinc_ctx_scheme": [_vp, _c.POINTER(_c.c_int), _c.POINTER(_u64)],
     "zinc_ct_add_batch": [_vp, _vp, _vp, _sz, _vp, _vp],
     "zinc_ct_sum_batch": [_vp, _vp, _sz, _vp, _vp],
+    "ckks_encode_batch_wide": [_vp, _i32, _vp, _sz, _vp, _vp],
+    "ckks_decrypt_batch_wide": [_vp, _vp, _i32, _vp, _sz, _vp, _vp, _vp, _vp],
 }
 
 _lib = None
@@ -181,7 +184,7 @@ def _as_pt(pt: torch.Tensor) -> torch.Tensor:
 
 def _kind_of(pt: torch.Tensor) -> int:
     if pt.dtype == torch.int64:
-        return PT_COEFF_I64
+        return PT_COEFF_I128 if pt.dim() == 3 else PT_COEFF_I64
     if pt.dtype == torch.float64:
         return PT_SLOTS_C128 if pt.dim() == 3 else PT_SLOTS_F64
     raise ZincError(f"unsupported plaintext dtype {pt.dtype}")
@@ -233,11 +236,36 @@ def ckks_decrypt_batch(ctx: Context, sk_ntt: torch.Tensor, form: int, ct: torch.
     coeff = torch.empty((b, ctx.n), dtype=torch.int64, device=ctx.dev())
     status = torch.empty((b,), dtype=torch.int32, device=ctx.dev())
     slots = slots and ctx.scheme == CKKS  # BFV / BGV: coeff = m in [0, t), no slots
+    wide = ctx.scheme == CKKS and ctx.log_scale >= 48  # 128-bit coefficients: ckks_decrypt_batch_wide
+    if wide:
+        coeff = None
     z = torch.empty((b, ctx.n // 2, 2), dtype=torch.float64, device=ctx.dev()) if slots else None
     _check(lib().ckks_decrypt_batch(ctx.handle, _ptr(sk_ntt), form, _ptr(ct), b, _ptr(z), _ptr(coeff), _ptr(status),
                                     _stream(stream)), "ckks_decrypt_batch")
     zc = torch.view_as_complex(z) if slots else None
     return coeff, status, zc
+
+
+def ckks_encode_batch_wide(ctx: Context, slots: torch.Tensor, out=None, stream=None):
+    """Encode slots (C-6) into 128-bit coefficients. Returns int64 [B,N,2] (lo, hi)."""
+    slots = _as_pt(slots)
+    b = slots.shape[0]
+    m = torch.empty((b, ctx.n, 2), dtype=torch.int64, device=ctx.dev()) if out is None else out
+    _check(lib().ckks_encode_batch_wide(ctx.handle, _kind_of(slots), _ptr(slots), b, _ptr(m), _stream(stream)),
+           "ckks_encode_batch_wide")
+    return m
+
+
+def ckks_decrypt_batch_wide(ctx: Context, sk_ntt: torch.Tensor, form: int, ct: torch.Tensor, slots: bool = True,
+                            stream=None):
+    """Dec with a two-limb CRT (f3). Returns (x int64 [B,N,2] (lo, hi), status int32 [B], slots or None)."""
+    b = ct.shape[0]
+    coeff = torch.empty((b, ctx.n, 2), dtype=torch.int64, device=ctx.dev())
+    status = torch.empty((b,), dtype=torch.int32, device=ctx.dev())
+    z = torch.empty((b, ctx.n // 2, 2), dtype=torch.float64, device=ctx.dev()) if slots else None
+    _check(lib().ckks_decrypt_batch_wide(ctx.handle, _ptr(sk_ntt), form, _ptr(ct), b, _ptr(z), _ptr(coeff),
+                                         _ptr(status), _stream(stream)), "ckks_decrypt_batch_wide")
+    return coeff, status, (torch.view_as_complex(z) if slots else None)
 
 
 def ckks_encode_batch(ctx: Context, slots: torch.Tensor, out=None, stream=None):

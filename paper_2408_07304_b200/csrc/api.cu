@@ -52,7 +52,7 @@ static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
                                                  "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
                                                  "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel",
-                                                 "ct_sum_kernel"};
+                                                 "ct_sum_kernel", "lift_kernel", "pt_add_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -95,6 +95,9 @@ struct TraceScope {
       return fail(ZINC_ECUDA, "launch %s failed: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
+// CKKS scales from 2^48 up encode slots into 128-bit coefficients (f3).
+static const int kWideLogScale = 48;
+
 // ------------------------------------------------------------------ tuning
 static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}};
 
@@ -103,6 +106,7 @@ struct zinc_ctx {
   int device, log_n, n, L, log_scale;
   int scheme = ZINC_SCHEME_CKKS;
   uint64_t t = 0;  // plaintext modulus (BFV, BGV)
+  bool wide = false;  // CKKS with log_scale >= 48: slot plaintexts take the 128-bit path
   std::vector<uint64_t> q, psi;
   std::vector<LimbConst> h_limbs;
   LimbConst *d_limbs = nullptr;
@@ -287,6 +291,7 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
   c->device = device;
   c->scheme = scheme;
   c->t = scheme == ZINC_SCHEME_CKKS ? 0 : plain_modulus;
+  c->wide = scheme == ZINC_SCHEME_CKKS && log_scale >= kWideLogScale;
   c->log_n = log_n;
   c->n = 1 << log_n;
   c->L = L;
@@ -323,6 +328,7 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     lc.ninv_sh = shoup(lc.ninv, q);
     lc.ninv_w = mulm(lc.ninv, itw[(size_t)i * n + 1].x, q);
     lc.ninv_w_sh = shoup(lc.ninv_w, q);
+    lc.r64 = (uint64_t)(((u128)1 << 64) % q);
     // scheme constants (section 4.2)
     lc.scheme = (uint32_t)scheme;
     if (c->t) {
@@ -434,10 +440,11 @@ static zinc_status check_form(int form) {
   return (form == ZINC_FORM_NTT || form == ZINC_FORM_COEFF) ? ZINC_OK : fail(ZINC_EINVAL, "bad form %d", form);
 }
 static zinc_status check_kind(int kind) {
-  return (kind >= ZINC_PT_COEFF_I64 && kind <= ZINC_PT_SLOTS_C128) ? ZINC_OK : fail(ZINC_EINVAL, "bad kind %d", kind);
+  return (kind >= ZINC_PT_COEFF_I64 && kind <= ZINC_PT_COEFF_I128) ? ZINC_OK : fail(ZINC_EINVAL, "bad kind %d", kind);
 }
 static size_t pt_stride_bytes(const zinc_ctx *c, int kind) {
-  return kind == ZINC_PT_COEFF_I64 ? (size_t)c->n * 8 : kind == ZINC_PT_SLOTS_F64 ? (size_t)c->n / 2 * 8 : (size_t)c->n * 8;
+  return kind == ZINC_PT_COEFF_I64 ? (size_t)c->n * 8 : kind == ZINC_PT_SLOTS_F64 ? (size_t)c->n / 2 * 8
+       : kind == ZINC_PT_COEFF_I128 ? (size_t)c->n * 16 : (size_t)c->n * 8;
 }
 
 static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, int64_t *m) {
@@ -454,16 +461,9 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
 }
 
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
-                               cudaStream_t s) {
-  EncodeArgs a{};
-  a.slots = (const double *)slots;
-  a.complex_slots = kind == ZINC_PT_SLOTS_C128;
-  a.perm = c->d_perm;
-  a.fft_tw = c->d_fft_tw;
-  a.twist = c->d_twist;
-  a.fft_tw_h = c->d_fft_tw_h;
-  a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
-  a.m_out = m;
+                               cudaStream_t s, bool wide = false) {
+  EncodeArgs a = encode_args(c, kind, slots, m);
+  a.wide = wide ? 1 : 0;
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
@@ -536,6 +536,47 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   return ZINC_OK;
 }
 
+// 128-bit plaintexts (f3: the paper's Delta = 2^55 puts |m_j| past 2^63).  Eq. 4
+// taken literally: per chunk, [encode slots to 128-bit coefficients ->] lift them
+// to RNS residues (-> NTT in NTT form), run the path with m = 0 and add the
+// residues into c1.  Same ciphertext bits as adding m inside the path kernels
+// (all arithmetic is exact); costs one more pass over c1.
+static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int form, int kind, const void *pt,
+                                size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s) {
+  const bool slots = kind != ZINC_PT_COEFF_I128;
+  const size_t n = c->n, L = c->L;
+  const size_t per_msg = (slots ? n * 16 : 0) + L * n * 8;
+  const size_t chunk = std::max<size_t>(1, std::min(batch, (size_t)(256ull << 20) / per_msg));
+  int64_t *m128 = nullptr;
+  uint64_t *res = nullptr;
+  if (slots) CUDA_TRY(cudaMallocAsync((void **)&m128, chunk * n * 16, s));
+  CUDA_TRY(cudaMallocAsync((void **)&res, chunk * L * n * 8, s));
+  const size_t in_stride = pt_stride_bytes(c, kind), ct_stride = 2 * L * n;
+  zinc_status st = ZINC_OK;
+  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
+    const size_t cnt = std::min(chunk, batch - off);
+    const int64_t *mw = slots ? m128 : (const int64_t *)((const char *)pt + off * in_stride);
+    if (slots && (st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m128, s, true))) break;
+    LiftArgs la{c->d_limbs, mw, res, cnt, (int)n, (int)L};
+    LAUNCH(ZINC_K_LIFT, s, launch_lift(la, s));
+    if (form == ZINC_FORM_NTT) {
+      NttArgs na{};
+      na.limbs = c->d_limbs;
+      na.tw = c->d_tw;
+      na.itw = c->d_itw;
+      na.data = res;
+      na.L = (int)L;
+      LAUNCH(ZINC_K_NTT, s, launch_ntt(c->log_n, na, 0, cnt * L, s));
+    }
+    if ((st = run_path(c, path, key, form, nullptr, cnt, seed, msg_base + off, ct + off * ct_stride, s))) break;
+    PtAddArgs pa{c->d_limbs, res, ct + off * ct_stride, cnt, (int)n, (int)L};
+    LAUNCH(ZINC_K_PT_ADD, s, launch_pt_add(pa, s));
+  }
+  if (m128) cudaFreeAsync(m128, s);
+  cudaFreeAsync(res, s);
+  return st;
+}
+
 // Encryption with any plaintext kind: int64 plaintexts go straight to the path
 // kernel; slots are encoded chunk by chunk into stream-ordered scratch sized to
 // stay resident in L2 between the encode and the path kernel.  The encodes run
@@ -547,6 +588,7 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
                                cudaStream_t s) {
   zinc_ctx *c = const_cast<zinc_ctx *>(cc);
   if (kind == ZINC_PT_COEFF_I64) return run_path(c, path, key, form, (const int64_t *)pt, batch, seed, msg_base, ct, s);
+  if (kind == ZINC_PT_COEFF_I128 || c->wide) return encrypt_wide(c, path, key, form, kind, pt, batch, seed, msg_base, ct, s);
   const size_t per_msg = (size_t)c->n * 8;
   const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());
   const size_t chunk = std::max<size_t>(1, std::min(batch, chunk_bytes / per_msg));
@@ -687,21 +729,46 @@ zinc_status ckks_encrypt_batch(const zinc_ctx *c, const uint64_t *pk_ntt, zinc_f
   return encrypt_any(c, PATH_VANILLA, pk_ntt, form, kind, pt, batch, seed, msg_base, ct, (cudaStream_t)stream);
 }
 
+static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int form, const uint64_t *ct,
+                                size_t batch, double *slots_out, int64_t *coeff_out, int64_t *coeff128_out,
+                                int32_t *status_out, bool wide, cudaStream_t s);
+
 zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_form form, const uint64_t *ct,
                                size_t batch, double *slots_out, int64_t *coeff_out, int32_t *status_out,
                                zinc_stream_t stream) {
   if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (c->wide && coeff_out)
+    return fail(ZINC_EINVAL, "log_scale >= 48: coefficients are 128-bit, use ckks_decrypt_batch_wide");
+  return decrypt_impl(c, sk_ntt, form, ct, batch, slots_out, coeff_out, nullptr, status_out, c->wide,
+                      (cudaStream_t)stream);
+}
+
+zinc_status ckks_decrypt_batch_wide(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_form form, const uint64_t *ct,
+                                    size_t batch, double *slots_out, int64_t *coeff128_out, int32_t *status_out,
+                                    zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (c->scheme != ZINC_SCHEME_CKKS) return fail(ZINC_EINVAL, "wide decryption is for CKKS contexts");
+  if (c->L < 2) return fail(ZINC_EINVAL, "wide decryption needs at least two limbs");
+  return decrypt_impl(c, sk_ntt, form, ct, batch, slots_out, nullptr, coeff128_out, status_out, true,
+                      (cudaStream_t)stream);
+}
+
+static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int form, const uint64_t *ct,
+                                size_t batch, double *slots_out, int64_t *coeff_out, int64_t *coeff128_out,
+                                int32_t *status_out, bool wide, cudaStream_t s) {
   if (batch == 0) return ZINC_OK;
   zinc_status st;
   if ((st = check_form(form)) || (st = check_ptrs({sk_ntt, ct}))) return st;
   for (const void *p : {(const void *)slots_out, (const void *)coeff_out, (const void *)status_out})
     if (p && ((uintptr_t)p & 7u)) return fail(ZINC_EINVAL, "output pointer misaligned");
+  if (coeff128_out && ((uintptr_t)coeff128_out & 15u)) return fail(ZINC_EINVAL, "output pointer misaligned");
   if (c->scheme != ZINC_SCHEME_CKKS && slots_out)
     return fail(ZINC_EINVAL, "BFV / BGV decryption has no slot decoding (slots_out must be NULL)");
   CUDA_TRY(cudaSetDevice(c->device));
-  cudaStream_t s = (cudaStream_t)stream;
   int64_t *x = coeff_out;
   if (!x) CUDA_TRY(cudaMallocAsync((void **)&x, batch * (size_t)c->n * 8, s));
+  int64_t *xw = coeff128_out;
+  if (wide && !xw) CUDA_TRY(cudaMallocAsync((void **)&xw, batch * (size_t)c->n * 16, s));
   DecryptArgs a{};
   a.limbs = c->d_limbs;
   a.tw = c->d_tw;
@@ -711,6 +778,10 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
   a.coeff_out = x;
   a.status_out = status_out;
   a.L = c->L;
+  if (wide) {
+    a.x128_out = xw;
+    a.q0inv_q1 = powm(c->q[0] % c->q[1], c->q[1] - 2, c->q[1]);
+  }
   uint64_t *xl = nullptr;
   if (c->scheme == ZINC_SCHEME_BFV) {
     CUDA_TRY(cudaMallocAsync((void **)&xl, batch * (size_t)c->L * c->n * 8, s));
@@ -740,7 +811,8 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
   if (xl) cudaFreeAsync(xl, s);
   if (st == ZINC_OK && slots_out) {
     DecodeArgs d{};
-    d.coeff = x;
+    d.coeff = wide ? xw : x;
+    d.wide = wide ? 1 : 0;
     d.perm = c->d_perm;
     d.fft_tw = c->d_fft_tw;
     d.twist = c->d_twist;
@@ -755,6 +827,7 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
     if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decode launch: %s", cudaGetErrorString(e));
   }
   if (!coeff_out) cudaFreeAsync(x, s);
+  if (wide && !coeff128_out) cudaFreeAsync(xw, s);
   return st;
 }
 
@@ -792,6 +865,17 @@ zinc_status zinc_ct_sum_batch(const zinc_ctx *c, const uint64_t *ct, size_t batc
   a.L = c->L;
   LAUNCH(ZINC_K_CT_SUM, (cudaStream_t)stream, launch_ct_sum(a, (cudaStream_t)stream));
   return ZINC_OK;
+}
+
+zinc_status ckks_encode_batch_wide(const zinc_ctx *c, zinc_pt_kind kind, const void *slots, size_t batch,
+                                   int64_t *m_out, zinc_stream_t stream) {
+  if (!c) return fail(ZINC_EINVAL, "null ctx");
+  if (batch == 0) return ZINC_OK;
+  if (kind != ZINC_PT_SLOTS_F64 && kind != ZINC_PT_SLOTS_C128) return fail(ZINC_EINVAL, "encode needs a slot kind");
+  zinc_status st;
+  if ((st = check_ptrs({slots, m_out}))) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  return encode_into(c, kind, slots, batch, m_out, (cudaStream_t)stream, true);
 }
 
 zinc_status ckks_encode_batch(const zinc_ctx *c, zinc_pt_kind kind, const void *slots, size_t batch, int64_t *m_out,

@@ -34,6 +34,7 @@ struct LimbConst {
   uint64_t delta_sh;
   uint64_t dec_i;    // BFV decrypt: floor(t Q~_i / q_i) mod t, Q~_i = (Q/q_i)^-1 mod q_i
   uint64_t dec_f;    // BFV decrypt: round(frac(t Q~_i / q_i) 2^64)
+  uint64_t r64;      // 2^64 mod q (128-bit plaintext residues)
 };
 enum : uint32_t { SCHEME_CKKS = 0, SCHEME_BFV = 1, SCHEME_BGV = 2 };
 
@@ -85,6 +86,30 @@ ZINC_DEV uint64_t reduce_m_plus_e(int64_t m, int e, uint64_t q, uint64_t mu) {
 // Residue of a small signed value |v| < q.
 ZINC_DEV uint64_t reduce_small(int64_t v, uint64_t q) {
   return v < 0 ? (uint64_t)(v + (int64_t)q) : (uint64_t)v;
+}
+
+// ------------------------------------------------------------------ wide plaintexts
+// A 128-bit plaintext coefficient is stored as an int64 pair (lo, hi): v = hi 2^64 + lo.
+// Integral double -> pair (round half away from zero first, as llround does).
+ZINC_DEV void store_i128(int64_t *p, double v) {
+  const double r = round(v);
+  if (fabs(r) < 9.0e18) {
+    const int64_t x = (int64_t)r;
+    p[0] = x;
+    p[1] = x < 0 ? -1 : 0;
+  } else {  // |r| >= 2^63: r has at most 53 significant bits, both parts are exact
+    const double hi = floor(r * 0x1p-64);
+    const double lo = r - hi * 0x1p64;  // [0, 2^64)
+    p[0] = (int64_t)(uint64_t)lo;
+    p[1] = (int64_t)hi;
+  }
+}
+ZINC_DEV double load_i128(const int64_t *p) { return (double)p[1] * 0x1p64 + (double)(uint64_t)p[0]; }
+// Canonical residue of hi 2^64 + lo (hi signed, lo unsigned).
+ZINC_DEV uint64_t reduce_i128(int64_t hi, uint64_t lo, const LimbConst &c) {
+  uint64_t l = lo - __umul64hi(lo, c.mu64) * c.q;  // [0, 2q)
+  l = csub(l, c.q);
+  return add_mod(mul_mod(reduce_i64q(hi, c.q, c.mu64), c.r64, c), l, c.q);
 }
 
 // ------------------------------------------------------------------ schemes

@@ -32,7 +32,7 @@ template <int LOGM> constexpr size_t encode_real_smem() {
 }
 
 // One CTA's work: encode message `b`; `buf` is the CTA's dynamic shared memory.
-template <int LOGM>
+template <int LOGM, bool WIDE = false>
 ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   constexpr int M = 1 << LOGM, LH = LOGM - 1, H = 1 << LH;
   constexpr int THREADS = 256, PER = M / THREADS;
@@ -73,7 +73,7 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   __syncthreads();
   fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, true>(stw, lds, sts);
   __syncthreads();
-  int64_t *m = a.m_out + b * (2 * M);
+  int64_t *m = a.m_out + b * (2 * M) * (WIDE ? 2 : 1);
   const double scale = a.scale;  // Delta / M
   constexpr int V = 4;  // independent post-processing iterations per batch
   static_assert(H % (THREADS * V) == 0, "post tiling");
@@ -96,10 +96,17 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
       const double2 o = make_double2(d.y, -d.x);  // -i d
       const double2 t = cmul(o, w[u]);
       const double2 y0 = cmul(cadd(e, t), tw0[u]), y1 = cmul(csubd(e, t), tw1[u]);
-      m[j] = llround(y0.x * scale);  // plain stores: the path kernel re-reads m from L2
-      m[j + M] = llround(y0.y * scale);
-      m[j + H] = llround(y1.x * scale);
-      m[j + H + M] = llround(y1.y * scale);
+      if constexpr (WIDE) {  // 128-bit coefficients (f3: Delta = 2^55 and large slots)
+        store_i128(m + 2 * j, y0.x * scale);
+        store_i128(m + 2 * (j + M), y0.y * scale);
+        store_i128(m + 2 * (j + H), y1.x * scale);
+        store_i128(m + 2 * (j + H + M), y1.y * scale);
+      } else {
+        m[j] = llround(y0.x * scale);  // plain stores: the path kernel re-reads m from L2
+        m[j + M] = llround(y0.y * scale);
+        m[j + H] = llround(y1.x * scale);
+        m[j + H + M] = llround(y1.y * scale);
+      }
     }
   }
 }

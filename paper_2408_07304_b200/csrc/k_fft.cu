@@ -37,12 +37,17 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   __syncthreads();
   fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
   __syncthreads();
-  int64_t *m = a.m_out + b * (2 * M);
+  int64_t *m = a.m_out + b * (2 * M) * (a.wide ? 2 : 1);
   const double scale = a.scale;  // Delta / M, a power of two
   auto emit = [&](int j, double2 v) {
     const double2 w = cmul(v, __ldg(a.twist + j));
-    m[j] = llround(w.x * scale);
-    m[j + M] = llround(w.y * scale);
+    if (a.wide) {
+      store_i128(m + 2 * j, w.x * scale);
+      store_i128(m + 2 * (j + M), w.y * scale);
+    } else {
+      m[j] = llround(w.x * scale);
+      m[j + M] = llround(w.y * scale);
+    }
   };
   if constexpr (!SPLIT) {
     fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false>(a.fft_tw, lds, emit);
@@ -62,10 +67,10 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
 
 // ============================================================ encode, real slots
 // (body in encode_real.cuh)
-template <int LOGM>
+template <int LOGM, bool WIDE>
 __global__ void __launch_bounds__(256, (LOGM <= 13 ? 2 : 1)) encode_real_kernel(EncodeArgs a) {
   extern __shared__ __align__(16) double2 buf[];
-  encode_real_body<LOGM>(a, blockIdx.x, buf);
+  encode_real_body<LOGM, WIDE>(a, blockIdx.x, buf);
 }
 
 // ============================================================ decode (C-10)
@@ -83,11 +88,12 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   extern __shared__ __align__(16) double2 buf[];
   const size_t b = blockIdx.x / (SPLIT ? 2 : 1);
   const int r = SPLIT ? (int)cluster_rank() : 0;
-  const int64_t *x = a.coeff + b * (2 * M);
+  const int64_t *x = a.coeff + b * (2 * M) * (a.wide ? 2 : 1);
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
   auto twisted = [&](int j) {
-    const double2 v = make_double2((double)x[j], (double)x[j + M]);
+    const double2 v = a.wide ? make_double2(load_i128(x + 2 * j), load_i128(x + 2 * (j + M)))
+                             : make_double2((double)x[j], (double)x[j + M]);
     return cmul(v, conj2(__ldg(a.twist + j)));
   };
   if constexpr (!SPLIT) {
@@ -121,7 +127,8 @@ template <int LOGM> static size_t fft_smem() {
 template <int LOGM>
 static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
   if (!a.complex_slots) {
-    return launch_ex(encode_real_kernel<LOGM>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
+    if (a.wide) return launch_ex(encode_real_kernel<LOGM, true>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
+    return launch_ex(encode_real_kernel<LOGM, false>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
   }
   constexpr int C = LOGM > 13 ? 2 : 1;
   return launch_ex(encode_kernel<LOGM>, dim3((unsigned)(batch * C)), FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,

@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256, 2) zinc_coeff_encode_kernel(ZincCoeffArgs
   const int P = enc_ctas > 0 ? max(1, (int)gridDim.x / enc_ctas) : 1 << 30;
   const int e = bid / P;
   if (bid % P == 0 && e < enc_ctas) {
-    encode_real_body<LOGM>(ea, (size_t)e, reinterpret_cast<double2 *>(smem));
+    encode_real_body<LOGM, false>(ea, (size_t)e, reinterpret_cast<double2 *>(smem));
   } else {
     const int z = bid - min(enc_ctas, e + 1);
     zinc_coeff_body<LC>(za, z % gx, z / gx, smem);

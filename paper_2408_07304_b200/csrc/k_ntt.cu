@@ -132,6 +132,24 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs
         a.xl_out[(b * L + i) * N + x] = xi;
         return;
       }
+      if (a.x128_out) {  // wide CKKS: x from limbs 0 and 1, checked on the others
+        int64_t *xw = a.x128_out + (b * N + x) * 2;
+        if (i == 0) {
+          xw[0] = (int64_t)xi;
+        } else if (i == 1) {
+          const uint64_t x0 = (uint64_t)xw[0];
+          const uint64_t x0r = reduce_i64q((int64_t)x0, q, c.mu64);
+          const uint64_t k = mul_mod(add_mod(xi, x0r ? q - x0r : 0, q), a.q0inv_q1, c);  // (x1 - x0) / q0 mod q1
+          unsigned __int128 X = (unsigned __int128)k * q0 + x0;  // [0, q0 q1)
+          const unsigned __int128 Q2 = (unsigned __int128)q0 * q;
+          __int128 Xs = (X > Q2 / 2) ? (__int128)X - (__int128)Q2 : (__int128)X;
+          xw[0] = (int64_t)(uint64_t)Xs;
+          xw[1] = (int64_t)(Xs >> 64);
+        } else if (reduce_i128(xw[1], (uint64_t)xw[0], c) != xi) {
+          bad = 1;
+        }
+        return;
+      }
       if (i == 0) {
         x0[x] = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
       } else {

@@ -66,6 +66,42 @@ cudaError_t launch_ct_sum(const CtSumArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ============================================================ wide plaintexts (f3)
+// res[b][i][j] = (hi 2^64 + lo) mod q_i for 128-bit coefficients (the paper's own
+// parameters put |Delta z| above 2^63).
+__global__ void __launch_bounds__(256) lift_kernel(LiftArgs a) {
+  const size_t total = a.batch * (size_t)a.n;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = idx / a.n, j = idx % a.n;
+    const int64_t lo = a.m[2 * idx], hi = a.m[2 * idx + 1];
+    for (int i = 0; i < a.L; ++i) a.res[(b * a.L + i) * a.n + j] = reduce_i128(hi, (uint64_t)lo, a.limbs[i]);
+  }
+}
+// Eq. 4 on a ciphertext of m = 0: c1 += m (residues in the ciphertext's form).
+__global__ void __launch_bounds__(256) pt_add_kernel(PtAddArgs a) {
+  const size_t ln = (size_t)a.L * a.n, pairs = a.batch * ln / 2;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += (size_t)gridDim.x * blockDim.x) {
+    const size_t w = 2 * p, b = w / ln, r = w % ln;
+    const uint64_t q = __ldg(&a.limbs[r / a.n].q);
+    uint64_t *c1 = a.ct + b * 2 * ln + r;
+    const ulonglong2 x = ld2_nc(a.res + w);
+    uint64_t c0, c1v;
+    ld2(c1, c0, c1v);
+    st2(c1, add_mod(c0, x.x, q), add_mod(c1v, x.y, q));
+  }
+}
+cudaError_t launch_lift(const LiftArgs &a, cudaStream_t s) {
+  const size_t total = a.batch * (size_t)a.n;
+  lift_kernel<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_pt_add(const PtAddArgs &a, cudaStream_t s) {
+  const size_t pairs = a.batch * (size_t)a.L * a.n / 2;
+  pt_add_kernel<<<(unsigned)std::min<size_t>((pairs + 255) / 256, 148 * 16), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 // ============================================================ samplers (debug)
 __global__ void sample_kernel(SampleArgs a) {
   size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -56,7 +56,23 @@ struct DecryptArgs {
   int64_t *coeff_out;
   int32_t *status_out;
   uint64_t *xl_out;       // BFV: residues [B][L][N] for bfv_scale_kernel
+  int64_t *x128_out;      // wide CKKS: x from limbs 0 and 1 (two-limb CRT), int64 pairs [B][N][2]
+  uint64_t q0inv_q1;      // q_0^-1 mod q_1
   int L;
+};
+struct LiftArgs {           // 128-bit plaintexts -> RNS residues (f3)
+  const LimbConst *limbs;
+  const int64_t *m;         // int64 pairs [B][N][2]
+  uint64_t *res;            // [B][L][N]
+  size_t batch;
+  int n, L;
+};
+struct PtAddArgs {          // c1 += plaintext residues (Eq. 4 on a ciphertext of m = 0)
+  const LimbConst *limbs;
+  const uint64_t *res;      // [B][L][N] (in the ciphertext's form)
+  uint64_t *ct;             // [B][2][L][N]
+  size_t batch;
+  int n, L;
 };
 struct BfvScaleArgs {
   const LimbConst *limbs;
@@ -71,11 +87,13 @@ struct EncodeArgs {
   const int *perm;
   const double2 *fft_tw, *twist;
   const double2 *fft_tw_h;  // W_{M/2}^e, e < M/4 (real-slot path)
+  int wide;                 // m_out holds 128-bit coefficients (int64 pairs)
   double scale;
   int64_t *m_out;
 };
 struct DecodeArgs {
-  const int64_t *coeff;
+  const int64_t *coeff;     // int64 [B][N], or int64 pairs [B][N][2] when wide
+  int wide;
   const int *perm;
   const double2 *fft_tw, *twist;
   double inv_scale;
@@ -126,6 +144,8 @@ cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, bool ints, size_t b
 cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);
 cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s);
 cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s);
+cudaError_t launch_lift(const LiftArgs &a, cudaStream_t s);
+cudaError_t launch_pt_add(const PtAddArgs &a, cudaStream_t s);
 cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s);
 cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s);
 cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s);
