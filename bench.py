@@ -307,6 +307,36 @@ def other_configs(Z, torch, names=("C1", "C2", "C4"), reps=2):
     return out
 
 
+def paper_params(Z, torch, reps=2, cap=4096):
+    """the paper's own parameters (N = 2^15, 881-bit Q, Delta = 2^55) on the
+    Table 2 dataset shapes (synthetic stand-ins, workloads.py).  Zinc (COEFF) and vanilla (NTT
+    form) from slots through the 128-bit plaintext path; up to `cap` messages per timed call,
+    job time = count / rate.  The paper's single-threaded SEAL totals are context only."""
+    paper_s = {"P_covid": (19.2, 8.2), "P_bitcoin": (62.2, 24.8), "P_hg38": (1983.6, 812.6)}  # Table 2
+    out = {}
+    for name in ("P_covid", "P_bitcoin", "P_hg38"):
+        cfg = CONFIGS[name]
+        ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
+        sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
+        cache = Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, Z.COEFF)
+        B = min(cfg.batch, cap)
+        zd = torch.from_numpy(np.ascontiguousarray(slots_batch(cfg, 0, B))).cuda()
+        ct = ctx.empty_ct(B)
+        zc = _timed(torch, lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, zd, cfg.enc_seed, 0, out=ct), reps)
+        _, st, zz = Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct[:8])
+        err = float(np.max(np.abs(zz.cpu().numpy() - slots_batch(cfg, 0, 8))))
+        vn = _timed(torch, lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, zd, cfg.enc_seed, 0, out=ct), reps)
+        rz, rv = B / (zc / 1e3), B / (vn / 1e3)
+        out[name] = {"count": cfg.batch, "timed_batch": B, "zinc_coeff_ct_per_s": rz, "vanilla_ntt_ct_per_s": rv,
+                     "zinc_job_s": cfg.batch / rz, "vanilla_job_s": cfg.batch / rv,
+                     "paper_seal_cpu_s": {"ckks": paper_s[name][0], "zinc": paper_s[name][1]},
+                     "decrypt_ok": int(st.sum().item()) == 0 and err < 1e-4, "max_abs_err_8": err}
+        del ct, zd
+        ctx.close()
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -532,6 +562,7 @@ def main():
             ct = None
             torch.cuda.empty_cache()
         result["other_configs"] = other_configs(Z, torch)
+        result["paper_params"] = paper_params(Z, torch)
 
     # ---------------- end to end through the host-buffer API
     if not args.no_e2e:

@@ -55,12 +55,21 @@ def _cfg(name, id_, log_n, bits, log_scale, batch, dist, complex_slots=False, ba
                   key_seed=0x5EED0000 + id_, cache_seed=0xCAC4E000 + id_, enc_seed=0xE4C00000 + id_)
 
 
+PAPER_BITS = (56,) + (55,) * 15  # BFVDefault(32768), 881-bit Q; the 56-bit prime is limb 0 (C-10)
+
 CONFIGS = {
     "C1": _cfg("C1", 1, 12, [36] * 3, 30, 256, "uniform"),
     "C2": _cfg("C2", 2, 13, [60, 40, 40, 60], 40, 4096, "uniform"),
     "C3": _cfg("C3", 3, 14, [54] * 8, 40, 16384, "c3_mix"),
     "C4": _cfg("C4", 4, 15, [55] * 16, 40, 8192, "complex_uniform", complex_slots=True),
     "C5": _cfg("C5", 5, 14, [54] * 8, 40, 4096, "uniform", batches=(1, 16, 256, 4096, 65536)),
+    # the paper's own parameters (N = 2^15, Delta = 2^55) with
+    # stand-ins shaped like Table 2's datasets (the data are not in the container):
+    # one ciphertext per Covid-19 day (16 metrics), per Bitcoin value, per hg38 row (values < 2^9,
+    # PAPER.md:396).  Counts are the paper's; value recipes are stated in message_slots.
+    "P_covid": _cfg("P_covid", 11, 15, PAPER_BITS, 55, 341, "covid"),
+    "P_bitcoin": _cfg("P_bitcoin", 12, 15, PAPER_BITS, 55, 1086, "bitcoin"),
+    "P_hg38": _cfg("P_hg38", 13, 15, PAPER_BITS, 55, 34424, "hg38"),
 }
 
 
@@ -75,6 +84,18 @@ def message_slots(cfg: Config, b: int) -> np.ndarray:
         if (b % cfg.batch) < cfg.batch // 2:
             return rng.uniform(-1.0, 1.0, s)
         return np.clip(rng.standard_normal(s), -4.0, 4.0)
+    if cfg.dist == "covid":      # 16 daily counts in the first slots, rest zero
+        out = np.zeros(s)
+        out[:16] = rng.integers(0, 1 << 20, 16)
+        return out
+    if cfg.dist == "bitcoin":    # one price-like value (needs 32 Rache pivots: < 2^32) in slot 0
+        out = np.zeros(s)
+        out[0] = rng.integers(1 << 20, 1 << 32)
+        return out
+    if cfg.dist == "hg38":       # one row of small genomic counts (< 2^9) in the first slots
+        out = np.zeros(s)
+        out[:8] = rng.integers(0, 1 << 9, 8)
+        return out
     if cfg.dist == "complex_uniform":
         re = rng.uniform(-1.0, 1.0, s)
         im = rng.uniform(-1.0, 1.0, s)
