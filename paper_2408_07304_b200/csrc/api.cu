@@ -470,6 +470,14 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
 
 // One encryption path over messages whose int64 plaintexts are at m (or none).
 enum Path { PATH_ZINC = 0, PATH_VANILLA = 1 };
+// Instantiation of the NTT-path kernels: 0 CKKS with lazy-free forward transforms (all
+// q < 2^59, so (1 + 2 log2 N) q < 2^64), 1 CKKS with conditional subtractions, 2 BFV / BGV.
+static int kernel_mode(const zinc_ctx *c) {
+  if (c->scheme != ZINC_SCHEME_CKKS) return 2;
+  for (uint64_t q : c->q)
+    if (q >= (1ull << 59)) return 1;
+  return 0;
+}
 static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, const int64_t *m, size_t batch,
                                      uint64_t seed, uint64_t msg_base, uint64_t *ct) {
   ZincCoeffArgs a{};
@@ -518,7 +526,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
-    LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, c->scheme != ZINC_SCHEME_CKKS, batch, groups, s));
+    LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, kernel_mode(c), batch, groups, s));
     return ZINC_OK;
   }
   VanillaArgs a{};
@@ -532,7 +540,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
-  LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, c->scheme != ZINC_SCHEME_CKKS, batch, groups, s));
+  LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, kernel_mode(c), batch, groups, s));
   return ZINC_OK;
 }
 

@@ -154,6 +154,17 @@ ZINC_DEV void gs_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_
 }
 // [0, 4q) -> [0, q)
 ZINC_DEV uint64_t canon4(uint64_t x, uint64_t q, uint64_t two_q) { return csub(csub(x, two_q), q); }
+// Forward butterfly without the conditional subtraction: X, Y < B q -> X' , Y' < (B + 2) q
+// (T = Shoup(Y) < 2q for any 64-bit Y).  Canonical inputs grow to < (1 + 2 s) q after s
+// stages, so a whole transform stays below 2^64 while (1 + 2 log2 N) q < 2^64: q < 2^59 for
+// N <= 2^15 ("lazy-free" transforms; 6 fewer ALU instructions per butterfly).
+ZINC_DEV void ct_bfly_nr(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
+  const uint64_t t = mul_shoup_lazy(Y, w, wp, q);
+  Y = X - t + two_q;
+  X = X + t;
+}
+// Any 64-bit value -> [0, q) (mu = floor(2^64 / q)): the end of a lazy-free transform.
+ZINC_DEV uint64_t reduce64(uint64_t x, uint64_t q, uint64_t mu) { return csub(x - __umul64hi(x, mu) * q, q); }
 
 // ------------------------------------------------------------------ Philox4x32-10
 // Salmon et al., SC'11.  Counter (block, msg_lo, msg_hi, tag<<16|limb),

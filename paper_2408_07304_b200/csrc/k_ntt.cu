@@ -6,8 +6,11 @@ namespace zinc {
 // ============================================================ Zinc, NTT form
 // c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2') (two DFTs,
 // no multiplication).
-template <int LOGN, bool INTS>
+// MODE 0: CKKS, lazy-free butterflies (every q < 2^59); 1: CKKS with conditional
+// subtractions; 2: BFV / BGV terms (with subtractions).
+template <int LOGN, int MODE>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArgs a) {
+  constexpr bool INTS = MODE == 2, NR = MODE == 0;
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
   constexpr int THREADS = G::THREADS;
@@ -38,21 +41,22 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArg
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
-    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
-                           to_smem<LOGN>(sm), stw);
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
+    ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
+                               to_smem<LOGN>(sm), stw);
     __syncthreads();
     stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
       const ulonglong2 z = ld2_nc(z1 + x);
-      st2_cs(ct0 + x, add_mod(z.x, canon4(v0, q, two_q), q), add_mod(z.y, canon4(v1, q, two_q), q));
+      st2_cs(ct0 + x, add_mod(z.x, canon(v0), q), add_mod(z.y, canon(v1), q));
     });
-    ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
+    ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
     __syncthreads();
     if constexpr (STW) {
       if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
     }
     stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
       const ulonglong2 z = ld2_nc(z2 + x);
-      st2_cs(ct1 + x, add_mod(z.x, canon4(v0, q, two_q), q), add_mod(z.y, canon4(v1, q, two_q), q));
+      st2_cs(ct1 + x, add_mod(z.x, canon(v0), q), add_mod(z.y, canon(v1), q));
     });
   }
 }
@@ -244,15 +248,16 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) ntt_kernel(NttArgs a) {
 }
 
 template <int LOGN>
-static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, bool ints, size_t batch, int groups, cudaStream_t s) {
+static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
   using G = Geo<LOGN>;
   const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN) + (G::SPLIT ? 0 : kSmemTw * sizeof(Tw));
   const dim3 grid = msg_grid<LOGN>(batch, groups);
-  if (ints) return launch_ex(zinc_ntt_kernel<LOGN, true>, grid, G::THREADS, smem, G::CLUSTER, s, a);
-  return launch_ex(zinc_ntt_kernel<LOGN, false>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  if (mode == 2) return launch_ex(zinc_ntt_kernel<LOGN, 2>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  if (mode == 1) return launch_ex(zinc_ntt_kernel<LOGN, 1>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(zinc_ntt_kernel<LOGN, 0>, grid, G::THREADS, smem, G::CLUSTER, s, a);
 }
-cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, bool ints, size_t batch, int groups, cudaStream_t s) {
-#define CALL(K) launch_zinc_ntt_t<K>(a, ints, batch, groups, s)
+cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
+#define CALL(K) launch_zinc_ntt_t<K>(a, mode, batch, groups, s)
   ZINC_LOGN_SWITCH(log_n, CALL)
 #undef CALL
 }

@@ -13,8 +13,10 @@ namespace zinc {
 //  COEFF form: NTT(u) -> epilogue: ct1 <- pk2 u^ (temporary), smem <- pk1 u^;
 //              INTT(smem) + e1 + m -> ct0;  INTT(ct1) + e2 -> ct1.
 // 3 transforms per limb either way.
-template <int LOGN, int FORM, bool INTS>
+// MODE as zinc_ntt_kernel: 0 CKKS lazy-free forward transforms (q < 2^59), 1 CKKS, 2 BFV / BGV.
+template <int LOGN, int FORM, int MODE>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs a) {
+  constexpr bool INTS = MODE == 2, NR = MODE == 0;
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
   constexpr int THREADS = G::THREADS;
@@ -53,26 +55,27 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
     if (FORM == 0) {
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
+      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
                              to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
-        st2(ct0 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
+        st2(ct0 + x, canon(v0), canon(v1));
       });
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
+      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
-        st2(ct1 + x, canon4(v0, q, two_q), canon4(v1, q, two_q));
+        st2(ct1 + x, canon(v0), canon(v1));
       });
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
+      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
                              stw);
       __syncthreads();
       if constexpr (STW) {
         if (i + 1 < hi) tws.issue(stw, tw + N);
       }
       stream_pairs<LOGN, 2>(sm, [&](int x, uint64_t v0, uint64_t v1) {
-        const uint64_t u0 = canon4(v0, q, two_q), u1 = canon4(v1, q, two_q);
+        const uint64_t u0 = canon(v0), u1 = canon(v1);
         const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
         uint64_t a0, a1, b0, b1;
         ld2(ct0 + x, a0, a1);
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
         st2_cs(ct1 + x, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
       });
     } else {
-      ntt_forward<LOGN, STW>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
+      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
                              stw);
       __syncthreads();
       if constexpr (STW) {
@@ -89,7 +92,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
         itws.wait();
       }
       stream_pairs<LOGN, 2>(sm, [&](int x, uint64_t v0, uint64_t v1) {
-        const uint64_t u0 = canon4(v0, q, two_q), u1 = canon4(v1, q, two_q);
+        const uint64_t u0 = canon(v0), u1 = canon(v1);
         const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
         st2(ct1 + x, mul_mod(p2.x, u0, c), mul_mod(p2.y, u1, c));  // temporary: pk2 u^
         sm[pad16(x - loff)] = mul_mod(p1.x, u0, c);                 // in place: pk1 u^
@@ -124,22 +127,21 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
 }
 
 template <int LOGN>
-static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, bool ints, size_t batch, int groups,
+static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                                     cudaStream_t s) {
   using G = Geo<LOGN>;
   const size_t twb = G::SPLIT ? 0 : (size_t)(form == 0 ? 1 : 2) * kSmemTw * sizeof(Tw);
   const size_t smem = ntt_smem_bytes<LOGN>() + (1 << LOGN) / 4 + 2 * (1 << LOGN) + twb;
   const dim3 grid = msg_grid<LOGN>(batch, groups);
-  if (ints) {
-    if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0, true>, grid, G::THREADS, smem, G::CLUSTER, s, a);
-    return launch_ex(vanilla_kernel<LOGN, 1, true>, grid, G::THREADS, smem, G::CLUSTER, s, a);
-  }
-  if (form == 0) return launch_ex(vanilla_kernel<LOGN, 0, false>, grid, G::THREADS, smem, G::CLUSTER, s, a);
-  return launch_ex(vanilla_kernel<LOGN, 1, false>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+#define VK(F, M) launch_ex(vanilla_kernel<LOGN, F, M>, grid, G::THREADS, smem, G::CLUSTER, s, a)
+  if (mode == 2) return form == 0 ? VK(0, 2) : VK(1, 2);
+  if (mode == 1) return form == 0 ? VK(0, 1) : VK(1, 1);
+  return form == 0 ? VK(0, 0) : VK(1, 0);
+#undef VK
 }
-cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, bool ints, size_t batch, int groups,
+cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                            cudaStream_t s) {
-#define CALL(K) launch_vanilla_t<K>(a, form, ints, batch, groups, s)
+#define CALL(K) launch_vanilla_t<K>(a, form, mode, batch, groups, s)
   ZINC_LOGN_SWITCH(log_n, CALL)
 #undef CALL
 }

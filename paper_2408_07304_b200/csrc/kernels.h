@@ -138,9 +138,9 @@ cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, s
 bool fused_supported(int log_n, int L);
 cudaError_t launch_zinc_coeff_encode(int log_n, const ZincCoeffArgs &za, int gy, const EncodeArgs &ea, int enc_ctas,
                                      cudaStream_t s);
-cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, bool ints, size_t batch, int groups,
+cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                            cudaStream_t s);
-cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, bool ints, size_t batch, int groups, cudaStream_t s);
+cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s);
 cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);
 cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s);
 cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s);

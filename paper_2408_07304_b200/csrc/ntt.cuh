@@ -39,7 +39,8 @@ struct SmemWords { static constexpr int value = (1 << LOGN) + ((1 << LOGN) >> 4)
 // of the group (T == 1: contiguous words base .. base + 2^K - 1).
 // SMEM_TW: `tw` points to a shared-memory copy of the table (the early passes'
 // indices are all < kSmemTw).
-template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool SMEM_TW = false, class Load, class Store>
+template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool SMEM_TW = false, bool NR = false,
+          class Load, class Store>
 ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, Store store) {
   constexpr int N = 1 << LOGN;
   constexpr int G = 1 << K;
@@ -60,7 +61,10 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
       for (int blk = 0; blk < (1 << l); ++blk) {
         const Tw w = SMEM_TW ? tw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
-        for (int j = 0; j < D; ++j) ct_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
+        for (int j = 0; j < D; ++j) {
+          if constexpr (NR) ct_bfly_nr(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
+          else ct_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
+        }
       }
     }
     if constexpr (GROUPED) {
@@ -180,7 +184,8 @@ template <int LOGN> ZINC_DEV int local_off() {
 // kernels may stage them in shared memory (STW) and pass the copy as `stw`.
 constexpr int kSmemTw = 1024;
 
-template <int LOGN, bool STW = false, class Load, class GStore>
+// NR: lazy-free butterflies (q < 2^59; outputs < 2^64 instead of [0, 4q), reduce with reduce64).
+template <int LOGN, bool STW = false, bool NR = false, class Load, class GStore>
 ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GStore gstore, const Tw *stw = nullptr) {
   using G = Geo<LOGN>;
   using P = Plan<G::LOGL>;
@@ -192,26 +197,26 @@ ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GSt
   __syncthreads();  // the previous transform may still read sm
   static_assert(!STW || (!G::SPLIT && (1 << (SC)) <= kSmemTw), "smem twiddles cover passes A and B");
   if constexpr (!G::SPLIT) {
-    ct_pass<LL, 0, P::KA, P::THREADS, false, STW>(STW ? stw : tw, q, 1, load, sst);
+    ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, load, sst);
     __syncthreads();
-    ct_pass<LL, SB, P::KB, P::THREADS, false, STW>(STW ? stw : tw, q, 1, sld, sst);
+    ct_pass<LL, SB, P::KB, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, sld, sst);
     __syncthreads();
-    ct_pass<LL, SC, P::KC, P::THREADS, true>(tw, q, 1, sld, gstore);
+    ct_pass<LL, SC, P::KC, P::THREADS, true, false, NR>(tw, q, 1, sld, gstore);
   } else {
     const int r = (int)cluster_rank();
     const Tw w1 = ldtw(tw + 1);
     const uint64_t two_q = 2 * q;
     auto load0 = [&](int x) {
-      const uint64_t X = csub(load(x), two_q);
+      const uint64_t X = NR ? load(x) : csub(load(x), two_q);
       const uint64_t t = mul_shoup_lazy(load(x + G::NL), w1.x, w1.y, q);
       return r == 0 ? X + t : X - t + two_q;
     };
     const int tb = 2 + r;
-    ct_pass<LL, 0, P::KA, P::THREADS>(tw, q, tb, load0, sst);
+    ct_pass<LL, 0, P::KA, P::THREADS, false, false, NR>(tw, q, tb, load0, sst);
     __syncthreads();
-    ct_pass<LL, SB, P::KB, P::THREADS>(tw, q, tb, sld, sst);
+    ct_pass<LL, SB, P::KB, P::THREADS, false, false, NR>(tw, q, tb, sld, sst);
     __syncthreads();
-    ct_pass<LL, SC, P::KC, P::THREADS, true>(tw, q, tb, sld,
+    ct_pass<LL, SC, P::KC, P::THREADS, true, false, NR>(tw, q, tb, sld,
         [&](int base, uint64_t (&v)[16]) { gstore(base + r * G::NL, v); });
   }
 }
