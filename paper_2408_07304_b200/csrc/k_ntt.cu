@@ -9,7 +9,7 @@ namespace zinc {
 // MODE 0: CKKS, lazy-free butterflies (every q < 2^59); 1: CKKS with conditional
 // subtractions; 2: BFV / BGV terms (with subtractions).
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArgs a) {
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MINB) zinc_ntt_kernel(ZincNttArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) zinc_ntt_kernel(ZincNttArg
 // One CTA per limb: a <- U(R_qi) (tag PK_A, limb i), s <- R_2 (SK), e <- chi (PK_E);
 // pk2 = a^, sk = s^, pk1 = -a^ s^ + e^ (NTT domain; C-5).
 template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS) keygen_kernel(KeygenArgs a) {
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MINB) keygen_kernel(KeygenArgs a) {
   using G = Geo<LOGN>;
   constexpr int N = 1 << LOGN;
   constexpr int THREADS = G::THREADS;
@@ -111,13 +111,13 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) keygen_kernel(KeygenArgs a
 // same condition as CKKS's check).  BFV needs every residue: each limb's x^(i)
 // goes to a scratch [B][L][N] and bfv_scale_kernel forms round(t x / Q) mod t.
 template <int LOGN, int FORM>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs a) {
-  using G = Geo<LOGN>;
+__global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) decrypt_kernel(DecryptArgs a) {
+  using G = Geo<LOGN, 13>;
   constexpr int N = 1 << LOGN;
   extern __shared__ __align__(16) uint64_t sm[];
   __shared__ int bad_flag;
   const size_t b = blockIdx.x / G::CLUSTER;
-  const int loff = local_off<LOGN>();
+  const int loff = local_off<LOGN, 13>();
   const int L = a.L;
   int bad = 0;
   int64_t *x0 = a.coeff_out + b * N;
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs
       if (c.scheme == SCHEME_BGV && i == L - 1) x0[x] = (int64_t)mod_t(x0[x], c.t, c.t_mu);
     };
     if (FORM == 0) {
-      ntt_inverse<LOGN>(sm, itw, c,
+      ntt_inverse<LOGN, false, 13>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = add_mod(c1[base + r], mul_mod(c2[base + r], s[base + r], c), q);
@@ -170,12 +170,12 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) decrypt_kernel(DecryptArgs
           epilogue);
     } else {
       const Tw *tw = a.tw + (size_t)i * N;
-      ntt_forward<LOGN>(sm, tw, q, [&](int x) { return c2[x]; },
+      ntt_forward<LOGN, false, false, 13>(sm, tw, q, [&](int x) { return c2[x]; },
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon4(v[r], q, two_q), s[base + r], c);
           });
-      ntt_inverse<LOGN>(sm, itw, c,
+      ntt_inverse<LOGN, false, 13>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
@@ -223,22 +223,22 @@ __global__ void __launch_bounds__(256) bfv_scale_kernel(BfvScaleArgs a) {
 
 // ============================================================ standalone NTT
 template <int LOGN, int INV>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS) ntt_kernel(NttArgs a) {
+__global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) ntt_kernel(NttArgs a) {
   constexpr int N = 1 << LOGN;
   extern __shared__ __align__(16) uint64_t sm[];
-  const size_t poly = blockIdx.x / Geo<LOGN>::CLUSTER;
+  const size_t poly = blockIdx.x / Geo<LOGN, 13>::CLUSTER;
   const int i = (int)(poly % a.L);
   uint64_t *p = a.data + poly * N;
   const LimbConst c = a.limbs[i];
   const uint64_t q = c.q, two_q = c.two_q;
   if (INV == 0) {
-    ntt_forward<LOGN>(sm, a.tw + (size_t)i * N, q, [&](int x) { return p[x]; },
+    ntt_forward<LOGN, false, false, 13>(sm, a.tw + (size_t)i * N, q, [&](int x) { return p[x]; },
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
           for (int r = 0; r < 16; ++r) p[base + r] = canon4(v[r], q, two_q);
         });
   } else {
-    ntt_inverse<LOGN>(sm, a.itw + (size_t)i * N, c,
+    ntt_inverse<LOGN, false, 13>(sm, a.itw + (size_t)i * N, c,
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
           for (int r = 0; r < 16; ++r) v[r] = p[base + r];
@@ -276,10 +276,10 @@ cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s) {
 
 template <int LOGN>
 static cudaError_t launch_decrypt_t(const DecryptArgs &a, int form, size_t batch, cudaStream_t s) {
-  using G = Geo<LOGN>;
-  const size_t smem = ntt_smem_bytes<LOGN>();
-  if (form == 0) return launch_ex(decrypt_kernel<LOGN, 0>, msg_grid<LOGN>(batch), G::THREADS, smem, G::CLUSTER, s, a);
-  return launch_ex(decrypt_kernel<LOGN, 1>, msg_grid<LOGN>(batch), G::THREADS, smem, G::CLUSTER, s, a);
+  using G = Geo<LOGN, 13>;
+  const size_t smem = ntt_smem_bytes<LOGN, 13>();
+  if (form == 0) return launch_ex(decrypt_kernel<LOGN, 0>, msg_grid<LOGN, 13>(batch), G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(decrypt_kernel<LOGN, 1>, msg_grid<LOGN, 13>(batch), G::THREADS, smem, G::CLUSTER, s, a);
 }
 cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s) {
   const size_t n = a.batch * (size_t)a.n;
@@ -295,10 +295,10 @@ cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t bat
 
 template <int LOGN>
 static cudaError_t launch_ntt_t(const NttArgs &a, int inv, size_t polys, cudaStream_t s) {
-  using G = Geo<LOGN>;
-  const size_t smem = ntt_smem_bytes<LOGN>();
-  if (inv == 0) return launch_ex(ntt_kernel<LOGN, 0>, msg_grid<LOGN>(polys), G::THREADS, smem, G::CLUSTER, s, a);
-  return launch_ex(ntt_kernel<LOGN, 1>, msg_grid<LOGN>(polys), G::THREADS, smem, G::CLUSTER, s, a);
+  using G = Geo<LOGN, 13>;
+  const size_t smem = ntt_smem_bytes<LOGN, 13>();
+  if (inv == 0) return launch_ex(ntt_kernel<LOGN, 0>, msg_grid<LOGN, 13>(polys), G::THREADS, smem, G::CLUSTER, s, a);
+  return launch_ex(ntt_kernel<LOGN, 1>, msg_grid<LOGN, 13>(polys), G::THREADS, smem, G::CLUSTER, s, a);
 }
 cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s) {
 #define CALL(K) launch_ntt_t<K>(a, inv, polys, s)

@@ -14,10 +14,15 @@ namespace zinc {
 //              INTT(smem) + e1 + m -> ct0;  INTT(ct1) + e2 -> ct1.
 // 3 transforms per limb either way.
 // MODE as zinc_ntt_kernel: 0 CKKS lazy-free forward transforms (q < 2^59), 1 CKKS, 2 BFV / BGV.
+// COEFF form (1 forward + 2 inverse transforms per limb) runs N = 2^14 as 2-CTA clusters.
+template <int FORM> __host__ __device__ constexpr int vanilla_lm() { return FORM == 1 ? 13 : 14; }
+
 template <int LOGN, int FORM, int MODE>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs a) {
+__global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LOGN, vanilla_lm<FORM>()>::MINB)
+    vanilla_kernel(VanillaArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
-  using G = Geo<LOGN>;
+  constexpr int LM = vanilla_lm<FORM>();
+  using G = Geo<LOGN, LM>;
   constexpr int N = 1 << LOGN;
   constexpr int THREADS = G::THREADS;
   extern __shared__ __align__(16) uint64_t sm[];
@@ -28,7 +33,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
   __shared__ __align__(8) uint64_t tw_mbar[2];
   TwStager tws{&tw_mbar[0], 0}, itws{&tw_mbar[1], 0};
   const size_t b = blockIdx.x / G::CLUSTER;
-  const int loff = local_off<LOGN>();
+  const int loff = local_off<LOGN, LM>();
   const uint64_t msg = a.msg_base + b;
   const int L = a.L;
   const int lo = blockIdx.y * a.limbs_per_cta;
@@ -57,24 +62,24 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
     if constexpr (STW) tws.wait();
     auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
     if (FORM == 0) {
-      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
-                             to_smem<LOGN>(sm), stw);
+      ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
+                             to_smem<LOGN, LM>(sm), stw);
       __syncthreads();
-      stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+      stream_pairs<LOGN, 4, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         st2(ct0 + x, canon(v0), canon(v1));
       });
-      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
+      ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN, LM>(sm), stw);
       __syncthreads();
-      stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+      stream_pairs<LOGN, 4, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         st2(ct1 + x, canon(v0), canon(v1));
       });
-      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
+      ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN, LM>(sm),
                              stw);
       __syncthreads();
       if constexpr (STW) {
         if (i + 1 < hi) tws.issue(stw, tw + N);
       }
-      stream_pairs<LOGN, 2>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+      stream_pairs<LOGN, 2, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         const uint64_t u0 = canon(v0), u1 = canon(v1);
         const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
         uint64_t a0, a1, b0, b1;
@@ -84,14 +89,14 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
         st2_cs(ct1 + x, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
       });
     } else {
-      ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN>(sm),
+      ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN, LM>(sm),
                              stw);
       __syncthreads();
       if constexpr (STW) {
         if (i + 1 < hi) tws.issue(stw, tw + N);
         itws.wait();
       }
-      stream_pairs<LOGN, 2>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+      stream_pairs<LOGN, 2, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         const uint64_t u0 = canon(v0), u1 = canon(v1);
         const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
         st2(ct1 + x, mul_mod(p2.x, u0, c), mul_mod(p2.y, u1, c));  // temporary: pk2 u^
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
         sm[pad16(x - loff + 1)] = mul_mod(p1.y, u1, c);
       });
       const Tw *itw = a.itw + (size_t)i * N;
-      ntt_inverse<LOGN, STW>(sm, itw, c,
+      ntt_inverse<LOGN, STW, LM>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
@@ -109,8 +114,8 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
           }, sitw);
       __syncthreads();  // the inverse's last stores may still read sm (split exchange) -- and ct1 temp visibility
-      load_share<LOGN>(sm, ct1);
-      ntt_inverse<LOGN, STW>(sm, itw, c,
+      load_share<LOGN, 4, LM>(sm, ct1);
+      ntt_inverse<LOGN, STW, LM>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
@@ -126,14 +131,19 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS) vanilla_kernel(VanillaArgs
   }
 }
 
+template <int LOGN, int F>
+static size_t vanilla_smem() {
+  using G = Geo<LOGN, vanilla_lm<F>()>;
+  const size_t twb = G::SPLIT ? 0 : (size_t)(F == 0 ? 1 : 2) * kSmemTw * sizeof(Tw);
+  return ntt_smem_bytes<LOGN, vanilla_lm<F>()>() + (1 << LOGN) / 4 + 2 * (1 << LOGN) + twb;
+}
+
 template <int LOGN>
 static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                                     cudaStream_t s) {
-  using G = Geo<LOGN>;
-  const size_t twb = G::SPLIT ? 0 : (size_t)(form == 0 ? 1 : 2) * kSmemTw * sizeof(Tw);
-  const size_t smem = ntt_smem_bytes<LOGN>() + (1 << LOGN) / 4 + 2 * (1 << LOGN) + twb;
-  const dim3 grid = msg_grid<LOGN>(batch, groups);
-#define VK(F, M) launch_ex(vanilla_kernel<LOGN, F, M>, grid, G::THREADS, smem, G::CLUSTER, s, a)
+#define VK(F, M)                                                                                              \
+  launch_ex(vanilla_kernel<LOGN, F, M>, msg_grid<LOGN, vanilla_lm<F>()>(batch, groups),                      \
+            Geo<LOGN, vanilla_lm<F>()>::THREADS, vanilla_smem<LOGN, F>(), Geo<LOGN, vanilla_lm<F>()>::CLUSTER, s, a)
   if (mode == 2) return form == 0 ? VK(0, 2) : VK(1, 2);
   if (mode == 1) return form == 0 ? VK(0, 1) : VK(1, 1);
   return form == 0 ? VK(0, 0) : VK(1, 0);

@@ -66,20 +66,20 @@ ZINC_DEV ulonglong2 ld2_nc(const void *p) {
 // word pairs.  Decoupling the epilogue's global loads (cache, pk, ct) from the
 // butterflies lets U iterations of 16-byte loads be in flight per thread
 // instead of exposing one L2 round trip per 16-word group.
-template <int LOGN>
+template <int LOGN, int LM = 14>
 ZINC_DEV auto to_smem(uint64_t *sm) {
-  const int loff = local_off<LOGN>();
+  const int loff = local_off<LOGN, LM>();
   return [sm, loff](int base, uint64_t (&v)[16]) {
 #pragma unroll
     for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = v[r];
   };
 }
 // f(xg, v0, v1): words xg, xg + 1 (global, xg even) of this CTA's share.
-template <int LOGN, int U = 4, class F>
+template <int LOGN, int U = 4, int LM = 14, class F>
 ZINC_DEV void stream_pairs(const uint64_t *sm, F f) {
-  constexpr int NL = Geo<LOGN>::NL, THREADS = Geo<LOGN>::THREADS;
+  constexpr int NL = Geo<LOGN, LM>::NL, THREADS = Geo<LOGN, LM>::THREADS;
   static_assert(NL % (2 * THREADS * U) == 0, "epilogue tiling");
-  const int loff = local_off<LOGN>();
+  const int loff = local_off<LOGN, LM>();
 #pragma unroll 1
   for (int x0 = 2 * threadIdx.x; x0 < NL; x0 += 2 * THREADS * U) {
 #pragma unroll
@@ -90,10 +90,10 @@ ZINC_DEV void stream_pairs(const uint64_t *sm, F f) {
   }
 }
 // Coalesced prologue: the CTA's share of a global limb into the smem buffer.
-template <int LOGN, int U = 4>
+template <int LOGN, int U = 4, int LM = 14>
 ZINC_DEV void load_share(uint64_t *sm, const uint64_t *src) {
-  constexpr int NL = Geo<LOGN>::NL, THREADS = Geo<LOGN>::THREADS;
-  const int loff = local_off<LOGN>();
+  constexpr int NL = Geo<LOGN, LM>::NL, THREADS = Geo<LOGN, LM>::THREADS;
+  const int loff = local_off<LOGN, LM>();
 #pragma unroll 1
   for (int x0 = 2 * threadIdx.x; x0 < NL; x0 += 2 * THREADS * U) {
     ulonglong2 v[U];
@@ -184,9 +184,11 @@ inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, int threads, s
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <int LOGN> static size_t ntt_smem_bytes() { return SmemWords<Geo<LOGN>::LOGL>::value * sizeof(uint64_t); }
-template <int LOGN> static dim3 msg_grid(size_t count, int groups = 1) {
-  return dim3((unsigned)(count * Geo<LOGN>::CLUSTER), groups);
+template <int LOGN, int LM = 14> static size_t ntt_smem_bytes() {
+  return SmemWords<Geo<LOGN, LM>::LOGL>::value * sizeof(uint64_t);
+}
+template <int LOGN, int LM = 14> static dim3 msg_grid(size_t count, int groups = 1) {
+  return dim3((unsigned)(count * Geo<LOGN, LM>::CLUSTER), groups);
 }
 
 #define ZINC_LOGN_SWITCH(log_n, CALL) \

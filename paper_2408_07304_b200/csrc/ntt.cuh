@@ -148,12 +148,17 @@ template <> struct Plan<14> { static constexpr int THREADS = 512, KA = 5, KB = 5
 // stages LOGN-1 .. 1 on its half, then stage 0 (with N^-1 folded in) exchanges
 // halves through distributed shared memory: CTA r finishes j in
 // [r N/4, (r+1) N/4) from both CTAs' buffers.
-template <int LOGN> struct Geo {
-  static constexpr bool SPLIT = LOGN > 14;
+// LM: the largest log2 N one CTA transforms alone (14 fits 128 KiB + padding in one
+// CTA's shared memory).  A kernel may choose LM = 13 at N = 2^14: two CTAs of 68 KiB per
+// limb, two clusters per SM, so one CTA's barriers and memory phases overlap the
+// other's butterflies (measured faster for the INTT-heavy kernels).
+template <int LOGN, int LM = 14> struct Geo {
+  static constexpr bool SPLIT = LOGN > LM;
   static constexpr int LOGL = SPLIT ? LOGN - 1 : LOGN;  // words per CTA = 2^LOGL
   static constexpr int NL = 1 << LOGL;
   static constexpr int CLUSTER = SPLIT ? 2 : 1;
   static constexpr int THREADS = Plan<LOGL>::THREADS;
+  static constexpr int MINB = (SPLIT && LOGL <= 13) ? 2 : 1;  // CTAs per SM the kernels aim for
 };
 
 ZINC_DEV uint32_t cluster_rank() {
@@ -172,8 +177,8 @@ ZINC_DEV T *peer_smem(T *p, uint32_t rank) {
   return reinterpret_cast<T *>(out);
 }
 // Index offset of this CTA's share of a limb (0 unless split).
-template <int LOGN> ZINC_DEV int local_off() {
-  if constexpr (Geo<LOGN>::SPLIT) return (int)cluster_rank() * Geo<LOGN>::NL;
+template <int LOGN, int LM = 14> ZINC_DEV int local_off() {
+  if constexpr (Geo<LOGN, LM>::SPLIT) return (int)cluster_rank() * Geo<LOGN, LM>::NL;
   else return 0;
 }
 
@@ -185,9 +190,9 @@ template <int LOGN> ZINC_DEV int local_off() {
 constexpr int kSmemTw = 1024;
 
 // NR: lazy-free butterflies (q < 2^59; outputs < 2^64 instead of [0, 4q), reduce with reduce64).
-template <int LOGN, bool STW = false, bool NR = false, class Load, class GStore>
+template <int LOGN, bool STW = false, bool NR = false, int LM = 14, class Load, class GStore>
 ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GStore gstore, const Tw *stw = nullptr) {
-  using G = Geo<LOGN>;
+  using G = Geo<LOGN, LM>;
   using P = Plan<G::LOGL>;
   constexpr int LL = G::LOGL;
   constexpr int SB = P::KA, SC = P::KA + P::KB;
@@ -226,10 +231,10 @@ ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GSt
 // outputs in [0, 2q) at global indices, lane-consecutive (coalesced).  When
 // split, every store happens after both CTAs of the pair consumed their inputs
 // (in-place use is safe).
-template <int LOGN, bool STW = false, class GLoad, class Store>
+template <int LOGN, bool STW = false, int LM = 14, class GLoad, class Store>
 ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad gload, Store store,
                           const Tw *sitw = nullptr) {
-  using G = Geo<LOGN>;
+  using G = Geo<LOGN, LM>;
   using P = Plan<G::LOGL>;
   constexpr int LL = G::LOGL;
   constexpr int SB = P::KA, SC = P::KA + P::KB;
