@@ -158,7 +158,9 @@ template <int LOGN, int LM = 14> struct Geo {
   static constexpr int NL = 1 << LOGL;
   static constexpr int CLUSTER = SPLIT ? 2 : 1;
   static constexpr int THREADS = Plan<LOGL>::THREADS;
-  static constexpr int MINB = (SPLIT && LOGL <= 13) ? 2 : 1;  // CTAs per SM the kernels aim for
+  // CTAs per SM the kernels aim for (caps registers so they fit beside shared memory):
+  // 2^12-word shares (~34 KiB) three, 2^13 (~68 KiB) two, 2^14 (~136 KiB) one.
+  static constexpr int MINB = LOGL <= 12 ? 3 : LOGL == 13 ? 2 : 1;
 };
 
 ZINC_DEV uint32_t cluster_rank() {
