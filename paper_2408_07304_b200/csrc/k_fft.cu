@@ -19,16 +19,31 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   extern __shared__ __align__(16) double2 buf[];
   const size_t b = blockIdx.x / (SPLIT ? 2 : 1);
   const int r = SPLIT ? (int)cluster_rank() : 0;
-  for (int k = threadIdx.x; k < M; k += P::THREADS) {
-    const int pos = a.perm[k] - r * ML;
-    if (SPLIT && (unsigned)pos >= (unsigned)ML) continue;
-    double2 z;
-    if (a.complex_slots) {
-      z = reinterpret_cast<const double2 *>(a.slots)[b * M + k];
-    } else {
-      z = make_double2(a.slots[b * M + k], 0.0);
+  // Slot k lands at bit-reversed position brv(h_k), h_k = (5^k mod 2N - 1) / 4.  h_k's lowest
+  // bit is k's parity (5^k = 1 or 5 mod 8), so half r of the split takes exactly the slots
+  // k = 2i + r.  The order g = 5^k mod 2N is generated in registers (2N = 4M is a power of
+  // two) and U independent slot loads are kept in flight per thread.
+  constexpr int KS = SPLIT ? 2 : 1, CNT = M / KS, U = 8;
+  static_assert(CNT % (P::THREADS * U) == 0, "scatter tiling");
+  constexpr uint32_t MASK = 4u * M - 1u;
+  const uint32_t gstep = pow5_mod_pow2((uint32_t)(KS * P::THREADS), MASK);
+  uint32_t g = pow5_mod_pow2((uint32_t)(KS * threadIdx.x + r), MASK);
+#pragma unroll 1
+  for (int i0 = threadIdx.x; i0 < CNT; i0 += P::THREADS * U) {
+    double2 zv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const size_t k = (size_t)KS * (i0 + u * P::THREADS) + r;
+      zv[u] = a.complex_slots ? __ldcs(reinterpret_cast<const double2 *>(a.slots) + b * M + k)
+                              : make_double2(__ldcs(a.slots + b * M + k), 0.0);
     }
-    buf[pad16(pos)] = z;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t h = g >> 2;
+      const int pos = (int)(__brev(h) >> (32 - LOGM)) - r * ML;
+      buf[pad16(pos)] = zv[u];
+      g = (g * gstep) & MASK;
+    }
   }
   __syncthreads();
   auto lds = [&](int i) { return buf[pad16(i)]; };
