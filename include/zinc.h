@@ -261,9 +261,11 @@ void zinc_launch_count_reset(void);
  *  ZINC_TUNE_COEFF_SMEM_PAD       extra bytes of dynamic shared memory requested by the COEFF-form
  *                                 Zinc kernel (limits how many of its CTAs share an SM with the
  *                                 overlapped encode; default 0)
+ *  ZINC_TUNE_PDL                  1 (default): the serial encode -> Zinc chunk pipeline chains its
+ *                                 launches with programmatic dependent launch; 0: plain stream order
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_OVERLAP = 2,
-       ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_COUNT = 4 };
+       ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_PDL = 4, ZINC_TUNE_COUNT = 5 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

@@ -99,7 +99,7 @@ struct TraceScope {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -635,10 +635,22 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
     return st;
   }
   if (!overlap) {
-    for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
+    // serial chunks, double-buffered scratch, chained with programmatic dependent launches
+    // (knob ZINC_TUNE_PDL): each kernel's prologue overlaps the previous kernel's tail
+    const bool pdl = g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 && path == PATH_ZINC &&
+                     form == ZINC_FORM_COEFF;
+    PdlScope pdl_scope(pdl);
+    const int nb = pdl && batch > chunk ? 2 : 1;
+    if (nb == 2 && nbuf == 1) {
+      cudaFreeAsync(m, s);
+      CUDA_TRY(cudaMallocAsync((void **)&m, 2 * chunk * per_msg, s));
+    }
+    size_t k = 0;
+    for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
       const size_t cnt = std::min(chunk, batch - off);
-      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m, s);
-      if (st == ZINC_OK) st = run_path(c, path, key, form, m, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
+      int64_t *mb = m + (size_t)(k % nb) * chunk * c->n;
+      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
+      if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
     }
     cudaFreeAsync(m, s);
     return st;

@@ -73,6 +73,10 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   __syncthreads();
   fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, true>(stw, lds, sts);
   __syncthreads();
+  // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
+  // this encode overwrites: the loads and the FFT above overlapped it, the stores wait.
+  pdl_trigger();
+  pdl_wait();
   int64_t *m = a.m_out + b * (2 * M) * (WIDE ? 2 : 1);
   const double scale = a.scale;  // Delta / M
   constexpr int V = 4;  // independent post-processing iterations per batch

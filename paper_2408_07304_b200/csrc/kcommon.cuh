@@ -160,6 +160,11 @@ inline cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// Programmatic dependent launch (PdlScope in kernels.h): kernels trigger their dependents
+// early and wait for their prerequisite grid before touching its outputs.
+ZINC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+ZINC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Launch with an optional thread-block cluster along x (2 for the N = 2^15 split).
 template <class... KArgs, class... Args>
 inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, int threads, size_t smem, int cluster,
@@ -171,15 +176,22 @@ inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, int threads, s
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (cluster > 1) {
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cluster;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = cluster;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (g_launch_pdl) {  // programmatic dependent launch (see PdlScope)
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   e = cudaLaunchKernelEx(&cfg, kernel, args...);
   return e != cudaSuccess ? e : cudaGetLastError();
 }

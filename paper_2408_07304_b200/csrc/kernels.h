@@ -12,6 +12,17 @@ namespace zinc {
 
 using Tw = ulonglong2;  // {w, floor(w 2^64 / q)}
 
+// Programmatic dependent launch for the launches made while a PdlScope is alive on this
+// thread: the next kernel in the stream may start once every CTA of the previous one has
+// started (griddepcontrol.launch_dependents) and must griddepcontrol.wait before touching
+// the previous kernel's outputs.  Used by the encode -> Zinc chunk pipeline.
+inline thread_local bool g_launch_pdl = false;
+struct PdlScope {
+  bool old;
+  explicit PdlScope(bool on) : old(g_launch_pdl) { g_launch_pdl = on; }
+  ~PdlScope() { g_launch_pdl = old; }
+};
+
 struct ZincCoeffArgs {
   const LimbConst *limbs;
   const uint64_t *cache;  // [2][L][N]

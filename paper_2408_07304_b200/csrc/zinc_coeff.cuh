@@ -68,6 +68,10 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   size_t b_end = b_begin + a.msgs_per_cta;
   if (b_end > a.batch) b_end = a.batch;
   const size_t lnn = (size_t)L * a.n;
+  // under a programmatic dependent launch the encode kernel that wrote m may still be
+  // running: everything above overlaps it; m is read only after its grid completed
+  pdl_trigger();
+  pdl_wait();
   // first message's plaintext words, fetched while the tile is in flight
   ulonglong2 mv = make_ulonglong2(0, 0);
   if (a.m && b_begin < b_end) mv = ld2_nc(a.m + b_begin * a.n + j);

@@ -58,20 +58,22 @@ def main():
               flush=True)
 
     rep("encode", timeit(lambda: Z.ckks_encode_batch(ctx, slots, out=m)), in_bytes + cfg.n * 8)
-    for pad in [int(x) for x in args.pads_kb.split(",")]:
-        Z.tune(Z.TUNE_COEFF_SMEM_PAD, pad << 10)
-        for mpc in [int(x) for x in args.mpc.split(",")]:
-            Z.tune(Z.TUNE_COEFF_MSGS_PER_CTA, mpc)
-            rep("zinc_i64", timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, m, 1, 0, out=ct)),
-                ct_bytes + cfg.n * 8, mpc=mpc, pad_kb=pad)
-        for ov in (0, 1, 2):
-            Z.tune(Z.TUNE_OVERLAP, ov)
-            for mb in [int(x) for x in args.chunks_mb.split(",")]:
-                Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, mb << 20)
-                for mpc in [int(x) for x in args.mpc.split(",")]:
-                    Z.tune(Z.TUNE_COEFF_MSGS_PER_CTA, mpc)
-                    rep("zinc_slots", timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, slots, 1, 0, out=ct)),
-                        ct_bytes + in_bytes, mpc=mpc, overlap=ov, chunk_mb=mb, pad_kb=pad)
+    for pdl in (1, 0):
+      Z.tune(Z.TUNE_PDL, pdl)
+      for pad in [int(x) for x in args.pads_kb.split(",")]:
+          Z.tune(Z.TUNE_COEFF_SMEM_PAD, pad << 10)
+          for mpc in [int(x) for x in args.mpc.split(",")]:
+              Z.tune(Z.TUNE_COEFF_MSGS_PER_CTA, mpc)
+              rep("zinc_i64", timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, m, 1, 0, out=ct)),
+                  ct_bytes + cfg.n * 8, mpc=mpc, pad_kb=pad, pdl=pdl)
+          for ov in (0, 1, 2):
+              Z.tune(Z.TUNE_OVERLAP, ov)
+              for mb in [int(x) for x in args.chunks_mb.split(",")]:
+                  Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, mb << 20)
+                  for mpc in [int(x) for x in args.mpc.split(",")]:
+                      Z.tune(Z.TUNE_COEFF_MSGS_PER_CTA, mpc)
+                      rep("zinc_slots", timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, slots, 1, 0, out=ct)),
+                          ct_bytes + in_bytes, mpc=mpc, overlap=ov, chunk_mb=mb, pad_kb=pad, pdl=pdl)
     Z.tune(Z.TUNE_COEFF_SMEM_PAD, 0)
     # correctness spot check against the serial path
     Z.tune(Z.TUNE_OVERLAP, 0)
