@@ -5,32 +5,48 @@ namespace zinc {
 
 // ============================================================ Zinc, NTT form
 // c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2') (two DFTs,
-// no multiplication).
+// no multiplication).  N <= 2^13: one CTA per (message, limb group).  N >= 2^14: a 2-CTA
+// cluster per message splits every transform by input parity (ntt_forward_dit2), each
+// CTA holding half a limb (68 KiB at 2^14: two clusters per SM) and only its parity's
+// samples; the transform's last stage streams the ciphertext pairs straight to HBM.
+template <int LOGN> struct ZincNttGeo {
+  static constexpr bool DIT = LOGN >= 14;
+  static constexpr int LOGL = DIT ? LOGN - 1 : LOGN, NL = 1 << LOGL;
+  static constexpr int THREADS = Plan<LOGL>::THREADS, CLUSTER = DIT ? 2 : 1;
+  static constexpr int MINB = LOGL <= 12 ? 3 : LOGL == 13 ? 2 : 1;
+  static constexpr size_t SMEM = SmemWords<LOGL>::value * sizeof(uint64_t) + 2 * NL + kSmemTw * sizeof(Tw);
+};
+
 // MODE 0: CKKS, lazy-free butterflies (every q < 2^59); 1: CKKS with conditional
 // subtractions; 2: BFV / BGV terms (with subtractions).
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MINB) zinc_ntt_kernel(ZincNttArgs a) {
+__global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::MINB) zinc_ntt_kernel(ZincNttArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
-  using G = Geo<LOGN>;
+  using G = ZincNttGeo<LOGN>;
   constexpr int N = 1 << LOGN;
   constexpr int THREADS = G::THREADS;
-  constexpr bool STW = !G::SPLIT;  // passes A and B read a shared-memory copy of W[0, kSmemTw)
   extern __shared__ __align__(16) uint64_t sm[];
-  int8_t *se1 = reinterpret_cast<int8_t *>(sm + SmemWords<G::LOGL>::value);
-  int8_t *se2 = se1 + N;
-  Tw *stw = reinterpret_cast<Tw *>(se2 + N);
+  int8_t *se1 = reinterpret_cast<int8_t *>(sm + SmemWords<G::LOGL>::value);  // [NL]: this CTA's samples
+  int8_t *se2 = se1 + G::NL;
+  Tw *stw = reinterpret_cast<Tw *>(se2 + G::NL);
   __shared__ __align__(8) uint64_t tw_mbar;
   TwStager tws{&tw_mbar, 0};
   const size_t b = blockIdx.x / G::CLUSTER;
+  const int r = G::DIT ? (int)cluster_rank() : 0;
   const uint64_t msg = a.msg_base + b;
   const int L = a.L;
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
-  if constexpr (STW) tws.init();
+  tws.init();
   __syncthreads();
-  if constexpr (STW) tws.issue(stw, a.tw + (size_t)lo * N);
-  sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ZINC_E1);
-  sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2);
+  tws.issue(stw, a.tw + (size_t)lo * N);
+  if constexpr (G::DIT) {
+    sample_cbd_parity<THREADS>(se1, N, a.seed, msg, TAG_ZINC_E1, r);
+    sample_cbd_parity<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2, r);
+  } else {
+    sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ZINC_E1);
+    sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2);
+  }
   __syncthreads();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
@@ -40,24 +56,34 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MINB) zinc_ntt_
     const uint64_t *z1 = a.cache + (size_t)i * N, *z2 = a.cache + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    if constexpr (STW) tws.wait();
     auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
-    ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
-                               to_smem<LOGN>(sm), stw);
-    __syncthreads();
-    stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+    auto out0 = [&](int x, uint64_t v0, uint64_t v1) {
       const ulonglong2 z = ld2_nc(z1 + x);
       st2_cs(ct0 + x, add_mod(z.x, canon(v0), q), add_mod(z.y, canon(v1), q));
-    });
-    ntt_forward<LOGN, STW, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
-    __syncthreads();
-    if constexpr (STW) {
-      if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
-    }
-    stream_pairs<LOGN>(sm, [&](int x, uint64_t v0, uint64_t v1) {
+    };
+    auto out1 = [&](int x, uint64_t v0, uint64_t v1) {
       const ulonglong2 z = ld2_nc(z2 + x);
       st2_cs(ct1 + x, add_mod(z.x, canon(v0), q), add_mod(z.y, canon(v1), q));
-    });
+    };
+    tws.wait();
+    if constexpr (G::DIT) {
+      // sample of coefficient x = 2 i' + r sits at i' = x >> 1
+      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x >> 1], c); },
+                                      out0, stw);
+      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); }, out1, stw,
+                                      [&]() {
+                                        if (i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
+                                      });
+    } else {
+      ntt_forward<LOGN, true, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
+                                  to_smem<LOGN>(sm), stw);
+      __syncthreads();
+      stream_pairs<LOGN>(sm, out0);
+      ntt_forward<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
+      __syncthreads();
+      if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
+      stream_pairs<LOGN>(sm, out1);
+    }
   }
 }
 
@@ -249,12 +275,11 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) n
 
 template <int LOGN>
 static cudaError_t launch_zinc_ntt_t(const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
-  using G = Geo<LOGN>;
-  const size_t smem = ntt_smem_bytes<LOGN>() + 2 * (1 << LOGN) + (G::SPLIT ? 0 : kSmemTw * sizeof(Tw));
-  const dim3 grid = msg_grid<LOGN>(batch, groups);
-  if (mode == 2) return launch_ex(zinc_ntt_kernel<LOGN, 2>, grid, G::THREADS, smem, G::CLUSTER, s, a);
-  if (mode == 1) return launch_ex(zinc_ntt_kernel<LOGN, 1>, grid, G::THREADS, smem, G::CLUSTER, s, a);
-  return launch_ex(zinc_ntt_kernel<LOGN, 0>, grid, G::THREADS, smem, G::CLUSTER, s, a);
+  using G = ZincNttGeo<LOGN>;
+  const dim3 grid((unsigned)(batch * G::CLUSTER), groups);
+  if (mode == 2) return launch_ex(zinc_ntt_kernel<LOGN, 2>, grid, G::THREADS, G::SMEM, G::CLUSTER, s, a);
+  if (mode == 1) return launch_ex(zinc_ntt_kernel<LOGN, 1>, grid, G::THREADS, G::SMEM, G::CLUSTER, s, a);
+  return launch_ex(zinc_ntt_kernel<LOGN, 0>, grid, G::THREADS, G::SMEM, G::CLUSTER, s, a);
 }
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
 #define CALL(K) launch_zinc_ntt_t<K>(a, mode, batch, groups, s)

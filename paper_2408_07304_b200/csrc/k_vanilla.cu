@@ -131,6 +131,71 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
   }
 }
 
+// NTT form at N >= 2^14: a 2-CTA cluster per message splits each of the three transforms by
+// input parity (ntt_forward_dit2, as zinc_ntt_kernel): 68 KiB halves, two clusters per SM at
+// 2^14, only this parity's samples, early-pass twiddles in shared memory, and the last stage
+// streams straight into the ciphertext.
+template <int LOGN> struct VanillaDitGeo {
+  static constexpr int LOGL = LOGN - 1, NL = 1 << LOGL;
+  static constexpr int THREADS = Plan<LOGL>::THREADS, MINB = LOGL == 13 ? 2 : 1;
+  static constexpr size_t SMEM = SmemWords<LOGL>::value * sizeof(uint64_t) + NL / 4 + 2 * NL + kSmemTw * sizeof(Tw);
+};
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LOGN>::MINB)
+    vanilla_ntt_dit_kernel(VanillaArgs a) {
+  constexpr bool INTS = MODE == 2, NR = MODE == 0;
+  using G = VanillaDitGeo<LOGN>;
+  constexpr int N = 1 << LOGN, THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  uint8_t *su = reinterpret_cast<uint8_t *>(sm + SmemWords<G::LOGL>::value);  // this parity's samples
+  int8_t *se1 = reinterpret_cast<int8_t *>(su + G::NL / 4), *se2 = se1 + G::NL;
+  Tw *stw = reinterpret_cast<Tw *>(se2 + G::NL);
+  __shared__ __align__(8) uint64_t tw_mbar;
+  TwStager tws{&tw_mbar, 0};
+  const size_t b = blockIdx.x / 2;
+  const int r = (int)cluster_rank();
+  const uint64_t msg = a.msg_base + b;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  tws.init();
+  __syncthreads();
+  tws.issue(stw, a.tw + (size_t)lo * N);
+  sample_ternary_parity<THREADS>(su, N, a.seed, msg, TAG_ENC_U, r);
+  sample_cbd_parity<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1, r);
+  sample_cbd_parity<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2, r);
+  __syncthreads();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
+    tws.wait();
+    // sample of coefficient x = 2 i' + r sits at i' = x >> 1
+    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x >> 1], c); },
+                                     [&](int x, uint64_t v0, uint64_t v1) { st2(ct0 + x, canon(v0), canon(v1)); }, stw);
+    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); },
+                                     [&](int x, uint64_t v0, uint64_t v1) { st2(ct1 + x, canon(v0), canon(v1)); }, stw);
+    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> 1), q); },
+        [&](int x, uint64_t v0, uint64_t v1) {
+          const uint64_t u0 = canon(v0), u1 = canon(v1);
+          const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
+          uint64_t a0, a1, b0, b1;
+          ld2(ct0 + x, a0, a1);
+          ld2(ct1 + x, b0, b1);
+          st2_cs(ct0 + x, add_mod(a0, mul_mod(p1.x, u0, c), q), add_mod(a1, mul_mod(p1.y, u1, c), q));
+          st2_cs(ct1 + x, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
+        },
+        stw, [&]() {
+          if (i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
+        });
+  }
+}
+
 template <int LOGN, int F>
 static size_t vanilla_smem() {
   using G = Geo<LOGN, vanilla_lm<F>()>;
@@ -144,6 +209,15 @@ static cudaError_t launch_vanilla_t(const VanillaArgs &a, int form, int mode, si
 #define VK(F, M)                                                                                              \
   launch_ex(vanilla_kernel<LOGN, F, M>, msg_grid<LOGN, vanilla_lm<F>()>(batch, groups),                      \
             Geo<LOGN, vanilla_lm<F>()>::THREADS, vanilla_smem<LOGN, F>(), Geo<LOGN, vanilla_lm<F>()>::CLUSTER, s, a)
+  if constexpr (LOGN >= 14) {
+    if (form == 0) {
+      using D = VanillaDitGeo<LOGN>;
+      const dim3 grid((unsigned)(batch * 2), groups);
+#define VD(M) launch_ex(vanilla_ntt_dit_kernel<LOGN, M>, grid, D::THREADS, D::SMEM, 2, s, a)
+      return mode == 2 ? VD(2) : mode == 1 ? VD(1) : VD(0);
+#undef VD
+    }
+  }
   if (mode == 2) return form == 0 ? VK(0, 2) : VK(1, 2);
   if (mode == 1) return form == 0 ? VK(0, 1) : VK(1, 1);
   return form == 0 ? VK(0, 0) : VK(1, 0);

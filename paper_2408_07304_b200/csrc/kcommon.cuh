@@ -34,6 +34,29 @@ ZINC_DEV void sample_ternary_packed(uint8_t *dst, int n, uint64_t seed, uint64_t
   }
 }
 ZINC_DEV int tern_at(const uint8_t *p, int x) { return (int)((p[x >> 2] >> ((x & 3) * 2)) & 3u) - 1; }
+// Parity-split samplers (the even/odd cluster transform): coefficients 2i + r only, stored at i.
+template <int THREADS>
+ZINC_DEV void sample_cbd_parity(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag, int r) {
+  for (int blk = threadIdx.x; blk < n / 2; blk += THREADS) {
+    const uint4 w = stream_block(seed, msg, tag, 0, blk);  // coefficients 2 blk, 2 blk + 1
+    dst[blk] = (int8_t)(r ? cbd_hi(w) : cbd_lo(w));
+  }
+}
+template <int THREADS>
+ZINC_DEV void sample_ternary_parity(uint8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag, int r) {
+  // block b: coefficients 4b..4b+3; parity r keeps 4b + r (local 2b) and 4b + 2 + r (local 2b + 1)
+  for (int blk2 = threadIdx.x; blk2 < n / 8; blk2 += THREADS) {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint4 w = stream_block(seed, msg, tag, 0, 2 * blk2 + h);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      packed |= (uint32_t)(tern(ws[r]) + 1) << (4 * h);
+      packed |= (uint32_t)(tern(ws[2 + r]) + 1) << (4 * h + 2);
+    }
+    dst[blk2] = (uint8_t)packed;
+  }
+}
 template <int THREADS>
 ZINC_DEV void sample_cbd_smem(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
   for (int blk = threadIdx.x; blk < n / 2; blk += THREADS) {

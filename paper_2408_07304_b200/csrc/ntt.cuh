@@ -228,6 +228,70 @@ ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GSt
   }
 }
 
+// Forward NTT of one limb by a 2-CTA cluster, split by input parity (no redundant work):
+// a(X) = a_e(X^2) + X a_o(X^2), and with k = 2k' + b, C-3's order gives
+//   a^[2k' + b] = E[k'] + (-1)^b psi^(2 brv'(k') + 1) O[k'],
+// where E, O are the N/2-point transforms of a_e, a_o with root psi^2 in the same order.
+// The N/2-point table with root psi^2 is the first half of the N-point table
+// (brv_N(i) = 2 brv_{N/2}(i) for i < N/2) and psi^(2 brv'(k') + 1) = W[N/2 + k'], so CTA r
+// runs the ordinary passes on inputs x = 2i + r, then the last stage exchanges halves over
+// distributed shared memory: CTA r finishes k' in [r N/4, (r+1) N/4) and hands the output
+// pair (2k', 2k'+1) -- global positions, values as the one-CTA transform's -- to
+// `pair(x, v0, v1)`.  The pair function must not write shared memory (the partner may
+// still be reading it); callers stream to global memory.
+struct NoHook {
+  ZINC_DEV void operator()() const {}
+};
+// after_b(): called by every thread once all threads are past pass B (the last use of stw).
+template <int LOGN, bool STW = false, bool NR = false, class Load, class Pair, class AfterB = NoHook>
+ZINC_DEV void ntt_forward_dit2(uint64_t *sm, const Tw *tw, uint64_t q, Load load, Pair pair,
+                               const Tw *stw = nullptr, AfterB after_b = AfterB()) {
+  constexpr int LL = LOGN - 1, NL = 1 << LL, QN = NL / 2;
+  using P = Plan<LL>;
+  constexpr int SB = P::KA, SC = P::KA + P::KB;
+  static_assert(SC + P::KC == LL && P::KC == 4, "plan");
+  static_assert(!STW || (1 << SC) <= kSmemTw, "smem twiddles cover passes A and B");
+  auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
+  auto sld = [&](int i) { return sm[pad16(i)]; };
+  const int r = (int)cluster_rank();
+  __syncthreads();
+  ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, [&](int i) { return load(2 * i + r); },
+                                                     sst);
+  __syncthreads();
+  ct_pass<LL, SB, P::KB, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, sld, sst);
+  __syncthreads();
+  after_b();
+  ct_pass<LL, SC, P::KC, P::THREADS, true, false, NR>(tw, q, 1, sld, [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sm[pad16(base + j)] = v[j];
+  });
+  cluster_sync_all();  // both halves transformed
+  const uint64_t *he = peer_smem(sm, 0), *ho = peer_smem(sm, 1);
+  const uint64_t two_q = 2 * q;
+  constexpr int U = 4;
+  static_assert(QN % (P::THREADS * U) == 0, "exchange tiling");
+#pragma unroll 1
+  for (int k0 = r * QN + threadIdx.x; k0 < (r + 1) * QN; k0 += P::THREADS * U) {
+    uint64_t e[U], o[U];
+    Tw w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * P::THREADS;
+      e[u] = he[pad16(k)];
+      o[u] = ho[pad16(k)];
+      w[u] = ldtw(tw + NL + k);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * P::THREADS;
+      const uint64_t E = NR ? e[u] : csub(e[u], two_q);
+      const uint64_t t = mul_shoup_lazy(o[u], w[u].x, w[u].y, q);
+      pair(2 * k, E + t, E - t + two_q);
+    }
+  }
+  cluster_sync_all();  // the partner finished reading this CTA's half
+}
+
 // Inverse NTT: `gload(base, v[16])` supplies each group of 16 contiguous inputs
 // in [0, 2q) (global position base); `store(idx, v)` gets the natural-order
 // outputs in [0, 2q) at global indices, lane-consecutive (coalesced).  When
