@@ -337,6 +337,34 @@ def paper_params(Z, torch, reps=2, cap=4096):
     return out
 
 
+def schemes(Z, torch, reps=2, B=4096, t=65537):
+    """BFV (Eq. 12) and BGV (Eq. 13) at C3's ring and modulus, Zinc (COEFF and
+    NTT form) and vanilla (NTT form) from int64 plaintexts mod t, with a decryption check."""
+    cfg = CONFIGS["C3"]
+    out = {"workload": "C3 ring, t = %d" % t, "batch": B}
+    for name, scheme in (("BFV", 1), ("BGV", 2)):
+        ctx = Z.Context(cfg.log_n, cfg.bits, 0, scheme=scheme, t=t)
+        sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
+        cache = {f: Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, f) for f in (Z.COEFF, Z.NTT)}
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        m = torch.randint(0, t, (B, cfg.n), dtype=torch.int64, device="cuda", generator=gen)
+        ct = ctx.empty_ct(B)
+        r = {}
+        for pname, fn in (
+                ("zinc_coeff", lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, m, cfg.enc_seed, 0, out=ct)),
+                ("zinc_ntt", lambda: Z.zinc_encrypt_batch(ctx, cache[Z.NTT], Z.NTT, m, cfg.enc_seed, 0, out=ct)),
+                ("vanilla_ntt", lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, m, cfg.enc_seed, 0, out=ct))):
+            ms = _timed(torch, fn, reps)
+            r[pname] = {"ms": ms, "ct_per_s": B / (ms / 1e3)}
+        coeff, st, _ = Z.ckks_decrypt_batch(ctx, sk, Z.NTT, ct[:64])
+        r["decrypt_ok"] = bool(torch.equal(coeff, m[:64])) and int(st.sum().item()) == 0
+        out[name] = r
+        del ct, m
+        ctx.close()
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -571,6 +599,7 @@ def main():
             torch.cuda.empty_cache()
         result["other_configs"] = other_configs(Z, torch)
         result["paper_params"] = paper_params(Z, torch)
+        result["schemes"] = schemes(Z, torch)
 
     # ---------------- end to end through the host-buffer API
     if not args.no_e2e:
