@@ -639,7 +639,6 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
     // (knob ZINC_TUNE_PDL): each kernel's prologue overlaps the previous kernel's tail
     const bool pdl = g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 && path == PATH_ZINC &&
                      form == ZINC_FORM_COEFF;
-    PdlScope pdl_scope(pdl);
     const int nb = pdl && batch > chunk ? 2 : 1;
     if (nb == 2 && nbuf == 1) {
       cudaFreeAsync(m, s);
@@ -649,7 +648,13 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
     for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
       const size_t cnt = std::min(chunk, batch - off);
       int64_t *mb = m + (size_t)(k % nb) * chunk * c->n;
-      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
+      {
+        // the first launch keeps a full dependency on whatever produced the inputs (its
+        // loads precede its griddepcontrol.wait); later ones chain on this pipeline's kernels
+        PdlScope pdl_scope(pdl && k > 0);
+        st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
+      }
+      PdlScope pdl_scope(pdl);
       if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
     }
     cudaFreeAsync(m, s);
