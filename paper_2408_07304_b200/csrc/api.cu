@@ -552,19 +552,29 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
 static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int form, int kind, const void *pt,
                                 size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s) {
   const bool slots = kind != ZINC_PT_COEFF_I128;
+  const bool direct = path == PATH_ZINC && form == ZINC_FORM_COEFF;  // kernel reads 128-bit m itself
   const size_t n = c->n, L = c->L;
-  const size_t per_msg = (slots ? n * 16 : 0) + L * n * 8;
-  const size_t chunk = std::max<size_t>(1, std::min(batch, (size_t)(256ull << 20) / per_msg));
+  const size_t per_msg = (slots ? n * 16 : 0) + (direct ? 0 : L * n * 8);
+  const size_t chunk = per_msg ? std::max<size_t>(1, std::min(batch, (size_t)(256ull << 20) / per_msg)) : batch;
   int64_t *m128 = nullptr;
   uint64_t *res = nullptr;
   if (slots) CUDA_TRY(cudaMallocAsync((void **)&m128, chunk * n * 16, s));
-  CUDA_TRY(cudaMallocAsync((void **)&res, chunk * L * n * 8, s));
+  if (!direct) CUDA_TRY(cudaMallocAsync((void **)&res, chunk * L * n * 8, s));
   const size_t in_stride = pt_stride_bytes(c, kind), ct_stride = 2 * L * n;
   zinc_status st = ZINC_OK;
   for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
     const size_t cnt = std::min(chunk, batch - off);
     const int64_t *mw = slots ? m128 : (const int64_t *)((const char *)pt + off * in_stride);
     if (slots && (st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m128, s, true))) break;
+    if (direct) {  // the add/inject kernel reads 128-bit plaintexts itself
+      ZincCoeffArgs za = zinc_coeff_args(c, key, nullptr, cnt, seed, msg_base + off, ct + off * ct_stride);
+      za.m128 = mw;
+      int threads = 256;
+      while (threads > 32 && zinc_coeff_smem(c->L, threads) > 72 * 1024) threads /= 2;
+      const size_t gy = (cnt + za.msgs_per_cta - 1) / za.msgs_per_cta;
+      LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(za, threads, (int)gy, 0, s));
+      continue;
+    }
     LiftArgs la{c->d_limbs, mw, res, cnt, (int)n, (int)L};
     LAUNCH(ZINC_K_LIFT, s, launch_lift(la, s));
     if (form == ZINC_FORM_NTT) {
@@ -581,7 +591,7 @@ static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int 
     LAUNCH(ZINC_K_PT_ADD, s, launch_pt_add(pa, s));
   }
   if (m128) cudaFreeAsync(m128, s);
-  cudaFreeAsync(res, s);
+  if (res) cudaFreeAsync(res, s);
   return st;
 }
 

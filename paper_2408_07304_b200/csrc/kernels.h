@@ -33,6 +33,7 @@ struct ZincCoeffArgs {
   uint64_t qmin;          // min_i q_i (fast-path bound)
   int n, L;
   int discard_m;          // m is library scratch: discard its L2 lines after reading
+  const int64_t *m128;    // CKKS 128-bit plaintexts (int64 pairs [batch][N][2]); overrides m
 };
 struct VanillaArgs {
   const LimbConst *limbs;

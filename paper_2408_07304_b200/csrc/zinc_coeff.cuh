@@ -84,6 +84,31 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
     }
   }
   const uint64_t qmin = a.qmin;
+  if (a.m128) {
+    // 128-bit plaintexts (f3, the paper's Delta = 2^55): the residue of hi 2^64 + lo + e1' per limb
+    pdl_wait();
+    for (size_t b = b_begin; b < b_end; ++b) {
+      const uint64_t msg = a.msg_base + b;
+      const int64_t *mp = a.m128 + (b * a.n + j) * 2;
+      const ulonglong2 p0 = ld2_nc(mp), p1 = ld2_nc(mp + 2);  // (lo, hi) of coefficients j, j + 1
+      const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
+      const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
+      const int e0 = cbd_lo(w1), e1 = cbd_hi(w1), f0 = cbd_lo(w2), f1 = cbd_hi(w2);
+      uint64_t *out = a.ct + b * 2 * lnn + j;
+#pragma unroll 1
+      for (int i = 0; i < L; ++i) {
+        const LimbConst &c = a.limbs[i];
+        const uint64_t q = sq[i];
+        uint64_t z10, z11, z20, z21;
+        ld2(tile + (size_t)i * T + jl, z10, z11);
+        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+        const uint64_t r0 = reduce_i128((int64_t)p0.y, p0.x, c), r1 = reduce_i128((int64_t)p1.y, p1.x, c);
+        st2_cs(out + (size_t)i * a.n, mod_add_signed(add_mod(z10, r0, q), e0, q), mod_add_signed(add_mod(z11, r1, q), e1, q));
+        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+      }
+    }
+    return;
+  }
   for (size_t b = b_begin; b < b_end; ++b) {
     const uint64_t msg = a.msg_base + b;
     const int64_t m0 = (int64_t)mv.x, m1 = (int64_t)mv.y;
