@@ -471,11 +471,12 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
 // One encryption path over messages whose int64 plaintexts are at m (or none).
 enum Path { PATH_ZINC = 0, PATH_VANILLA = 1 };
 // Instantiation of the NTT-path kernels: 0 CKKS with lazy-free forward transforms (all
-// q < 2^59, so (1 + 2 log2 N) q < 2^64), 1 CKKS with conditional subtractions, 2 BFV / BGV.
+// q < 2^58, so (3 + 4 log2 N) q < 2^64, see ct_bfly_nr), 1 CKKS with conditional
+// subtractions, 2 BFV / BGV.
 static int kernel_mode(const zinc_ctx *c) {
   if (c->scheme != ZINC_SCHEME_CKKS) return 2;
   for (uint64_t q : c->q)
-    if (q >= (1ull << 59)) return 1;
+    if (q >= (1ull << 58)) return 1;
   return 0;
 }
 static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, const int64_t *m, size_t batch,

@@ -154,13 +154,22 @@ ZINC_DEV void gs_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_
 }
 // [0, 4q) -> [0, q)
 ZINC_DEV uint64_t canon4(uint64_t x, uint64_t q, uint64_t two_q) { return csub(csub(x, two_q), q); }
-// Forward butterfly without the conditional subtraction: X, Y < B q -> X' , Y' < (B + 2) q
-// (T = Shoup(Y) < 2q for any 64-bit Y).  Canonical inputs grow to < (1 + 2 s) q after s
-// stages, so a whole transform stays below 2^64 while (1 + 2 log2 N) q < 2^64: q < 2^59 for
-// N <= 2^15 ("lazy-free" transforms; 6 fewer ALU instructions per butterfly).
+// High word of a 64 x 64-bit product from three 32-bit partial products (a_hi b_hi exact, the
+// cross terms' high halves; the low x low product and the cross terms' low halves dropped):
+// exact - 2 <= result <= exact.
+ZINC_DEV uint64_t umulhi_approx(uint64_t a, uint64_t b) {
+  const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32), bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
+  return (uint64_t)ah * bh + __umulhi(al, bh) + __umulhi(ah, bl);
+}
+// Forward butterfly without the conditional subtraction and with the cheaper Shoup quotient:
+// T = w Y - umulhi_approx(w', Y) q is w Y mod q plus at most 3q (the quotient is at most 2
+// short of Shoup's, which is itself within 1), so T < 4q and X, Y < B q -> X', Y' < (B + 4) q.
+// Canonical inputs stay below (1 + 4 s) q after s stages: a whole transform (plus one exact
+// split stage) fits in 64 bits while q < 2^58 for N <= 2^15 ("lazy-free" transforms: no
+// subtraction, one 32 x 32 -> 64 and two high-half multiplies instead of four for w'Y).
 ZINC_DEV void ct_bfly_nr(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
-  const uint64_t t = mul_shoup_lazy(Y, w, wp, q);
-  Y = X - t + two_q;
+  const uint64_t t = w * Y - umulhi_approx(wp, Y) * q;
+  Y = X - t + 2 * two_q;
   X = X + t;
 }
 // Any 64-bit value -> [0, q) (mu = floor(2^64 / q)): the end of a lazy-free transform.
