@@ -201,6 +201,25 @@ static zinc_status upload(T **dst, const std::vector<T> &src) {
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
+// Stream-ordered scratch, released (cudaFreeAsync on its stream) on every exit path.
+struct ScratchBuf {
+  void *p = nullptr;
+  cudaStream_t s;
+  explicit ScratchBuf(cudaStream_t s_) : s(s_) {}
+  ScratchBuf(const ScratchBuf &) = delete;
+  ScratchBuf &operator=(const ScratchBuf &) = delete;
+  ~ScratchBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+  }
+  cudaError_t alloc(size_t bytes) {
+    release();
+    return cudaMallocAsync(&p, bytes, s);
+  }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
 extern "C" {
 
 const char *zinc_last_error(void) { return g_err.c_str(); }
@@ -557,10 +576,11 @@ static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int 
   const size_t n = c->n, L = c->L;
   const size_t per_msg = (slots ? n * 16 : 0) + (direct ? 0 : L * n * 8);
   const size_t chunk = per_msg ? std::max<size_t>(1, std::min(batch, (size_t)(256ull << 20) / per_msg)) : batch;
-  int64_t *m128 = nullptr;
-  uint64_t *res = nullptr;
-  if (slots) CUDA_TRY(cudaMallocAsync((void **)&m128, chunk * n * 16, s));
-  if (!direct) CUDA_TRY(cudaMallocAsync((void **)&res, chunk * L * n * 8, s));
+  ScratchBuf m128b(s), resb(s);
+  if (slots) CUDA_TRY(m128b.alloc(chunk * n * 16));
+  if (!direct) CUDA_TRY(resb.alloc(chunk * L * n * 8));
+  int64_t *m128 = m128b.as<int64_t>();
+  uint64_t *res = resb.as<uint64_t>();
   const size_t in_stride = pt_stride_bytes(c, kind), ct_stride = 2 * L * n;
   zinc_status st = ZINC_OK;
   for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
@@ -591,8 +611,6 @@ static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int 
     PtAddArgs pa{c->d_limbs, res, ct + off * ct_stride, cnt, (int)n, (int)L};
     LAUNCH(ZINC_K_PT_ADD, s, launch_pt_add(pa, s));
   }
-  if (m128) cudaFreeAsync(m128, s);
-  if (res) cudaFreeAsync(res, s);
   return st;
 }
 
@@ -616,8 +634,13 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
                      fused_supported(c->log_n, c->L);
   const bool overlap = mode == 1 && batch > chunk;
   const int nbuf = (overlap || (fused && batch > chunk)) ? 2 : 1;
-  int64_t *m = nullptr;
-  CUDA_TRY(cudaMallocAsync((void **)&m, nbuf * chunk * per_msg, s));
+  // serial chunks chained with programmatic dependent launches (knob ZINC_TUNE_PDL) double-buffer
+  const bool pdl = !overlap && !fused && g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 &&
+                   path == PATH_ZINC && form == ZINC_FORM_COEFF;
+  const int nb = (nbuf == 2 || (pdl && batch > chunk)) ? 2 : 1;
+  ScratchBuf mbuf(s);
+  CUDA_TRY(mbuf.alloc(nb * chunk * per_msg));
+  int64_t *m = mbuf.as<int64_t>();
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_stride = (size_t)2 * c->L * c->n;
   zinc_status st = ZINC_OK;
@@ -642,19 +665,10 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
       g_launches.fetch_add(1, std::memory_order_relaxed);
       if (e != cudaSuccess) st = fail(ZINC_ECUDA, "fused encode/zinc launch: %s", cudaGetErrorString(e));
     }
-    cudaFreeAsync(m, s);
     return st;
   }
   if (!overlap) {
-    // serial chunks, double-buffered scratch, chained with programmatic dependent launches
-    // (knob ZINC_TUNE_PDL): each kernel's prologue overlaps the previous kernel's tail
-    const bool pdl = g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 && path == PATH_ZINC &&
-                     form == ZINC_FORM_COEFF;
-    const int nb = pdl && batch > chunk ? 2 : 1;
-    if (nb == 2 && nbuf == 1) {
-      cudaFreeAsync(m, s);
-      CUDA_TRY(cudaMallocAsync((void **)&m, 2 * chunk * per_msg, s));
-    }
+    // serial chunks; with PDL each kernel's prologue overlaps the previous kernel's tail
     size_t k = 0;
     for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
       const size_t cnt = std::min(chunk, batch - off);
@@ -668,42 +682,38 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
       PdlScope pdl_scope(pdl);
       if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
     }
-    cudaFreeAsync(m, s);
     return st;
   }
+  // side-stream overlap: events order the double-buffered scratch between the two streams
   std::lock_guard<std::mutex> lock(c->side_mu);
-  cudaEvent_t ev_in, ev_enc[2], ev_use[2];
-  CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
-  for (int k = 0; k < 2; ++k) {
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_enc[k], cudaEventDisableTiming));
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_use[k], cudaEventDisableTiming));
-  }
+  struct Events {
+    cudaEvent_t ev[5] = {};
+    ~Events() {
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } E;
+  for (cudaEvent_t &e : E.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t ev_in = E.ev[0], *ev_enc = E.ev + 1, *ev_use = E.ev + 3;
   CUDA_TRY(cudaEventRecord(ev_in, s));  // inputs and the scratch allocation are ready
   CUDA_TRY(cudaStreamWaitEvent(c->side, ev_in, 0));
+  cudaError_t ce = cudaSuccess;
   size_t k = 0;
-  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
+  for (size_t off = 0; off < batch && st == ZINC_OK && ce == cudaSuccess; off += chunk, ++k) {
     const int buf = (int)(k & 1);
     const size_t cnt = std::min(chunk, batch - off);
     int64_t *mb = m + (size_t)buf * chunk * c->n;
-    if (k >= 2) CUDA_TRY(cudaStreamWaitEvent(c->side, ev_use[buf], 0));  // chunk k-2 consumed mb
-    st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, c->side);
-    if (st != ZINC_OK) break;
-    CUDA_TRY(cudaEventRecord(ev_enc[buf], c->side));
-    CUDA_TRY(cudaStreamWaitEvent(s, ev_enc[buf], 0));
-    st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
-    if (st != ZINC_OK) break;
-    CUDA_TRY(cudaEventRecord(ev_use[buf], s));
+    if (k >= 2 && (ce = cudaStreamWaitEvent(c->side, ev_use[buf], 0)) != cudaSuccess) break;  // chunk k-2 read mb
+    if ((st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, c->side)) != ZINC_OK) break;
+    if ((ce = cudaEventRecord(ev_enc[buf], c->side)) != cudaSuccess) break;
+    if ((ce = cudaStreamWaitEvent(s, ev_enc[buf], 0)) != cudaSuccess) break;
+    if ((st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true))) break;
+    ce = cudaEventRecord(ev_use[buf], s);
   }
-  if (st != ZINC_OK) {  // keep the caller's stream ordered after whatever was enqueued on the side stream
-    cudaEventRecord(ev_in, c->side);
-    cudaStreamWaitEvent(s, ev_in, 0);
-  }
-  cudaFreeAsync(m, s);
-  cudaEventDestroy(ev_in);
-  for (int j = 0; j < 2; ++j) {
-    cudaEventDestroy(ev_enc[j]);
-    cudaEventDestroy(ev_use[j]);
-  }
+  // the caller's stream (and the scratch release on it) stays after everything on the side stream
+  cudaEventRecord(ev_in, c->side);
+  cudaStreamWaitEvent(s, ev_in, 0);
+  if (ce != cudaSuccess && st == ZINC_OK) st = fail(ZINC_ECUDA, "side-stream ordering: %s", cudaGetErrorString(ce));
   return st;
 }
 
@@ -801,10 +811,11 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
   if (c->scheme != ZINC_SCHEME_CKKS && slots_out)
     return fail(ZINC_EINVAL, "BFV / BGV decryption has no slot decoding (slots_out must be NULL)");
   CUDA_TRY(cudaSetDevice(c->device));
-  int64_t *x = coeff_out;
-  if (!x) CUDA_TRY(cudaMallocAsync((void **)&x, batch * (size_t)c->n * 8, s));
-  int64_t *xw = coeff128_out;
-  if (wide && !xw) CUDA_TRY(cudaMallocAsync((void **)&xw, batch * (size_t)c->n * 16, s));
+  ScratchBuf xb(s), xwb(s), xlb(s);
+  if (!coeff_out) CUDA_TRY(xb.alloc(batch * (size_t)c->n * 8));
+  if (wide && !coeff128_out) CUDA_TRY(xwb.alloc(batch * (size_t)c->n * 16));
+  int64_t *x = coeff_out ? coeff_out : xb.as<int64_t>();
+  int64_t *xw = coeff128_out ? coeff128_out : xwb.as<int64_t>();
   DecryptArgs a{};
   a.limbs = c->d_limbs;
   a.tw = c->d_tw;
@@ -818,10 +829,9 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
     a.x128_out = xw;
     a.q0inv_q1 = powm(c->q[0] % c->q[1], c->q[1] - 2, c->q[1]);
   }
-  uint64_t *xl = nullptr;
   if (c->scheme == ZINC_SCHEME_BFV) {
-    CUDA_TRY(cudaMallocAsync((void **)&xl, batch * (size_t)c->L * c->n * 8, s));
-    a.xl_out = xl;
+    CUDA_TRY(xlb.alloc(batch * (size_t)c->L * c->n * 8));
+    a.xl_out = xlb.as<uint64_t>();
   }
   st = ZINC_OK;
   {
@@ -836,7 +846,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
   if (st == ZINC_OK && c->scheme == ZINC_SCHEME_BFV) {
     BfvScaleArgs f{};
     f.limbs = c->d_limbs;
-    f.xl = xl;
+    f.xl = xlb.as<uint64_t>();
     f.m_out = x;
     f.batch = batch;
     f.n = c->n;
@@ -844,7 +854,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
     LAUNCH(ZINC_K_BFV_SCALE, s, launch_bfv_scale(f, s));
     if (status_out) CUDA_TRY(cudaMemsetAsync(status_out, 0, batch * sizeof(int32_t), s));
   }
-  if (xl) cudaFreeAsync(xl, s);
+  xlb.release();
   if (st == ZINC_OK && slots_out) {
     DecodeArgs d{};
     d.coeff = wide ? xw : x;
@@ -862,8 +872,6 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
     g_launches.fetch_add(1);
     if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decode launch: %s", cudaGetErrorString(e));
   }
-  if (!coeff_out) cudaFreeAsync(x, s);
-  if (wide && !coeff128_out) cudaFreeAsync(xw, s);
   return st;
 }
 
@@ -1019,19 +1027,28 @@ zinc_status zinc_encrypt_batch_host(const zinc_ctx *cc, int path, const uint64_t
   }
   for (int k = 0; k < 2; ++k)
     if (!c->h_streams[k]) CUDA_TRY(cudaStreamCreateWithFlags(&c->h_streams[k], cudaStreamNonBlocking));
+  // two streams alternate chunks; on any error both are drained before returning so that no
+  // copy still references the caller's host buffers
   size_t idx = 0;
+  cudaError_t ce = cudaSuccess;
+  st = ZINC_OK;
   for (size_t off = 0; off < batch; off += chunk, ++idx) {
     const int k = (int)(idx & 1);
     cudaStream_t s = c->h_streams[k];
     const size_t cnt = std::min(chunk, batch - off);
-    CUDA_TRY(cudaMemcpyAsync(c->h_pt_d[k], (const char *)pt_host + off * in_stride, cnt * in_stride,
-                             cudaMemcpyHostToDevice, s));
-    st = encrypt_any(c, path, key, form, kind, c->h_pt_d[k], cnt, seed, msg_base + off, c->h_ct_d[k], s);
-    if (st) return st;
-    CUDA_TRY(cudaMemcpyAsync(ct_host + off * ct_words, c->h_ct_d[k], cnt * ct_words * 8, cudaMemcpyDeviceToHost, s));
+    ce = cudaMemcpyAsync(c->h_pt_d[k], (const char *)pt_host + off * in_stride, cnt * in_stride,
+                         cudaMemcpyHostToDevice, s);
+    if (ce != cudaSuccess) break;
+    if ((st = encrypt_any(c, path, key, form, kind, c->h_pt_d[k], cnt, seed, msg_base + off, c->h_ct_d[k], s))) break;
+    ce = cudaMemcpyAsync(ct_host + off * ct_words, c->h_ct_d[k], cnt * ct_words * 8, cudaMemcpyDeviceToHost, s);
+    if (ce != cudaSuccess) break;
   }
-  for (int k = 0; k < 2; ++k) CUDA_TRY(cudaStreamSynchronize(c->h_streams[k]));
-  return ZINC_OK;
+  for (int k = 0; k < 2; ++k) {
+    const cudaError_t e = cudaStreamSynchronize(c->h_streams[k]);
+    if (ce == cudaSuccess) ce = e;
+  }
+  if (st == ZINC_OK && ce != cudaSuccess) st = fail(ZINC_ECUDA, "host pipeline: %s", cudaGetErrorString(ce));
+  return st;
 }
 
 }  // extern "C"
