@@ -233,7 +233,8 @@ enum {
   ZINC_K_CT_SUM = 13,    /* aggregation of a batch */
   ZINC_K_LIFT = 14,      /* 128-bit plaintexts -> RNS residues */
   ZINC_K_PT_ADD = 15,    /* c1 += plaintext residues */
-  ZINC_K_COUNT = 16
+  ZINC_K_ZINC_PIPE = 16,  /* persistent encode -> Zinc COEFF pipeline (ZINC_TUNE_OVERLAP = 3) */
+  ZINC_K_COUNT = 17
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */
@@ -257,15 +258,23 @@ void zinc_launch_count_reset(void);
  *                                 serial chunks on the caller's stream; 1: encode chunk k+1 on an
  *                                 internal high-priority stream; 2: one fused launch per chunk carries
  *                                 the encode of chunk k+1 and the add/inject of chunk k (real slots,
- *                                 N <= 2^14, L <= 8; otherwise serial)
+ *                                 N <= 2^14, L <= 8; otherwise serial); 3: one persistent
+ *                                 cooperative launch for the whole batch in which encoder CTAs fill
+ *                                 an L2-resident ring of plaintexts that streamer CTAs consume
+ *                                 (real slots, Zinc COEFF form, C1/C2/C3 shapes; otherwise serial)
  *  ZINC_TUNE_COEFF_SMEM_PAD       extra bytes of dynamic shared memory requested by the COEFF-form
  *                                 Zinc kernel (limits how many of its CTAs share an SM with the
  *                                 overlapped encode; default 0)
  *  ZINC_TUNE_PDL                  1 (default): the serial encode -> Zinc chunk pipeline chains its
  *                                 launches with programmatic dependent launch; 0: plain stream order
+ *  ZINC_TUNE_PIPE_ENC_CTAS        encoder CTAs per SM of the persistent pipeline (OVERLAP = 3; default 1;
+ *                                 0: only the CTAs the streamers leave over)
+ *  ZINC_TUNE_PIPE_VARIANT         persistent pipeline geometry: 0 (default) 3 CTAs/SM, radix-8 encode
+ *                                 passes; 1: 3 CTAs/SM, radix-16; 2: 2 CTAs/SM, radix-16
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_OVERLAP = 2,
-       ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_PDL = 4, ZINC_TUNE_COUNT = 5 };
+       ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_PDL = 4, ZINC_TUNE_PIPE_ENC_CTAS = 5, ZINC_TUNE_PIPE_VARIANT = 6,
+       ZINC_TUNE_COUNT = 7 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

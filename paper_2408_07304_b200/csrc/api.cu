@@ -52,7 +52,8 @@ static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
                                                  "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
                                                  "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel",
-                                                 "ct_sum_kernel", "lift_kernel", "pt_add_kernel"};
+                                                 "ct_sum_kernel", "lift_kernel", "pt_add_kernel",
+                                                 "zinc_pipe_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -99,11 +100,12 @@ struct TraceScope {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}, {1}, {0}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
   int device, log_n, n, L, log_scale;
+  int num_sms = 0;
   int scheme = ZINC_SCHEME_CKKS;
   uint64_t t = 0;  // plaintext modulus (BFV, BGV)
   bool wide = false;  // CKKS with log_scale >= 48: slot plaintexts take the 128-bit path
@@ -405,6 +407,10 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     return st;
   }
   c->qmin = *std::min_element(c->q.begin(), c->q.end());
+  if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    zinc_ctx_destroy(c);
+    return fail(ZINC_ECUDA, "device attribute query failed");
+  }
   // the side stream gets the highest priority so the block scheduler hands freed
   // SM slots to the (short) encode CTAs ahead of the streaming kernel's backlog
   int prio_lo = 0, prio_hi = 0;
@@ -632,10 +638,13 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
   const long long mode = g_tune[ZINC_TUNE_OVERLAP].load();
   const bool fused = mode == 2 && path == PATH_ZINC && form == ZINC_FORM_COEFF && kind == ZINC_PT_SLOTS_F64 &&
                      fused_supported(c->log_n, c->L);
+  const bool pipe = mode == 3 && path == PATH_ZINC && form == ZINC_FORM_COEFF && kind == ZINC_PT_SLOTS_F64 &&
+                    c->scheme == ZINC_SCHEME_CKKS && pipe_supported(c->log_n, c->L) && batch < (1ull << 31) &&
+                    chunk >= std::min<size_t>(batch, (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load()));
   const bool overlap = mode == 1 && batch > chunk;
   const int nbuf = (overlap || (fused && batch > chunk)) ? 2 : 1;
   // serial chunks chained with programmatic dependent launches (knob ZINC_TUNE_PDL) double-buffer
-  const bool pdl = !overlap && !fused && g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 &&
+  const bool pdl = !pipe && !overlap && !fused && g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 &&
                    path == PATH_ZINC && form == ZINC_FORM_COEFF;
   const int nb = (nbuf == 2 || (pdl && batch > chunk)) ? 2 : 1;
   ScratchBuf mbuf(s);
@@ -644,6 +653,29 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_stride = (size_t)2 * c->L * c->n;
   zinc_status st = ZINC_OK;
+  if (pipe) {
+    // one persistent launch: the ring is the scratch (chunk messages), plus its sync words
+    ScratchBuf sync(s);
+    const int ring = (int)chunk;
+    const size_t sync_bytes = pipe_sync_words(ring, c->n / 512) * sizeof(uint32_t);
+    CUDA_TRY(sync.alloc(sync_bytes));
+    CUDA_TRY(cudaMemsetAsync(sync.p, 0, sync_bytes, s));
+    PipeArgs pa{};
+    pa.z = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
+    pa.e = encode_args(c, kind, pt, m);
+    pa.sync = sync.as<uint32_t>();
+    pa.ring = ring;
+    pa.enc_per_sm = (int)std::min<long long>(8, g_tune[ZINC_TUNE_PIPE_ENC_CTAS].load());
+    pa.tiles = c->n / 512;
+    cudaError_t e;
+    {
+      TraceScope ts(ZINC_K_ZINC_PIPE, s);
+      e = launch_zinc_pipe(c->log_n, pa, (int)g_tune[ZINC_TUNE_PIPE_VARIANT].load(), c->num_sms, s);
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (e != cudaSuccess) st = fail(ZINC_ECUDA, "persistent encode/zinc launch: %s", cudaGetErrorString(e));
+    return st;
+  }
   if (fused) {
     // launch k: encode chunk k (k < nch) into m[k % 2] | add/inject chunk k-1 from m[(k-1) % 2]
     const size_t nch = (batch + chunk - 1) / chunk;

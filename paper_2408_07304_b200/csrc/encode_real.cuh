@@ -26,6 +26,49 @@ ZINC_DEV uint32_t pow5_mod_pow2(uint32_t e, uint32_t mask) {
   return r;
 }
 
+// Split step, twist and rounding of one message's half-length FFT result `buf`
+// into the plaintext coefficients m[0, 2M) (C-6).
+template <int LOGM, bool WIDE>
+ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *buf) {
+  constexpr int M = 1 << LOGM, H = M / 2, THREADS = 256;
+  const int tid = threadIdx.x;
+  const double scale = a.scale;  // Delta / M
+  constexpr int V = 4;  // independent post-processing iterations per batch
+  static_assert(H % (THREADS * V) == 0, "post tiling");
+#pragma unroll 1
+  for (int j0 = tid; j0 < H; j0 += THREADS * V) {
+    double2 w[V], tw0[V], tw1[V];
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int j = j0 + u * THREADS;
+      w[u] = __ldg(a.fft_tw + j);
+      tw0[u] = __ldg(a.twist + j);
+      tw1[u] = __ldg(a.twist + j + H);
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const int j = j0 + u * THREADS;
+      const double2 xj = buf[pad16(j)], xr = conj2(buf[pad16((H - j) & (H - 1))]);
+      const double2 e = make_double2(0.5 * (xj.x + xr.x), 0.5 * (xj.y + xr.y));
+      const double2 d = make_double2(0.5 * (xj.x - xr.x), 0.5 * (xj.y - xr.y));
+      const double2 o = make_double2(d.y, -d.x);  // -i d
+      const double2 t = cmul(o, w[u]);
+      const double2 y0 = cmul(cadd(e, t), tw0[u]), y1 = cmul(csubd(e, t), tw1[u]);
+      if constexpr (WIDE) {  // 128-bit coefficients (f3: Delta = 2^55 and large slots)
+        store_i128(m + 2 * j, y0.x * scale);
+        store_i128(m + 2 * (j + M), y0.y * scale);
+        store_i128(m + 2 * (j + H), y1.x * scale);
+        store_i128(m + 2 * (j + H + M), y1.y * scale);
+      } else {
+        m[j] = llround(y0.x * scale);  // plain stores: the path kernel re-reads m from L2
+        m[j + M] = llround(y0.y * scale);
+        m[j + H] = llround(y1.x * scale);
+        m[j + H + M] = llround(y1.y * scale);
+      }
+    }
+  }
+}
+
 // Shared memory bytes of one real-slot encode CTA (FFT buffer + twiddles).
 template <int LOGM> constexpr size_t encode_real_smem() {
   return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + (1 << (LOGM - 1)) / 2) * sizeof(double2);
@@ -77,42 +120,65 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   // this encode overwrites: the loads and the FFT above overlapped it, the stores wait.
   pdl_trigger();
   pdl_wait();
-  int64_t *m = a.m_out + b * (2 * M) * (WIDE ? 2 : 1);
-  const double scale = a.scale;  // Delta / M
-  constexpr int V = 4;  // independent post-processing iterations per batch
-  static_assert(H % (THREADS * V) == 0, "post tiling");
-#pragma unroll 1
-  for (int j0 = tid; j0 < H; j0 += THREADS * V) {
-    double2 w[V], tw0[V], tw1[V];
+  encode_real_post<LOGM, WIDE>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf);
+}
+
+// Shared memory bytes of the lighter encode role of the persistent pipeline
+// (FFT buffer only: twiddles are read through L1).
+template <int LOGM> constexpr size_t encode_real_lite_smem() {
+  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16) * sizeof(double2);
+}
+
+// The same encode for the persistent pipeline (k_pipe.cu): slots are read
+// straight into registers (two halves, no in-place permutation, no TMA), the
+// FFT twiddles come through L1, and the plaintext goes to ring slot `b_out`
+// after `before_store()` (which waits until that slot is free) returns.
+template <int LOGM, int NPASS, class Hook>
+ZINC_DEV void encode_real_lite_body(const EncodeArgs &a, size_t b, size_t b_out, double2 *buf, Hook before_store) {
+  constexpr int M = 1 << LOGM, LH = LOGM - 1;
+  constexpr int THREADS = 256, PER = M / THREADS, HALF = PER / 2;
+  using P = FftPlan<LH>;
+  double *bufd = reinterpret_cast<double *>(buf);
+  const int tid = threadIdx.x;
+  constexpr uint32_t MASK = 4u * M - 1u;  // mod 2N
+  uint32_t g = pow5_mod_pow2((uint32_t)tid, MASK);
+  const uint32_t step = pow5_mod_pow2((uint32_t)THREADS, MASK);
+  const double *src = a.slots + b * M + tid;
 #pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int j = j0 + u * THREADS;
-      w[u] = __ldg(a.fft_tw + j);
-      tw0[u] = __ldg(a.twist + j);
-      tw1[u] = __ldg(a.twist + j + H);
-    }
+  for (int half = 0; half < 2; ++half) {
+    double zv[HALF];
 #pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int j = j0 + u * THREADS;
-      const double2 xj = buf[pad16(j)], xr = conj2(buf[pad16((H - j) & (H - 1))]);
-      const double2 e = make_double2(0.5 * (xj.x + xr.x), 0.5 * (xj.y + xr.y));
-      const double2 d = make_double2(0.5 * (xj.x - xr.x), 0.5 * (xj.y - xr.y));
-      const double2 o = make_double2(d.y, -d.x);  // -i d
-      const double2 t = cmul(o, w[u]);
-      const double2 y0 = cmul(cadd(e, t), tw0[u]), y1 = cmul(csubd(e, t), tw1[u]);
-      if constexpr (WIDE) {  // 128-bit coefficients (f3: Delta = 2^55 and large slots)
-        store_i128(m + 2 * j, y0.x * scale);
-        store_i128(m + 2 * (j + M), y0.y * scale);
-        store_i128(m + 2 * (j + H), y1.x * scale);
-        store_i128(m + 2 * (j + H + M), y1.y * scale);
-      } else {
-        m[j] = llround(y0.x * scale);  // plain stores: the path kernel re-reads m from L2
-        m[j + M] = llround(y0.y * scale);
-        m[j + H] = llround(y1.x * scale);
-        m[j + H + M] = llround(y1.y * scale);
-      }
+    for (int i = 0; i < HALF; ++i) zv[i] = __ldg(src + (half * HALF + i) * THREADS);
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) {
+      const uint32_t h = g >> 2;  // h_k = (g_k - 1) / 4
+      const int pos = (int)(__brev(h >> 1) >> (32 - LH));
+      bufd[2 * pad16(pos) + (h & 1)] = zv[i];
+      g = (g * step) & MASK;
     }
   }
+  __syncthreads();
+  auto lds = [&](int i) { return buf[pad16(i)]; };
+  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
+  if constexpr (NPASS == 3) {  // radix-16 passes (16 complex values per thread)
+    fft_pass<LH, 0, P::K1, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+    __syncthreads();
+    fft_pass<LH, P::K1, P::K2, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+    __syncthreads();
+    fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+  } else {  // radix-8 passes: half the registers, one more trip through shared memory
+    static_assert(LH >= 10, "four-pass plan");
+    fft_pass<LH, 0, 3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 3, 3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 6, 3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 9, LH - 9, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
+  }
+  __syncthreads();
+  before_store();
+  encode_real_post<LOGM, false>(a, a.m_out + b_out * (2 * M), buf);
 }
 
 }  // namespace zinc

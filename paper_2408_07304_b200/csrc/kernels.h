@@ -137,6 +137,16 @@ struct SampleArgs {
   size_t n;
   void *out;
 };
+// Persistent encode -> Zinc COEFF pipeline (k_pipe.cu).  z.m and e.m_out are the
+// ring of `ring` int64 plaintext slots; sync holds pipe_sync_words(ring) zeroed words.
+struct PipeArgs {
+  ZincCoeffArgs z;
+  EncodeArgs e;
+  uint32_t *sync;
+  int ring, tiles;
+  int enc_per_sm;  // encoder CTAs per SM (0: only the CTAs left over by the streamers)
+  int streamers;   // set by the launcher: a multiple of tiles
+};
 struct IntPeakArgs {
   uint64_t q, w, wp;
   int iters;
@@ -150,6 +160,9 @@ cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, s
 bool fused_supported(int log_n, int L);
 cudaError_t launch_zinc_coeff_encode(int log_n, const ZincCoeffArgs &za, int gy, const EncodeArgs &ea, int enc_ctas,
                                      cudaStream_t s);
+bool pipe_supported(int log_n, int L);
+size_t pipe_sync_words(int ring, int tiles);
+cudaError_t launch_zinc_pipe(int log_n, const PipeArgs &p, int variant, int num_sms, cudaStream_t s);
 cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                            cudaStream_t s);
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s);

@@ -38,6 +38,8 @@ def main():
     ap.add_argument("--mpc", default="1,2,4,8,16")
     ap.add_argument("--chunks-mb", default="16,32,48")
     ap.add_argument("--pads-kb", default="0,12")
+    ap.add_argument("--pdl", default="1,0")
+    ap.add_argument("--overlaps", default="0,1,2")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     B = args.batch or cfg.batch
@@ -58,7 +60,7 @@ def main():
               flush=True)
 
     rep("encode", timeit(lambda: Z.ckks_encode_batch(ctx, slots, out=m)), in_bytes + cfg.n * 8)
-    for pdl in (1, 0):
+    for pdl in [int(x) for x in args.pdl.split(",")]:
       Z.tune(Z.TUNE_PDL, pdl)
       for pad in [int(x) for x in args.pads_kb.split(",")]:
           Z.tune(Z.TUNE_COEFF_SMEM_PAD, pad << 10)
@@ -66,7 +68,7 @@ def main():
               Z.tune(Z.TUNE_COEFF_MSGS_PER_CTA, mpc)
               rep("zinc_i64", timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, m, 1, 0, out=ct)),
                   ct_bytes + cfg.n * 8, mpc=mpc, pad_kb=pad, pdl=pdl)
-          for ov in (0, 1, 2):
+          for ov in [int(x) for x in args.overlaps.split(",")]:
               Z.tune(Z.TUNE_OVERLAP, ov)
               for mb in [int(x) for x in args.chunks_mb.split(",")]:
                   Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, mb << 20)

@@ -340,6 +340,37 @@ def test_tuning_knobs_never_change_results(Z, orc, knobs):
     assert torch.equal(ref, got) and torch.equal(ref_v, got_v)
 
 
+@pytest.mark.parametrize("name,batch,ring,enc,mpc,variant", [
+    ("C3", 70, 256, 1, 2, 0), ("C3", 70, 2, 0, 2, 0), ("C3", 33, 3, 2, 3, 1), ("C3", 1, 256, 1, 2, 2),
+    ("C3", 300, 16, 2, 1, 0), ("C1", 257, 4, 0, 2, 0), ("C2", 129, 8, 5, 4, 2), ("C2", 40, 40, 1, 8, 1)])
+def test_persistent_pipeline_bit_exact(Z, orc, name, batch, ring, enc, mpc, variant):
+    """The persistent encode -> Zinc COEFF pipeline (ZINC_TUNE_OVERLAP = 3: encoder CTAs fill a
+    ring of L2-resident plaintexts that streamer CTAs consume) gives the serial path's
+    ciphertexts bit for bit, including a ring as small as one work item (many laps per slot),
+    only the leftover CTAs encoding, more encoders than messages, and ragged batches; and the
+    oracle's."""
+    s = setup_for(Z, orc, name)
+    z = torch.from_numpy(slots_batch(s.cfg, 0, batch)).cuda()
+    ref = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 5, 1000)
+    knobs = {Z.TUNE_OVERLAP: 3, Z.TUNE_ENCODE_CHUNK_BYTES: ring * s.cfg.n * 8, Z.TUNE_PIPE_ENC_CTAS: enc,
+             Z.TUNE_COEFF_MSGS_PER_CTA: mpc, Z.TUNE_PIPE_VARIANT: variant}
+    old = {k: Z.tune(k, v) for k, v in knobs.items()}
+    try:
+        Z.launch_count_reset()
+        got = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 5, 1000)
+        torch.cuda.synchronize()
+        launches = Z.launch_count()
+    finally:
+        for k, v in old.items():
+            Z.tune(k, v)
+    assert launches == 1                      # one persistent launch for the whole batch
+    assert torch.equal(ref, got)
+    m = Z.ckks_encode_batch(s.ctx, z[-1:]).cpu().numpy()[0]
+    want = orc.zinc_encrypt(s.P, orc.precompute_cache(s.P, s.o_pk, s.cfg.cache_seed, COEFF), COEFF, m, 5,
+                            1000 + batch - 1)
+    assert np.array_equal(got[-1].cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
 def test_ct_add_and_sum_bit_exact_and_decrypt(Z, orc, name):
     """Eq. 2 kernels: batched (+) and aggregation bit-exact against
