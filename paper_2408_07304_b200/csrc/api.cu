@@ -100,7 +100,7 @@ struct TraceScope {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}, {1}, {0}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}, {1}, {0}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -533,6 +533,8 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   if (path == PATH_ZINC && form == ZINC_FORM_COEFF) {
     ZincCoeffArgs a = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
     a.discard_m = m_is_scratch ? 1 : 0;
+    a.prefetch = (const char *)g_l2_prefetch.p;
+    a.prefetch_bytes = g_l2_prefetch.bytes & ~(size_t)15;
     int threads = 256;
     while (threads > 32 && zinc_coeff_smem(c->L, threads) > 72 * 1024) threads /= 2;
     const size_t gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
@@ -712,7 +714,12 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
         st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
       }
       PdlScope pdl_scope(pdl);
+      // the Zinc kernel of this chunk warms the next chunk's slots into L2 for its encode
+      const size_t nxt = std::min(chunk, batch - std::min(batch, off + chunk));
+      const bool pf = g_tune[ZINC_TUNE_L2_PREFETCH].load() != 0 && nxt > 0 && aligned16(pt) && in_stride % 16 == 0;
+      g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + chunk) * in_stride, nxt * in_stride} : L2Prefetch{};
       if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
+      g_l2_prefetch = L2Prefetch{};
     }
     return st;
   }

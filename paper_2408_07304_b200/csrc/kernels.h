@@ -16,6 +16,12 @@ using Tw = ulonglong2;  // {w, floor(w 2^64 / q)}
 // thread: the next kernel in the stream may start once every CTA of the previous one has
 // started (griddepcontrol.launch_dependents) and must griddepcontrol.wait before touching
 // the previous kernel's outputs.  Used by the encode -> Zinc chunk pipeline.
+// L2 prefetch request handed from the chunk pipeline to the next Zinc COEFF launch
+struct L2Prefetch {
+  const void *p = nullptr;
+  size_t bytes = 0;
+};
+inline thread_local L2Prefetch g_l2_prefetch;
 inline thread_local bool g_launch_pdl = false;
 struct PdlScope {
   bool old;
@@ -34,6 +40,8 @@ struct ZincCoeffArgs {
   int n, L;
   int discard_m;          // m is library scratch: discard its L2 lines after reading
   const int64_t *m128;    // CKKS 128-bit plaintexts (int64 pairs [batch][N][2]); overrides m
+  const char *prefetch;   // the next chunk's slots: warmed into L2 while this chunk streams
+  size_t prefetch_bytes;  // (16-byte multiple; 0: none)
 };
 struct VanillaArgs {
   const LimbConst *limbs;

@@ -62,6 +62,16 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
                    ::"r"(dst), "l"(src), "r"(bytes), "r"(mb) : "memory");
     }
   }
+  if (threadIdx.x == 32 && a.prefetch_bytes) {
+    // warm this CTA's share of the next chunk's slots into L2 (the next encode reads them)
+    const size_t nblk = (size_t)gridDim.x * gridDim.y;
+    const size_t share = ((a.prefetch_bytes + nblk - 1) / nblk + 15) & ~(size_t)15;
+    const size_t lo = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * share;
+    if (lo < a.prefetch_bytes) {
+      const uint32_t sz = (uint32_t)min(share, a.prefetch_bytes - lo);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.prefetch + lo), "r"(sz) : "memory");
+    }
+  }
   const int jl = 2 * threadIdx.x;       // local coefficient pair
   const int j = j0 + jl;
   const size_t b_begin = (size_t)group_y * a.msgs_per_cta;

@@ -1,0 +1,34 @@
+"""A/B of one tuning knob on the slots -> Zinc COEFF path (C3 by default):
+python scripts/ab_knob.py KNOB V0 V1 [config].  Alternates the two values 4 times,
+median of 5 each, and checks the ciphertexts are identical.  Development tool."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2408_07304_b200 as Z  # noqa: E402
+from workloads import CONFIGS, slots_batch  # noqa: E402
+from sweep_zinc import timeit  # noqa: E402
+
+knob, v0, v1 = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
+cfg = CONFIGS[sys.argv[4] if len(sys.argv) > 4 else "C3"]
+ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
+_, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
+cache = Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, Z.COEFF)
+z = slots_batch(cfg, 0, cfg.batch)
+if cfg.complex_slots:
+    z = np.stack([z.real, z.imag], axis=-1)
+slots = torch.from_numpy(np.ascontiguousarray(z)).cuda()
+ct = ctx.empty_ct(cfg.batch)
+res = {v0: [], v1: []}
+outs = {}
+for _ in range(4):
+    for v in (v0, v1):
+        Z.tune(knob, v)
+        res[v].append(timeit(lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, slots, 1, 0, out=ct)))
+        outs[v] = ct.clone() if v not in outs else outs[v]
+print(json.dumps({"knob": knob, str(v0): float(np.median(res[v0])), str(v1): float(np.median(res[v1])),
+                  "all": {str(k): v for k, v in res.items()}, "equal": bool(torch.equal(outs[v0], outs[v1]))}))
