@@ -28,9 +28,9 @@ ZINC_DEV uint32_t pow5_mod_pow2(uint32_t e, uint32_t mask) {
 
 // Split step, twist and rounding of one message's half-length FFT result `buf`
 // into the plaintext coefficients m[0, 2M) (C-6).
-template <int LOGM, bool WIDE>
+template <int LOGM, bool WIDE, int THREADS = 256>
 ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *buf) {
-  constexpr int M = 1 << LOGM, H = M / 2, THREADS = 256;
+  constexpr int M = 1 << LOGM, H = M / 2;
   const int tid = threadIdx.x;
   const double scale = a.scale;  // Delta / M
   constexpr int V = 4;  // independent post-processing iterations per batch
@@ -74,13 +74,37 @@ template <int LOGM> constexpr size_t encode_real_smem() {
   return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + (1 << (LOGM - 1)) / 2) * sizeof(double2);
 }
 
+// The half-length DIT FFT of the encode: NPASS = 3 radix-16 passes (FftPlan) or
+// NPASS = 4 radix-8 passes (3 + 3 + 3 + rest; half the registers per thread).
+template <int LH, int THREADS, int NPASS, bool TW_SMEM, class Ld, class St>
+ZINC_DEV void encode_fft(const double2 *tw, Ld lds, St sts) {
+  using P = FftPlan<LH>;
+  if constexpr (NPASS == 3) {
+    fft_pass<LH, 0, P::K1, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, P::K1, P::K2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+  } else {
+    static_assert(LH >= 10, "four-pass plan");
+    fft_pass<LH, 0, 3, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 3, 3, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 6, 3, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 9, LH - 9, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+  }
+}
+
 // One CTA's work: encode message `b`; `buf` is the CTA's dynamic shared memory.
-template <int LOGM, bool WIDE = false>
+// THREADS = 256 with radix-16 passes, or 512 with radix-8 passes (NPASS = 4): twice
+// the warps on one message's latency-bound phases at the same shared memory.
+template <int LOGM, bool WIDE = false, int THREADS = 256, int NPASS = 3>
 ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   constexpr int M = 1 << LOGM, LH = LOGM - 1, H = 1 << LH;
-  constexpr int THREADS = 256, PER = M / THREADS;
-  using P = FftPlan<LH>;
-  static_assert(P::THREADS == THREADS, "plan");
+  constexpr int PER = M / THREADS;
+  static_assert(NPASS == 4 || FftPlan<LH>::THREADS == THREADS, "plan");
   double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2]
   double *bufd = reinterpret_cast<double *>(buf);
   __shared__ __align__(8) uint64_t mbar;
@@ -110,17 +134,13 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   __syncthreads();
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
-  fft_pass<LH, 0, P::K1, THREADS, true, false, 1, true>(stw, lds, sts);
-  __syncthreads();
-  fft_pass<LH, P::K1, P::K2, THREADS, true, false, 1, true>(stw, lds, sts);
-  __syncthreads();
-  fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, true>(stw, lds, sts);
+  encode_fft<LH, THREADS, NPASS, true>(stw, lds, sts);
   __syncthreads();
   // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
   // this encode overwrites: the loads and the FFT above overlapped it, the stores wait.
   pdl_trigger();
   pdl_wait();
-  encode_real_post<LOGM, WIDE>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf);
+  encode_real_post<LOGM, WIDE, THREADS>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf);
 }
 
 // Shared memory bytes of the lighter encode role of the persistent pipeline
@@ -137,7 +157,6 @@ template <int LOGM, int NPASS, class Hook>
 ZINC_DEV void encode_real_lite_body(const EncodeArgs &a, size_t b, size_t b_out, double2 *buf, Hook before_store) {
   constexpr int M = 1 << LOGM, LH = LOGM - 1;
   constexpr int THREADS = 256, PER = M / THREADS, HALF = PER / 2;
-  using P = FftPlan<LH>;
   double *bufd = reinterpret_cast<double *>(buf);
   const int tid = threadIdx.x;
   constexpr uint32_t MASK = 4u * M - 1u;  // mod 2N
@@ -160,22 +179,7 @@ ZINC_DEV void encode_real_lite_body(const EncodeArgs &a, size_t b, size_t b_out,
   __syncthreads();
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
-  if constexpr (NPASS == 3) {  // radix-16 passes (16 complex values per thread)
-    fft_pass<LH, 0, P::K1, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-    __syncthreads();
-    fft_pass<LH, P::K1, P::K2, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-    __syncthreads();
-    fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-  } else {  // radix-8 passes: half the registers, one more trip through shared memory
-    static_assert(LH >= 10, "four-pass plan");
-    fft_pass<LH, 0, 3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-    __syncthreads();
-    fft_pass<LH, 3, 3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-    __syncthreads();
-    fft_pass<LH, 6, 3, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-    __syncthreads();
-    fft_pass<LH, 9, LH - 9, THREADS, true, false, 1, false>(a.fft_tw_h, lds, sts);
-  }
+  encode_fft<LH, THREADS, NPASS, false>(a.fft_tw_h, lds, sts);
   __syncthreads();
   before_store();
   encode_real_post<LOGM, false>(a, a.m_out + b_out * (2 * M), buf);
