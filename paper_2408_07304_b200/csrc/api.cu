@@ -113,7 +113,7 @@ struct zinc_ctx {
   std::vector<LimbConst> h_limbs;
   LimbConst *d_limbs = nullptr;
   Tw *d_tw = nullptr, *d_itw = nullptr;
-  double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr;
+  double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr, *d_post_tw = nullptr;
   int *d_perm = nullptr;
   // host-API pipeline buffers (grow-only, guarded)
   std::mutex host_mu;
@@ -276,6 +276,7 @@ zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
   cudaFree(ctx->d_itw);
   cudaFree(ctx->d_fft_tw);
   cudaFree(ctx->d_twist);
+  cudaFree(ctx->d_post_tw);
   cudaFree(ctx->d_fft_tw_h);
   cudaFree(ctx->d_perm);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -393,6 +394,20 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     long double ang = -pi * (long double)j / (long double)n;
     twist[j] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
+  // split tables of the real-slot encode's post step: t_j = e^{-i pi j/N} = A[j/64] B[j%64],
+  // p_j = e^{-5 i pi j/N} = A5[j/64] B5[j%64], j < N/4
+  const int na = (n / 4) / 64;
+  std::vector<double2> post_tw;
+  for (int k : {1, 5}) {
+    for (int x = 0; x < na; ++x) {
+      long double ang = -pi * (long double)k * 64.0L * (long double)x / (long double)n;
+      post_tw.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+    }
+    for (int x = 0; x < 64; ++x) {
+      long double ang = -pi * (long double)k * (long double)x / (long double)n;
+      post_tw.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+    }
+  }
   uint64_t g = 1;
   for (int k = 0; k < M; ++k) {
     perm[k] = (int)brv((uint32_t)((g - 1) / 4), log_m);
@@ -402,7 +417,7 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
   if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(ZINC_ECUDA, "cudaSetDevice(%d) failed", device); }
   if ((st = upload(&c->d_limbs, c->h_limbs)) || (st = upload(&c->d_tw, tw)) || (st = upload(&c->d_itw, itw)) ||
       (st = upload(&c->d_fft_tw, ftw)) || (st = upload(&c->d_twist, twist)) || (st = upload(&c->d_perm, perm)) ||
-      (st = upload(&c->d_fft_tw_h, ftw_h))) {
+      (st = upload(&c->d_fft_tw_h, ftw_h)) || (st = upload(&c->d_post_tw, post_tw))) {
     zinc_ctx_destroy(c);
     return st;
   }
@@ -480,6 +495,7 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
   a.fft_tw = c->d_fft_tw;
   a.twist = c->d_twist;
   a.fft_tw_h = c->d_fft_tw_h;
+  a.post_tw = c->d_post_tw;
   a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
   a.m_out = m;
   return a;

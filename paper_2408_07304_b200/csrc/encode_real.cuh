@@ -27,33 +27,37 @@ ZINC_DEV uint32_t pow5_mod_pow2(uint32_t e, uint32_t mask) {
 }
 
 // Split step, twist and rounding of one message's half-length FFT result `buf`
-// into the plaintext coefficients m[0, 2M) (C-6).
-template <int LOGM, bool WIDE, int THREADS = 256>
-ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *buf) {
-  constexpr int M = 1 << LOGM, H = M / 2;
+// into the plaintext coefficients m[0, 2M) (C-6).  For j < H = M/2:
+//   E = (X_j + conj X_{H-j}) / 2,  O = -i (X_j - conj X_{H-j}) / 2,
+//   y0 = (E + W_M^j O) zeta^-j = E t_j + O p_j,   y1 = (E - W_M^j O) zeta^-(j+H) = (E t_j - O p_j) c
+// with t_j = zeta^-j = e^{-i pi j / N}, p_j = W_M^j t_j = e^{-5 i pi j / N} and the constant
+// c = zeta^-H = e^{-i pi / 4} (H = N/4).  t_j and p_j come from two split tables each
+// (j = 64 a + b: t_j = A[a] B[b], p_j = A5[a] B5[b]; `ptw` = [A | B | A5 | B5], H/64 + 64
+// entries per pair, 4 KiB at N = 2^14) instead of 48 bytes of L2-resident tables per j.
+template <int LOGM, bool WIDE, int THREADS = 256, bool PT_SMEM = true>
+ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *buf, const double2 *ptw) {
+  constexpr int M = 1 << LOGM, H = M / 2, NA = H / 64;
+  constexpr double R = 0.70710678118654752440;  // c = R (1 - i)
+  const double2 *tA = ptw, *tB = ptw + NA, *tA5 = tB + 64, *tB5 = tA5 + NA;
+  auto ld = [](const double2 *p) { return PT_SMEM ? *p : __ldg(p); };
   const int tid = threadIdx.x;
   const double scale = a.scale;  // Delta / M
   constexpr int V = 4;  // independent post-processing iterations per batch
   static_assert(H % (THREADS * V) == 0, "post tiling");
 #pragma unroll 1
   for (int j0 = tid; j0 < H; j0 += THREADS * V) {
-    double2 w[V], tw0[V], tw1[V];
 #pragma unroll
     for (int u = 0; u < V; ++u) {
       const int j = j0 + u * THREADS;
-      w[u] = __ldg(a.fft_tw + j);
-      tw0[u] = __ldg(a.twist + j);
-      tw1[u] = __ldg(a.twist + j + H);
-    }
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const int j = j0 + u * THREADS;
+      const double2 t = cmul(ld(tA + (j >> 6)), ld(tB + (j & 63)));
+      const double2 pj = cmul(ld(tA5 + (j >> 6)), ld(tB5 + (j & 63)));
       const double2 xj = buf[pad16(j)], xr = conj2(buf[pad16((H - j) & (H - 1))]);
       const double2 e = make_double2(0.5 * (xj.x + xr.x), 0.5 * (xj.y + xr.y));
       const double2 d = make_double2(0.5 * (xj.x - xr.x), 0.5 * (xj.y - xr.y));
       const double2 o = make_double2(d.y, -d.x);  // -i d
-      const double2 t = cmul(o, w[u]);
-      const double2 y0 = cmul(cadd(e, t), tw0[u]), y1 = cmul(csubd(e, t), tw1[u]);
+      const double2 U = cmul(e, t), W = cmul(o, pj);
+      const double2 y0 = cadd(U, W), df = csubd(U, W);
+      const double2 y1 = make_double2(R * (df.x + df.y), R * (df.y - df.x));
       if constexpr (WIDE) {  // 128-bit coefficients (f3: Delta = 2^55 and large slots)
         store_i128(m + 2 * j, y0.x * scale);
         store_i128(m + 2 * (j + M), y0.y * scale);
@@ -69,9 +73,13 @@ ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *b
   }
 }
 
+// Entries of the split post tables (A, B, A5, B5).
+template <int LOGM> __host__ __device__ constexpr int encode_post_tw_entries() { return 2 * ((1 << (LOGM - 1)) / 64 + 64); }
+
 // Shared memory bytes of one real-slot encode CTA (FFT buffer + twiddles).
 template <int LOGM> constexpr size_t encode_real_smem() {
-  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + (1 << (LOGM - 1)) / 2) * sizeof(double2);
+  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + (1 << (LOGM - 1)) / 2 + encode_post_tw_entries<LOGM>()) *
+         sizeof(double2);
 }
 
 // The half-length DIT FFT of the encode: NPASS = 3 radix-16 passes (FftPlan) or
@@ -105,16 +113,19 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   constexpr int M = 1 << LOGM, LH = LOGM - 1, H = 1 << LH;
   constexpr int PER = M / THREADS;
   static_assert(NPASS == 4 || FftPlan<LH>::THREADS == THREADS, "plan");
-  double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2]
+  double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2], then post tables
+  double2 *sptw = stw + H / 2;
+  constexpr int NPT = encode_post_tw_entries<LOGM>();
   double *bufd = reinterpret_cast<double *>(buf);
   __shared__ __align__(8) uint64_t mbar;
   const int tid = threadIdx.x;
   if (tid == 0) mbar_init(&mbar, 1);
   __syncthreads();
   if (tid == 0) {
-    mbar_expect_tx(&mbar, (uint32_t)(M * sizeof(double) + (H / 2) * sizeof(double2)));
+    mbar_expect_tx(&mbar, (uint32_t)(M * sizeof(double) + (H / 2 + NPT) * sizeof(double2)));
     bulk_g2s(buf, a.slots + b * M, M * sizeof(double), &mbar);  // raw slots into the buffer prefix
     bulk_g2s(stw, a.fft_tw_h, (H / 2) * sizeof(double2), &mbar);
+    bulk_g2s(sptw, a.post_tw, NPT * sizeof(double2), &mbar);
   }
   constexpr uint32_t MASK = 4u * M - 1u;  // mod 2N
   uint32_t g = pow5_mod_pow2((uint32_t)tid, MASK);
@@ -140,7 +151,7 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   // this encode overwrites: the loads and the FFT above overlapped it, the stores wait.
   pdl_trigger();
   pdl_wait();
-  encode_real_post<LOGM, WIDE, THREADS>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf);
+  encode_real_post<LOGM, WIDE, THREADS>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf, sptw);
 }
 
 // Shared memory bytes of the lighter encode role of the persistent pipeline
@@ -182,7 +193,7 @@ ZINC_DEV void encode_real_lite_body(const EncodeArgs &a, size_t b, size_t b_out,
   encode_fft<LH, THREADS, NPASS, false>(a.fft_tw_h, lds, sts);
   __syncthreads();
   before_store();
-  encode_real_post<LOGM, false>(a, a.m_out + b_out * (2 * M), buf);
+  encode_real_post<LOGM, false, THREADS, false>(a, a.m_out + b_out * (2 * M), buf, a.post_tw);
 }
 
 }  // namespace zinc
