@@ -28,25 +28,21 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
   extern __shared__ __align__(16) uint64_t sm[];
   uint8_t *su = reinterpret_cast<uint8_t *>(sm + SmemWords<G::LOGL>::value);
   int8_t *se1 = reinterpret_cast<int8_t *>(su + N / 4), *se2 = se1 + N;
-  constexpr bool STW = !G::SPLIT;  // early passes read shared-memory copies of W[0, kSmemTw)
-  Tw *stw = reinterpret_cast<Tw *>(se2 + N), *sitw = stw + kSmemTw;  // sitw: COEFF form only
-  __shared__ __align__(8) uint64_t tw_mbar[2];
-  TwStager tws{&tw_mbar[0], 0}, itws{&tw_mbar[1], 0};
+  // early forward passes read shared-memory copies of W[0, kSmemTw); the inverse twiddles stay
+  // in L1/L2: staging them too (16 KiB more) would cost the COEFF form a CTA per SM at N <= 2^13
+  constexpr bool STW = !G::SPLIT;
+  Tw *stw = reinterpret_cast<Tw *>(se2 + N);
+  __shared__ __align__(8) uint64_t tw_mbar;
+  TwStager tws{&tw_mbar, 0};
   const size_t b = blockIdx.x / G::CLUSTER;
   const int loff = local_off<LOGN, LM>();
   const uint64_t msg = a.msg_base + b;
   const int L = a.L;
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
-  if constexpr (STW) {
-    tws.init();
-    if (FORM == 1) itws.init();
-  }
+  if constexpr (STW) tws.init();
   __syncthreads();
-  if constexpr (STW) {
-    tws.issue(stw, a.tw + (size_t)lo * N);
-    if (FORM == 1) itws.issue(sitw, a.itw + (size_t)lo * N);
-  }
+  if constexpr (STW) tws.issue(stw, a.tw + (size_t)lo * N);
   sample_ternary_packed<THREADS>(su, N, a.seed, msg, TAG_ENC_U);
   sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1);
   sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2);
@@ -94,7 +90,6 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
       __syncthreads();
       if constexpr (STW) {
         if (i + 1 < hi) tws.issue(stw, tw + N);
-        itws.wait();
       }
       stream_pairs<LOGN, 2, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
         const uint64_t u0 = canon(v0), u1 = canon(v1);
@@ -104,7 +99,7 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
         sm[pad16(x - loff + 1)] = mul_mod(p1.y, u1, c);
       });
       const Tw *itw = a.itw + (size_t)i * N;
-      ntt_inverse<LOGN, STW, LM>(sm, itw, c,
+      ntt_inverse<LOGN, false, LM>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
@@ -112,21 +107,15 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
           [&](int x, uint64_t v) {
             uint64_t e = pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c);
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
-          }, sitw);
+          }, nullptr);
       __syncthreads();  // the inverse's last stores may still read sm (split exchange) -- and ct1 temp visibility
       load_share<LOGN, 4, LM>(sm, ct1);
-      ntt_inverse<LOGN, STW, LM>(sm, itw, c,
+      ntt_inverse<LOGN, false, LM>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
-          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[x], c), q)); }, sitw);
-      if constexpr (STW) {
-        if (i + 1 < hi) {
-          __syncthreads();  // every thread is past the inverse's smem-twiddle passes
-          itws.issue(sitw, itw + N);
-        }
-      }
+          [&](int x, uint64_t v) { __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[x], c), q)); }, nullptr);
     }
   }
 }
@@ -199,7 +188,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
 template <int LOGN, int F>
 static size_t vanilla_smem() {
   using G = Geo<LOGN, vanilla_lm<F>()>;
-  const size_t twb = G::SPLIT ? 0 : (size_t)(F == 0 ? 1 : 2) * kSmemTw * sizeof(Tw);
+  const size_t twb = G::SPLIT ? 0 : (size_t)kSmemTw * sizeof(Tw);
   return ntt_smem_bytes<LOGN, vanilla_lm<F>()>() + (1 << LOGN) / 4 + 2 * (1 << LOGN) + twb;
 }
 

@@ -50,9 +50,8 @@ ZINC_DEV void sample_ternary_parity(uint8_t *dst, int n, uint64_t seed, uint64_t
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint4 w = stream_block(seed, msg, tag, 0, 2 * blk2 + h);
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-      packed |= (uint32_t)(tern(ws[r]) + 1) << (4 * h);
-      packed |= (uint32_t)(tern(ws[2 + r]) + 1) << (4 * h + 2);
+      packed |= (uint32_t)(tern(r ? w.y : w.x) + 1) << (4 * h);  // selects, not a local array
+      packed |= (uint32_t)(tern(r ? w.w : w.z) + 1) << (4 * h + 2);
     }
     dst[blk2] = (uint8_t)packed;
   }
