@@ -273,10 +273,13 @@ void zinc_launch_count_reset(void);
  *                                 passes; 1: 3 CTAs/SM, radix-16; 2: 2 CTAs/SM, radix-16
  *  ZINC_TUNE_L2_PREFETCH          1 (default): in the serial chunk pipeline, each Zinc COEFF launch
  *                                 prefetches the next chunk's slots into L2 for its encode; 0: off
+ *  ZINC_TUNE_ENCODE_LITE          real-slot encode variant: 1 (default) the 68 KiB shared-memory encode
+ *                                 on the side stream (OVERLAP = 1) only; 2 everywhere; 0 never
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_OVERLAP = 2,
        ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_PDL = 4, ZINC_TUNE_PIPE_ENC_CTAS = 5, ZINC_TUNE_PIPE_VARIANT = 6,
-       ZINC_TUNE_L2_PREFETCH = 7, ZINC_TUNE_COUNT = 8 };
+       ZINC_TUNE_L2_PREFETCH = 7, ZINC_TUNE_ENCODE_LITE = 8,
+       ZINC_TUNE_COUNT = 9 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

@@ -24,7 +24,7 @@ __all__ = [
     "zinc_keygen", "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch",
     "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
     "zinc_debug_sample", "zinc_int_peak", "zinc_ct_add_batch", "zinc_ct_sum_batch", "zinc_encrypt_batch_host", "launch_count",
-    "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_OVERLAP", "TUNE_COEFF_SMEM_PAD", "TUNE_PDL", "TUNE_PIPE_ENC_CTAS", "TUNE_PIPE_VARIANT", "TUNE_L2_PREFETCH", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
+    "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_OVERLAP", "TUNE_COEFF_SMEM_PAD", "TUNE_PDL", "TUNE_PIPE_ENC_CTAS", "TUNE_PIPE_VARIANT", "TUNE_L2_PREFETCH", "TUNE_ENCODE_LITE", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
 ]
 
 NTT, COEFF = 0, 1
@@ -349,7 +349,7 @@ def profile_read() -> dict:
 
 
 TUNE_COEFF_MSGS_PER_CTA, TUNE_ENCODE_CHUNK_BYTES, TUNE_OVERLAP, TUNE_COEFF_SMEM_PAD, TUNE_PDL = 0, 1, 2, 3, 4
-TUNE_PIPE_ENC_CTAS, TUNE_PIPE_VARIANT, TUNE_L2_PREFETCH = 5, 6, 7
+TUNE_PIPE_ENC_CTAS, TUNE_PIPE_VARIANT, TUNE_L2_PREFETCH, TUNE_ENCODE_LITE = 5, 6, 7, 8
 
 
 def tune(knob: int, value: int) -> int:

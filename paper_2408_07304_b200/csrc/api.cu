@@ -100,7 +100,7 @@ struct TraceScope {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}, {1}, {0}, {1}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}, {1}, {0}, {1}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -502,9 +502,10 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
 }
 
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
-                               cudaStream_t s, bool wide = false) {
+                               cudaStream_t s, bool wide = false, bool lite = false) {
   EncodeArgs a = encode_args(c, kind, slots, m);
   a.wide = wide ? 1 : 0;
+  a.lite = (lite || g_tune[ZINC_TUNE_ENCODE_LITE].load() == 2) ? 1 : 0;
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
@@ -759,7 +760,9 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
     const size_t cnt = std::min(chunk, batch - off);
     int64_t *mb = m + (size_t)buf * chunk * c->n;
     if (k >= 2 && (ce = cudaStreamWaitEvent(c->side, ev_use[buf], 0)) != cudaSuccess) break;  // chunk k-2 read mb
-    if ((st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, c->side)) != ZINC_OK) break;
+    // the light encode fits beside two streaming CTAs per SM (with ZINC_TUNE_COEFF_SMEM_PAD)
+    const bool lite = g_tune[ZINC_TUNE_ENCODE_LITE].load() != 0;
+    if ((st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, c->side, false, lite)) != ZINC_OK) break;
     if ((ce = cudaEventRecord(ev_enc[buf], c->side)) != cudaSuccess) break;
     if ((ce = cudaStreamWaitEvent(s, ev_enc[buf], 0)) != cudaSuccess) break;
     if ((st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true))) break;

@@ -320,7 +320,7 @@ def test_int_peak_kernel_runs(Z, orc):
 
 @pytest.mark.parametrize("knobs", [{0: 1, 1: 1 << 20, 2: 1, 3: 0}, {0: 7, 1: 3 << 20, 2: 0, 3: 12 << 10},
                                    {0: 2, 1: 1 << 20, 2: 1, 3: 12 << 10}, {0: 3, 1: 1 << 20, 2: 0, 4: 0, 7: 0},
-                                   {0: 2, 1: 2 << 20, 2: 2, 4: 1}])
+                                   {0: 2, 1: 2 << 20, 2: 2, 4: 1}, {8: 2}, {2: 1, 3: 12 << 10, 8: 1}])
 def test_tuning_knobs_never_change_results(Z, orc, knobs):
     """Launch geometry (messages per CTA, encode chunk, side-stream / fused overlap, smem
     reservation, programmatic dependent launch) changes timing only: ciphertexts stay
