@@ -371,6 +371,47 @@ def test_persistent_pipeline_bit_exact(Z, orc, name, batch, ring, enc, mpc, vari
     assert np.array_equal(got[-1].cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_persistent_pipeline_falls_back_where_unsupported(Z, orc, name):
+    """With ZINC_TUNE_OVERLAP = 3, calls the persistent kernel does not cover (complex slots,
+    int64 plaintexts, NTT form, the vanilla path, the host-buffer call's chunks) give the
+    default path's ciphertexts."""
+    s = setup_for(Z, orc, name)
+    z = slots_batch(s.cfg, 0, 9)
+    if s.cfg.complex_slots:
+        z = np.stack([z.real, z.imag], axis=-1)
+    z = torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    m = Z.ckks_encode_batch(s.ctx, z)
+    calls = [lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 4, 7),
+             lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, m, 4, 7),
+             lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, z, 4, 7),
+             lambda: Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, z[:3], 4, 7)]
+    ref = [f() for f in calls]
+    old = Z.tune(Z.TUNE_OVERLAP, 3)
+    try:
+        got = [f() for f in calls]
+        torch.cuda.synchronize()
+    finally:
+        Z.tune(Z.TUNE_OVERLAP, old)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+
+
+def test_persistent_pipeline_through_host_call(Z, orc):
+    """The host-buffer call (pinned in/out, two streams) with the persistent kernel per chunk
+    gives the device call's ciphertexts (ragged last chunk)."""
+    s = setup_for(Z, orc, "C3")
+    zh = torch.from_numpy(np.ascontiguousarray(slots_batch(s.cfg, 0, 21))).pin_memory()
+    ref = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, zh.cuda(), 6, 50).cpu()
+    out = torch.empty(ref.shape, dtype=torch.uint64).pin_memory()
+    old = Z.tune(Z.TUNE_OVERLAP, 3)
+    try:
+        Z.zinc_encrypt_batch_host(s.ctx, Z.PATH_ZINC, s.cache[COEFF], COEFF, zh, 6, 50, out, chunk=8)
+    finally:
+        Z.tune(Z.TUNE_OVERLAP, old)
+    assert torch.equal(ref, out)
+
+
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
 def test_ct_add_and_sum_bit_exact_and_decrypt(Z, orc, name):
     """Eq. 2 kernels: batched (+) and aggregation bit-exact against
