@@ -133,6 +133,19 @@ ZINC_DEV uint64_t pt_plus_e(int64_t m, int e, const LimbConst &c) {
   return reduce_i64q((int64_t)mt + (int64_t)c.t * e, c.q, c.mu64);
 }
 // Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).
+// The plaintext-plus-error input of the first forward transform as a two-phase load
+// (ntt.cuh TwoPhase): fetch(x) reads m[x] from global memory, lift(raw, x) adds the sample
+// (stored at x >> SHIFT: 1 for parity-split sample buffers) and reduces.
+template <bool INTS, int SHIFT = 0>
+struct PtLoad {
+  const int64_t *m;
+  const int8_t *se1;
+  const LimbConst &c;
+  ZINC_DEV int64_t fetch(int x) const { return m ? m[x] : 0; }
+  ZINC_DEV uint64_t lift(int64_t raw, int x) const { return pt_plus_e<INTS>(raw, se1[x >> SHIFT], c); }
+  ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
+};
+
 template <bool INTS = true>
 ZINC_DEV uint64_t err_term(int e, const LimbConst &c) {
   return (INTS && c.scheme == SCHEME_BGV) ? reduce_i64q((int64_t)c.t * e, c.q, c.mu64) : reduce_small(e, c.q);

@@ -68,14 +68,13 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
     tws.wait();
     if constexpr (G::DIT) {
       // sample of coefficient x = 2 i' + r sits at i' = x >> 1
-      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x >> 1], c); },
-                                      out0, stw);
+      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c}, out0, stw);
       ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); }, out1, stw,
                                       [&]() {
                                         if (i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
                                       });
     } else {
-      ntt_forward<LOGN, true, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
+      ntt_forward<LOGN, true, NR>(sm, tw, q, PtLoad<INTS>{m, se1, c},
                                   to_smem<LOGN>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN>(sm, out0);

@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
     if constexpr (STW) tws.wait();
     auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
     if (FORM == 0) {
-      ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c); },
+      ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, PtLoad<INTS>{m, se1, c},
                              to_smem<LOGN, LM>(sm), stw);
       __syncthreads();
       stream_pairs<LOGN, 4, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
     auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
     tws.wait();
     // sample of coefficient x = 2 i' + r sits at i' = x >> 1
-    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return pt_plus_e<INTS>(m ? m[x] : 0, se1[x >> 1], c); },
+    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c},
                                      [&](int x, uint64_t v0, uint64_t v1) { st2(ct0 + x, canon(v0), canon(v1)); }, stw);
     ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); },
                                      [&](int x, uint64_t v0, uint64_t v1) { st2(ct1 + x, canon(v0), canon(v1)); }, stw);

@@ -33,6 +33,12 @@ ZINC_DEV int pad16(int i) { return i + (i >> 4); }
 template <int LOGN>
 struct SmemWords { static constexpr int value = (1 << LOGN) + ((1 << LOGN) >> 4); };
 
+// A two-phase load (`fetch(idx)` -> raw int64 from global memory, `lift(raw, idx)` -> the
+// residue) lets a pass issue all of its group's global loads before the first lift, so
+// their latencies overlap instead of each one stalling the lift that consumes it.
+template <class L, class = void> struct TwoPhase { static constexpr bool value = false; };
+template <class L> struct TwoPhase<L, decltype((void)&L::fetch)> { static constexpr bool value = true; };
+
 // ---------------------------------------------------------------- forward pass
 // Load(idx) -> uint64 in [0, 4q); Store(idx, v) with v in [0, 4q).  With
 // GROUPED, Store is called once per group as store(base, v) with the 2^K words
@@ -52,8 +58,16 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
     const int beta = g / T, o = g % T;
     const int base = beta * (T << K) + o;
     uint64_t v[G];
+    if constexpr (TwoPhase<Load>::value) {
+      int64_t raw[G];
 #pragma unroll
-    for (int r = 0; r < G; ++r) v[r] = load(base + r * T);
+      for (int r = 0; r < G; ++r) raw[r] = load.fetch(base + r * T);
+#pragma unroll
+      for (int r = 0; r < G; ++r) v[r] = load.lift(raw[r], base + r * T);
+    } else {
+#pragma unroll
+      for (int r = 0; r < G; ++r) v[r] = load(base + r * T);
+    }
 #pragma unroll
     for (int l = 0; l < K; ++l) {
       const int D = G >> (l + 1);
@@ -255,8 +269,18 @@ ZINC_DEV void ntt_forward_dit2(uint64_t *sm, const Tw *tw, uint64_t q, Load load
   auto sld = [&](int i) { return sm[pad16(i)]; };
   const int r = (int)cluster_rank();
   __syncthreads();
-  ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, [&](int i) { return load(2 * i + r); },
-                                                     sst);
+  if constexpr (TwoPhase<Load>::value) {
+    struct Parity {  // local index i -> coefficient 2 i + r
+      const Load &l;
+      int r;
+      ZINC_DEV int64_t fetch(int i) const { return l.fetch(2 * i + r); }
+      ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, 2 * i + r); }
+    };
+    ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, Parity{load, r}, sst);
+  } else {
+    ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, [&](int i) { return load(2 * i + r); },
+                                                       sst);
+  }
   __syncthreads();
   ct_pass<LL, SB, P::KB, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, sld, sst);
   __syncthreads();
