@@ -68,12 +68,22 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
 #pragma unroll
       for (int r = 0; r < G; ++r) v[r] = load(base + r * T);
     }
+    // global-memory twiddles of this group: all 2^K - 1 issued before the first butterfly
+    constexpr bool PRE = !SMEM_TW && K <= 4;
+    Tw wpre[PRE ? G - 1 : 1];
+    if constexpr (PRE) {
+#pragma unroll
+      for (int l = 0; l < K; ++l)
+#pragma unroll
+        for (int blk = 0; blk < (1 << l); ++blk) wpre[(1 << l) - 1 + blk] = ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
+    }
 #pragma unroll
     for (int l = 0; l < K; ++l) {
       const int D = G >> (l + 1);
 #pragma unroll
       for (int blk = 0; blk < (1 << l); ++blk) {
-        const Tw w = SMEM_TW ? tw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
+        const Tw w = PRE ? wpre[(1 << l) - 1 + blk]
+                         : SMEM_TW ? tw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           if constexpr (NR) ct_bfly_nr(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
