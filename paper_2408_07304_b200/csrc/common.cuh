@@ -151,6 +151,22 @@ ZINC_DEV uint64_t err_term(int e, const LimbConst &c) {
   return (INTS && c.scheme == SCHEME_BGV) ? reduce_i64q((int64_t)c.t * e, c.q, c.mu64) : reduce_small(e, c.q);
 }
 
+// Input of either Zinc NTT-form transform as one two-phase load, so both transforms run
+// through one copy of the transform code: t = 0 gives m + e1' (fetching m), t = 1 gives
+// e2' (no global load).  Samples are parity-split (stored at x >> 1).
+template <bool INTS>
+struct ZincTLoad {
+  const int64_t *m;
+  const int8_t *se;
+  const LimbConst &c;
+  int t;
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? m[x] : 0; }
+  ZINC_DEV uint64_t lift(int64_t raw, int x) const {
+    return t == 0 ? pt_plus_e<INTS>(raw, se[x >> 1], c) : err_term<INTS>(se[x >> 1], c);
+  }
+  ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
+};
+
 // Forward Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> [0, 4q).
 ZINC_DEV void ct_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
   uint64_t x = csub(X, two_q);

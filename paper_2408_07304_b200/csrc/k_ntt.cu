@@ -67,12 +67,21 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
     };
     tws.wait();
     if constexpr (G::DIT) {
-      // sample of coefficient x = 2 i' + r sits at i' = x >> 1
-      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c}, out0, stw);
-      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); }, out1, stw,
-                                      [&]() {
-                                        if (i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
-                                      });
+      // both transforms through one copy of the transform code (the kernel is instruction-
+      // fetch bound otherwise); sample of coefficient x = 2 i' + r sits at i' = x >> 1
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {
+        const uint64_t *z = t ? z2 : z1;
+        uint64_t *ctt = t ? ct1 : ct0;
+        ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, ZincTLoad<INTS>{m, t ? se2 : se1, c, t},
+            [&](int x, uint64_t v0, uint64_t v1) {
+              const ulonglong2 zz = ld2_nc(z + x);
+              st2_cs(ctt + x, add_mod(zz.x, canon(v0), q), add_mod(zz.y, canon(v1), q));
+            },
+            stw, [&]() {
+              if (t == 1 && i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
+            });
+      }
     } else {
       ntt_forward<LOGN, true, NR>(sm, tw, q, PtLoad<INTS>{m, se1, c},
                                   to_smem<LOGN>(sm), stw);
