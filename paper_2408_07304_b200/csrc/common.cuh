@@ -153,8 +153,8 @@ ZINC_DEV uint64_t err_term(int e, const LimbConst &c) {
 
 // Input of either Zinc NTT-form transform as one two-phase load, so both transforms run
 // through one copy of the transform code: t = 0 gives m + e1' (fetching m), t = 1 gives
-// e2' (no global load).  Samples are parity-split (stored at x >> 1).
-template <bool INTS>
+// e2' (no global load).  Samples are stored at x >> SHIFT (1: parity-split buffers).
+template <bool INTS, int SHIFT = 1>
 struct ZincTLoad {
   const int64_t *m;
   const int8_t *se;
@@ -162,7 +162,7 @@ struct ZincTLoad {
   int t;
   ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? m[x] : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
-    return t == 0 ? pt_plus_e<INTS>(raw, se[x >> 1], c) : err_term<INTS>(se[x >> 1], c);
+    return t == 0 ? pt_plus_e<INTS>(raw, se[x >> SHIFT], c) : err_term<INTS>(se[x >> SHIFT], c);
   }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
 };

@@ -57,14 +57,6 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
-    auto out0 = [&](int x, uint64_t v0, uint64_t v1) {
-      const ulonglong2 z = ld2_nc(z1 + x);
-      st2_cs(ct0 + x, add_mod(z.x, canon(v0), q), add_mod(z.y, canon(v1), q));
-    };
-    auto out1 = [&](int x, uint64_t v0, uint64_t v1) {
-      const ulonglong2 z = ld2_nc(z2 + x);
-      st2_cs(ct1 + x, add_mod(z.x, canon(v0), q), add_mod(z.y, canon(v1), q));
-    };
     tws.wait();
     if constexpr (G::DIT) {
       // both transforms through one copy of the transform code (the kernel is instruction-
@@ -83,14 +75,28 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
             });
       }
     } else {
-      ntt_forward<LOGN, true, NR>(sm, tw, q, PtLoad<INTS>{m, se1, c},
-                                  to_smem<LOGN>(sm), stw);
-      __syncthreads();
-      stream_pairs<LOGN>(sm, out0);
-      ntt_forward<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
-      __syncthreads();
-      if (i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
-      stream_pairs<LOGN>(sm, out1);
+      // one copy of the transform code for both transforms at N = 2^13 (+6 %); at 2^12 the
+      // 80-register budget favours two specialised copies (measured)
+      constexpr bool ONE = LOGN >= 13;
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t) {
+        const uint64_t *z = t ? z2 : z1;
+        uint64_t *ctt = t ? ct1 : ct0;
+        auto out = [&](int x, uint64_t v0, uint64_t v1) {
+          const ulonglong2 zz = ld2_nc(z + x);
+          st2_cs(ctt + x, add_mod(zz.x, canon(v0), q), add_mod(zz.y, canon(v1), q));
+        };
+        if constexpr (ONE) {
+          ntt_forward<LOGN, true, NR>(sm, tw, q, ZincTLoad<INTS, 0>{m, t ? se2 : se1, c, t}, to_smem<LOGN>(sm), stw);
+        } else if (t == 0) {
+          ntt_forward<LOGN, true, NR>(sm, tw, q, PtLoad<INTS>{m, se1, c}, to_smem<LOGN>(sm), stw);
+        } else {
+          ntt_forward<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x], c); }, to_smem<LOGN>(sm), stw);
+        }
+        __syncthreads();
+        if (t == 1 && i + 1 < hi) tws.issue(stw, tw + N);  // next limb's table lands during this epilogue
+        stream_pairs<LOGN>(sm, out);
+      }
     }
   }
 }
