@@ -174,12 +174,15 @@ ZINC_DEV void ct_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_
   X = x + t;
   Y = x - t + two_q;
 }
-// Inverse Gentleman-Sande butterfly, lazy: X, Y in [0, 2q) -> [0, 2q).
-ZINC_DEV void gs_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
-  uint64_t s = csub(X + Y, two_q);
-  uint64_t d = X - Y + two_q;
-  Y = mul_shoup_lazy(d, w, wp, q);
-  X = s;
+// Inverse Gentleman-Sande butterfly, lazy: X, Y in [0, 4q) -> [0, 4q) (every q < 2^60 here,
+// so 8q < 2^64).  The sum comes back below 4q with one conditional subtraction; the product
+// uses the 3-partial-product Shoup quotient (umulhi_approx below: w d mod q plus at most 3q).
+ZINC_DEV uint64_t umulhi_approx(uint64_t a, uint64_t b);
+ZINC_DEV void gs_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t four_q) {
+  const uint64_t s = X + Y;
+  const uint64_t d = X - Y + four_q;
+  Y = w * d - umulhi_approx(wp, d) * q;
+  X = s >= four_q ? s - four_q : s;
 }
 // [0, 4q) -> [0, q)
 ZINC_DEV uint64_t canon4(uint64_t x, uint64_t q, uint64_t two_q) { return csub(csub(x, two_q), q); }

@@ -101,7 +101,7 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
 }
 
 // ---------------------------------------------------------------- inverse pass
-// Load -> [0, 2q); Store gets [0, 2q).  When LAST (S0 == 0), stage 0 multiplies
+// Load -> [0, 4q); intermediate values stay in [0, 4q); Store gets [0, 2q) after the folded last stage (FOLD), [0, 4q) otherwise.  When LAST (S0 == 0), stage 0 multiplies
 // the sum by N^-1 and the difference by N^-1 psi^-brv(1) (folded scaling).
 // With GROUPED, Load is called once per group as load(base, v).
 template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool FOLD = true, bool SMEM_TW = false,
@@ -111,7 +111,7 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Lo
   constexpr int G = 1 << K;
   constexpr int T = N >> (S0 + K);
   constexpr int NGROUPS = N / G;
-  const uint64_t q = c.q, two_q = c.two_q;
+  const uint64_t q = c.q, four_q = 2 * c.two_q;
 #pragma unroll 1
   for (int g = threadIdx.x; g < NGROUPS; g += THREADS) {
     const int beta = g / T, o = g % T;
@@ -131,8 +131,8 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Lo
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           uint64_t X = v[j], Y = v[j + D];
-          uint64_t s = X + Y;                 // [0, 4q)
-          uint64_t d = X - Y + two_q;         // (0, 4q)
+          uint64_t s = X + Y;                 // [0, 8q)
+          uint64_t d = X - Y + four_q;        // (0, 8q)
           v[j] = mul_shoup_lazy(s, c.ninv, c.ninv_sh, q);
           v[j + D] = mul_shoup_lazy(d, c.ninv_w, c.ninv_w_sh, q);
         }
@@ -141,7 +141,7 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Lo
         for (int blk = 0; blk < (1 << l); ++blk) {
           const Tw w = SMEM_TW ? itw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(itw + (tb << (S0 + l)) + (beta << l) + blk);
 #pragma unroll
-          for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
+          for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, four_q);
         }
       }
     }
@@ -359,13 +359,13 @@ ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad
     gs_pass<LL, 0, P::KA, P::THREADS, false, false>(itw, c, tb, sld, sst);
     cluster_sync_all();  // both halves complete and every input consumed
     const uint64_t *h0 = peer_smem(sm, 0), *h1 = peer_smem(sm, 1);
-    const uint64_t two_q = c.two_q, q = c.q;
+    const uint64_t four_q = 2 * c.two_q, q = c.q;
     constexpr int QN = G::NL / 2;
 #pragma unroll 2
     for (int j = r * QN + threadIdx.x; j < (r + 1) * QN; j += P::THREADS) {
-      const uint64_t X = h0[pad16(j)], Y = h1[pad16(j)];
+      const uint64_t X = h0[pad16(j)], Y = h1[pad16(j)];  // [0, 4q)
       store(j, mul_shoup_lazy(X + Y, c.ninv, c.ninv_sh, q));
-      store(j + G::NL, mul_shoup_lazy(X - Y + two_q, c.ninv_w, c.ninv_w_sh, q));
+      store(j + G::NL, mul_shoup_lazy(X - Y + four_q, c.ninv_w, c.ninv_w_sh, q));
     }
     cluster_sync_all();  // the partner finished reading this CTA's buffer
   }
