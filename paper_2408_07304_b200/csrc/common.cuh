@@ -141,7 +141,7 @@ struct PtLoad {
   const int64_t *m;
   const int8_t *se1;
   const LimbConst &c;
-  ZINC_DEV int64_t fetch(int x) const { return m ? m[x] : 0; }
+  ZINC_DEV int64_t fetch(int x) const { return m ? __ldg(m + x) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const { return pt_plus_e<INTS>(raw, se1[x >> SHIFT], c); }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
 };
@@ -160,7 +160,7 @@ struct ZincTLoad {
   const int8_t *se;
   const LimbConst &c;
   int t;
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? m[x] : 0; }
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? __ldg(m + x) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     return t == 0 ? pt_plus_e<INTS>(raw, se[x >> SHIFT], c) : err_term<INTS>(se[x >> SHIFT], c);
   }

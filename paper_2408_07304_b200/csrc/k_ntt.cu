@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) d
     const Tw *itw = a.itw + (size_t)i * N;
     auto epilogue = [&](int x, uint64_t v) {
       uint64_t xi = csub(v, q);
-      if (FORM == 1) xi = add_mod(xi, c1[x], q);
+      if (FORM == 1) xi = add_mod(xi, __ldg(c1 + x), q);  // read-only: may be hoisted above the stores
       if (c.scheme == SCHEME_BFV) {
         a.xl_out[(b * L + i) * N + x] = xi;
         return;
@@ -205,15 +205,16 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) d
       ntt_inverse<LOGN, false, 13>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[r] = add_mod(c1[base + r], mul_mod(c2[base + r], s[base + r], c), q);
+            for (int r = 0; r < 16; ++r)
+              v[r] = add_mod(__ldg(c1 + base + r), mul_mod(__ldg(c2 + base + r), __ldg(s + base + r), c), q);
           },
           epilogue);
     } else {
       const Tw *tw = a.tw + (size_t)i * N;
-      ntt_forward<LOGN, false, false, 13>(sm, tw, q, [&](int x) { return c2[x]; },
+      ntt_forward<LOGN, false, false, 13>(sm, tw, q, [&](int x) { return __ldg(c2 + x); },
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon4(v[r], q, two_q), s[base + r], c);
+            for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon4(v[r], q, two_q), __ldg(s + base + r), c);
           });
       ntt_inverse<LOGN, false, 13>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
             for (int r = 0; r < 16; ++r) v[r] = sm[pad16(base - loff + r)];
           },
           [&](int x, uint64_t v) {
-            uint64_t e = pt_plus_e<INTS>(m ? m[x] : 0, se1[x], c);
+            uint64_t e = pt_plus_e<INTS>(m ? __ldg(m + x) : 0, se1[x], c);  // read-only: hoistable above the stores
             __stcs(ct0 + x, add_mod(csub(v, q), e, q));
           }, nullptr);
       __syncthreads();  // the inverse's last stores may still read sm (split exchange) -- and ct1 temp visibility
