@@ -186,12 +186,23 @@ ZINC_DEV void gs_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_
 }
 // [0, 4q) -> [0, q)
 ZINC_DEV uint64_t canon4(uint64_t x, uint64_t q, uint64_t two_q) { return csub(csub(x, two_q), q); }
+// [0, 8q) -> [0, q): outputs of the forward transforms with conditional subtractions
+ZINC_DEV uint64_t canon8(uint64_t x, uint64_t q, uint64_t two_q) { return canon4(csub(x, 2 * two_q), q, two_q); }
 // High word of a 64 x 64-bit product from three 32-bit partial products (a_hi b_hi exact, the
 // cross terms' high halves; the low x low product and the cross terms' low halves dropped):
 // exact - 2 <= result <= exact.
 ZINC_DEV uint64_t umulhi_approx(uint64_t a, uint64_t b) {
   const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32), bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
   return (uint64_t)ah * bh + __umulhi(al, bh) + __umulhi(ah, bl);
+}
+// Forward butterfly for moduli up to 2^60 (no lazy-free headroom): X, Y in [0, 8q) -> [0, 8q)
+// with one conditional subtraction and the 3-partial-product Shoup quotient (T < 4q).
+ZINC_DEV uint64_t umulhi_approx(uint64_t a, uint64_t b);
+ZINC_DEV void ct_bfly_a(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t four_q) {
+  const uint64_t x = csub(X, four_q);
+  const uint64_t t = w * Y - umulhi_approx(wp, Y) * q;
+  X = x + t;
+  Y = x - t + four_q;
 }
 // Forward butterfly without the conditional subtraction and with the cheaper Shoup quotient:
 // T = w Y - umulhi_approx(w', Y) q is w Y mod q plus at most 3q (the quotient is at most 2

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
     const uint64_t *z1 = a.cache + (size_t)i * N, *z2 = a.cache + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
     tws.wait();
     if constexpr (G::DIT) {
       // both transforms through one copy of the transform code (the kernel is instruction-
@@ -126,19 +126,19 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MINB) keygen_ke
   ntt_forward<LOGN>(sm, tw, q, [&](int x) { return uniform_mod(stream_block(a.seed, 0, TAG_PK_A, i, x), q); },
       [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) pk2[base + r] = canon4(v[r], q, two_q);
+        for (int r = 0; r < 16; ++r) pk2[base + r] = canon8(v[r], q, two_q);
       });
   ntt_forward<LOGN>(sm, tw, q, [&](int x) { return reduce_small(ss[x], q); },
       [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) sk[base + r] = canon4(v[r], q, two_q);
+        for (int r = 0; r < 16; ++r) sk[base + r] = canon8(v[r], q, two_q);
       });
   ntt_forward<LOGN>(sm, tw, q, [&](int x) { return err_term(se[x], c); },  // BGV: t e (reading A17)
       [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
           uint64_t as = mul_mod(pk2[base + r], sk[base + r], c);
-          pk1[base + r] = add_mod(q - as == q ? 0 : q - as, canon4(v[r], q, two_q), q);
+          pk1[base + r] = add_mod(q - as == q ? 0 : q - as, canon8(v[r], q, two_q), q);
         }
       });
 }
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) d
       ntt_forward<LOGN, false, false, 13>(sm, tw, q, [&](int x) { return __ldg(c2 + x); },
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon4(v[r], q, two_q), __ldg(s + base + r), c);
+            for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon8(v[r], q, two_q), __ldg(s + base + r), c);
           });
       ntt_inverse<LOGN, false, 13>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) n
     ntt_forward<LOGN, false, false, 13>(sm, a.tw + (size_t)i * N, q, [&](int x) { return p[x]; },
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-          for (int r = 0; r < 16; ++r) p[base + r] = canon4(v[r], q, two_q);
+          for (int r = 0; r < 16; ++r) p[base + r] = canon8(v[r], q, two_q);
         });
   } else {
     ntt_inverse<LOGN, false, 13>(sm, a.itw + (size_t)i * N, c,

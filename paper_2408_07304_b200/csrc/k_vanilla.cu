@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
     if (FORM == 0) {
       ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, PtLoad<INTS>{m, se1, c},
                              to_smem<LOGN, LM>(sm), stw);
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon4(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
     tws.wait();
     // sample of coefficient x = 2 i' + r sits at i' = x >> 1
     ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c},

@@ -40,7 +40,7 @@ template <class L, class = void> struct TwoPhase { static constexpr bool value =
 template <class L> struct TwoPhase<L, decltype((void)&L::fetch)> { static constexpr bool value = true; };
 
 // ---------------------------------------------------------------- forward pass
-// Load(idx) -> uint64 in [0, 4q); Store(idx, v) with v in [0, 4q).  With
+// Load(idx) -> uint64 in [0, 4q); Store(idx, v) with v in [0, 8q) (ct_bfly_a), or below 2^64 with NR.  With
 // GROUPED, Store is called once per group as store(base, v) with the 2^K words
 // of the group (T == 1: contiguous words base .. base + 2^K - 1).
 // SMEM_TW: `tw` points to a shared-memory copy of the table (the early passes'
@@ -87,7 +87,7 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
 #pragma unroll
         for (int j = 0; j < D; ++j) {
           if constexpr (NR) ct_bfly_nr(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
-          else ct_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, two_q);
+          else ct_bfly_a(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, 2 * two_q);
         }
       }
     }
@@ -318,7 +318,7 @@ ZINC_DEV void ntt_forward_dit2(uint64_t *sm, const Tw *tw, uint64_t q, Load load
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k = k0 + u * P::THREADS;
-      const uint64_t E = NR ? e[u] : csub(e[u], two_q);
+      const uint64_t E = NR ? e[u] : csub(csub(e[u], 2 * two_q), two_q);  // [0, 8q) -> [0, 2q)
       const uint64_t t = mul_shoup_lazy(o[u], w[u].x, w[u].y, q);
       pair(2 * k, E + t, E - t + two_q);
     }
