@@ -663,7 +663,8 @@ static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key
   const bool overlap = mode == 1 && batch > chunk;
   const int nbuf = (overlap || (fused && batch > chunk)) ? 2 : 1;
   // serial chunks chained with programmatic dependent launches (knob ZINC_TUNE_PDL) double-buffer
-  const bool pdl = !pipe && !overlap && !fused && g_tune[ZINC_TUNE_PDL].load() != 0 && kind == ZINC_PT_SLOTS_F64 &&
+  const bool pdl = !pipe && !overlap && !fused && g_tune[ZINC_TUNE_PDL].load() != 0 &&
+                   (kind == ZINC_PT_SLOTS_F64 || kind == ZINC_PT_SLOTS_C128) &&
                    path == PATH_ZINC && form == ZINC_FORM_COEFF;
   const int nb = (nbuf == 2 || (pdl && batch > chunk)) ? 2 : 1;
   ScratchBuf mbuf(s);

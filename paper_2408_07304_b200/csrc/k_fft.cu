@@ -52,6 +52,10 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   __syncthreads();
   fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
   __syncthreads();
+  // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
+  // this encode overwrites: the loads and the first passes overlapped it, the stores wait.
+  pdl_trigger();
+  pdl_wait();
   int64_t *m = a.m_out + b * (2 * M) * (a.wide ? 2 : 1);
   const double scale = a.scale;  // Delta / M, a power of two
   auto emit = [&](int j, double2 v) {

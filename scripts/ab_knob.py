@@ -1,5 +1,5 @@
 """A/B of one tuning knob on the slots -> Zinc COEFF path (C3 by default):
-python scripts/ab_knob.py KNOB V0 V1 [config].  Alternates the two values 4 times,
+python scripts/ab_knob.py KNOB V0 V1 [config] [batch].  Alternates the two values 4 times,
 median of 5 each, and checks the ciphertexts are identical.  Development tool."""
 import json
 import os
@@ -18,11 +18,12 @@ cfg = CONFIGS[sys.argv[4] if len(sys.argv) > 4 else "C3"]
 ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
 _, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
 cache = Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, Z.COEFF)
-z = slots_batch(cfg, 0, cfg.batch)
+B = int(sys.argv[5]) if len(sys.argv) > 5 else cfg.batch
+z = slots_batch(cfg, 0, B)
 if cfg.complex_slots:
     z = np.stack([z.real, z.imag], axis=-1)
 slots = torch.from_numpy(np.ascontiguousarray(z)).cuda()
-ct = ctx.empty_ct(cfg.batch)
+ct = ctx.empty_ct(B)
 res = {v0: [], v1: []}
 outs = {}
 for _ in range(4):
