@@ -114,6 +114,7 @@ struct zinc_ctx {
   LimbConst *d_limbs = nullptr;
   Tw *d_tw = nullptr, *d_itw = nullptr;
   double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr, *d_post_tw = nullptr;
+  double2 *d_twist_split = nullptr;
   int *d_perm = nullptr;
   // host-API pipeline buffers (grow-only, guarded)
   std::mutex host_mu;
@@ -277,6 +278,7 @@ zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
   cudaFree(ctx->d_fft_tw);
   cudaFree(ctx->d_twist);
   cudaFree(ctx->d_post_tw);
+  cudaFree(ctx->d_twist_split);
   cudaFree(ctx->d_fft_tw_h);
   cudaFree(ctx->d_perm);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -394,6 +396,16 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     long double ang = -pi * (long double)j / (long double)n;
     twist[j] = make_double2((double)cosl(ang), (double)sinl(ang));
   }
+  // complex-slot encode twist zeta^-j = A'[j / 64] B[j % 64], j < M = N/2
+  std::vector<double2> twist_split;
+  for (int x = 0; x < M / 64; ++x) {
+    long double ang = -pi * 64.0L * (long double)x / (long double)n;
+    twist_split.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+  }
+  for (int x = 0; x < 64; ++x) {
+    long double ang = -pi * (long double)x / (long double)n;
+    twist_split.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+  }
   // split tables of the real-slot encode's post step: t_j = e^{-i pi j/N} = A[j/64] B[j%64],
   // p_j = e^{-5 i pi j/N} = A5[j/64] B5[j%64], j < N/4
   const int na = (n / 4) / 64;
@@ -417,7 +429,8 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
   if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(ZINC_ECUDA, "cudaSetDevice(%d) failed", device); }
   if ((st = upload(&c->d_limbs, c->h_limbs)) || (st = upload(&c->d_tw, tw)) || (st = upload(&c->d_itw, itw)) ||
       (st = upload(&c->d_fft_tw, ftw)) || (st = upload(&c->d_twist, twist)) || (st = upload(&c->d_perm, perm)) ||
-      (st = upload(&c->d_fft_tw_h, ftw_h)) || (st = upload(&c->d_post_tw, post_tw))) {
+      (st = upload(&c->d_fft_tw_h, ftw_h)) || (st = upload(&c->d_post_tw, post_tw)) ||
+      (st = upload(&c->d_twist_split, twist_split))) {
     zinc_ctx_destroy(c);
     return st;
   }
@@ -496,6 +509,7 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
   a.twist = c->d_twist;
   a.fft_tw_h = c->d_fft_tw_h;
   a.post_tw = c->d_post_tw;
+  a.twist_split = c->d_twist_split;
   a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));
   a.m_out = m;
   return a;

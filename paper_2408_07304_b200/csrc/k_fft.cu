@@ -58,8 +58,10 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   pdl_wait();
   int64_t *m = a.m_out + b * (2 * M) * (a.wide ? 2 : 1);
   const double scale = a.scale;  // Delta / M, a power of two
+  // twist zeta^-j from two small L1-resident tables instead of 16 B of L2 table per output
+  const double2 *tA = a.twist_split, *tB = a.twist_split + M / 64;
   auto emit = [&](int j, double2 v) {
-    const double2 w = cmul(v, __ldg(a.twist + j));
+    const double2 w = cmul(v, cmul(__ldg(tA + (j >> 6)), __ldg(tB + (j & 63))));
     if (a.wide) {
       store_i128(m + 2 * j, w.x * scale);
       store_i128(m + 2 * (j + M), w.y * scale);

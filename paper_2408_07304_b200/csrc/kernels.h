@@ -108,6 +108,7 @@ struct EncodeArgs {
   const double2 *fft_tw, *twist;
   const double2 *fft_tw_h;  // W_{M/2}^e, e < M/4 (real-slot path)
   const double2 *post_tw;   // real-slot split step: [A | B | A5 | B5] (encode_real_post)
+  const double2 *twist_split;  // complex-slot twist zeta^-j = A'[j >> 6] B[j & 63], j < M: [A' | B]
   int wide;                 // m_out holds 128-bit coefficients (int64 pairs)
   int lite;                 // real slots: the 68 KiB shared-memory encode (twiddles through L1)
   double scale;
