@@ -30,7 +30,7 @@ def run(cfg, B, scheme=0, t=0):
             assert int(st.sum()) == 0
             Z.zinc_ct_sum_batch(ctx, Z.zinc_ct_add_batch(ctx, ct, ct))
     if scheme == 0:
-        for mode in (0, 1, 2):
+        for mode in (0, 1, 2, 3):
             Z.tune(Z.TUNE_OVERLAP, mode)
             Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, 1 << 16)
             Z.zinc_encrypt_batch(ctx, Z.zinc_precompute_cache(ctx, pk, 2, Z.COEFF), Z.COEFF, pt, 3, 0)
