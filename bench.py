@@ -67,17 +67,30 @@ def bytes_per_ct(cfg, kind="slots"):
     return ct + cfg.n * 8
 
 
-def alu_peak_derived(sm_mhz):
-    """The lazy Shoup butterfly as compiled (SASS of int_peak_kernel): 14.9 fma-pipe
-    (IMAD family) + 15.0 alu-pipe instructions, 30 issue slots.  Both pipes take 64 lanes/clk/SM
-    (B300_MICROARCH.md: rt_SMSP = 2) and issue is 128 lanes/clk/SM, so 15/64 clk per butterfly
-    per SM bounds it: 148 x f_sm x 64 / 15."""
-    return 148 * sm_mhz * 1e6 * 64.0 / 15.0
+# K11 butterfly variants (include/zinc.h zinc_int_peak) and their SASS mix as compiled
+# (scripts/sass_bfly.py on int_peak_kernel<V>, profiles/r02_k11_sass.txt): instructions per
+# butterfly, of which on the fma pipe (IMAD family, HFMA2 zeroing).
+BFLY = {0: ("ct_bfly", 29.625, 14.75), 1: ("ct_bfly_nr", 23.125, 14.125), 2: ("ct_bfly_a", 29.875, 14.5),
+        3: ("gs_bfly", 28.25, 14.125)}
+
+
+def alu_peak_derived(sm_mhz, fma_per_bfly):
+    """Issue-model bound of one butterfly variant: the fma pipe takes 64 lanes/clk/SM
+    (B300_MICROARCH.md: rt_SMSP = 2), so fma_per_bfly / 64 clk per butterfly per SM."""
+    return 148 * sm_mhz * 1e6 * 64.0 / fma_per_bfly
+
+
+def path_transforms(cfg, path):
+    """(forward, inverse) transforms per ciphertext of each transform path:
+    vanilla 3 L (NTT form: 3 forward; COEFF form: 1 forward + 2 inverse), Zinc NTT form 2 L
+    forward, decrypt (COEFF form) L forward + L inverse."""
+    return {"zinc_ntt": (2 * cfg.L, 0), "vanilla_ntt": (3 * cfg.L, 0), "vanilla_coeff": (cfg.L, 2 * cfg.L),
+            "decrypt_coeff": (cfg.L, cfg.L)}[path]
 
 
 def butterflies_per_ct(cfg, path):
-    half = cfg.n // 2 * cfg.log_n
-    return (3 if path.startswith("vanilla") else 2) * cfg.L * half
+    f, i = path_transforms(cfg, path)
+    return (f + i) * (cfg.n // 2 * cfg.log_n)
 
 
 # ---------------------------------------------------------------- clocks
@@ -437,36 +450,48 @@ def main():
         elif path == "vanilla_coeff":
             Z.ckks_encrypt_batch(ctx, pk, Z.COEFF, slots, cfg.enc_seed, base, out=ct)
 
-    # validity gate: every path's output decrypts within tolerance
+    # validity gate: every path's output, from the exact call the timed region
+    # makes, decrypts within tolerance with a consistent CRT, sampled at the first and last
+    # message of every 256-message block -- so every chunk of every chunk chain (Zinc COEFF:
+    # 256-message chunks; transform paths: 16-wave chunks) and both halves of C3's A13 mix
     validity = {}
-    probe = min(B, 64)
+    probe_idx = sorted(set([b for k in range(0, B, 256) for b in (k, min(B, k + 256) - 1)]))
+    pidx = torch.tensor(probe_idx, device=ctx.dev())
+    ref_all = slots_h[probe_idx, :, 0] + 1j * slots_h[probe_idx, :, 1] if cfg.complex_slots else slots_h[probe_idx]
     for p in paths:
         run(p)
         form = Z.COEFF if p.endswith("coeff") else Z.NTT
-        _, st, z = Z.ckks_decrypt_batch(ctx, sk, form, ct[:probe])
-        zz = z.cpu().numpy()
-        ref = slots_h[:probe, :, 0] + 1j * slots_h[:probe, :, 1] if cfg.complex_slots else slots_h[:probe]
-        err = float(np.max(np.abs(zz - ref)))
+        _, st, z = Z.ckks_decrypt_batch(ctx, sk, form, ct.index_select(0, pidx).contiguous())
+        err = float(np.max(np.abs(z.cpu().numpy() - ref_all)))
         ok = int(st.sum().item()) == 0 and err < cfg.tolerance()
-        validity[p] = {"crt_ok": int(st.sum().item()) == 0, "max_abs_err": err, "ok": ok}
+        validity[p] = {"crt_ok": int(st.sum().item()) == 0, "max_abs_err": err, "ok": ok,
+                       "tolerance": cfg.tolerance(), "sampled": len(probe_idx)}
         if not ok:
             log(f"validity gate failed for {p}: {validity[p]}")
             sys.exit(3)
+    validity["sampled_indices"] = probe_idx
 
     for _ in range(args.warmup):
         for p in paths:
             run(p)
     torch.cuda.synchronize()
 
-    # int-peak microkernel (K11): denominator for the integer-bound paths
+    # int-peak microkernel (K11) per butterfly variant: the denominators of the transform paths
     sink = torch.zeros(2, dtype=torch.uint64, device=ctx.dev())
-    Z.zinc_int_peak(ctx, 148 * 8, 200, sink)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    bf = Z.zinc_int_peak(ctx, 148 * 8, 4000, sink)
-    e1.record()
-    torch.cuda.synchronize()
-    int_peak = bf / (e0.elapsed_time(e1) / 1e3)
+    nr_ok = max(ctx.q) < (1 << 58)
+    k11 = {}
+    for v in ((1, 2, 3) if nr_ok else (2, 3)):
+        Z.zinc_int_peak(ctx, 148 * 8, 200, sink, variant=v)
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            bf = Z.zinc_int_peak(ctx, 148 * 8, 4000, sink, variant=v)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, bf / (e0.elapsed_time(e1) / 1e3))
+        k11[v] = best
+    fwd_v = 1 if nr_ok else 2  # the forward butterfly the CKKS transform kernels run at this modulus
 
     # ---------------- timed region
     ev = {p: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -491,12 +516,16 @@ def main():
     # Per-kernel device times come from one extra, untimed step with the library's launch
     # tracing on: its events sit between launches on the stream, which would break the
     # programmatic dependent launches of the slot pipeline inside the timed region.
-    Z.profile_enable(True)
+    prof, prof_path = {}, {}
     for p in paths:
+        Z.profile_enable(True)
         run(p)
-    torch.cuda.synchronize()
-    prof = {k: (v[0] * args.steps, v[1] * args.steps) for k, v in Z.profile_read().items()}
-    Z.profile_enable(False)
+        torch.cuda.synchronize()
+        prof_path[p] = Z.profile_read()
+        Z.profile_enable(False)
+        for k, v in prof_path[p].items():
+            a0, a1 = prof.get(k, (0.0, 0))
+            prof[k] = (a0 + v[0] * args.steps, a1 + v[1] * args.steps)
 
     seg = {p: sum(a.elapsed_time(b) for a, b in ev[p]) / args.steps for p in paths}  # ms per step per path
     seg = dict(zip(paths, max_over_ranks([seg[p] for p in paths], device=ctx.dev())))
@@ -528,21 +557,27 @@ def main():
                     roof["traffic"] = t["dram_bytes_per_msg"] * msgs_per_launch
                     roof["traffic_source"] = "profiles/ncu_traffic.json (ncu --set full, per message, scaled)"
         alu = {}
-        for p, kname in (("vanilla_ntt", "vanilla_kernel"), ("zinc_ntt", "zinc_ntt_kernel")):
-            if p in seg:
-                kms = prof.get(kname, (0.0, 0))[0]
-                ach = butterflies_per_ct(cfg, p) * B / (seg[p] / 1e3)
-                # the kernel serves every path of its family (vanilla: both forms) in the timed region
-                n_paths = sum(1 for q in paths if q.split("_")[0] == p.split("_")[0] and
-                              (q.startswith("vanilla") or q == p))
-                kach = butterflies_per_ct(cfg, p) * B * args.steps * n_paths / (kms / 1e3) if kms else ach
-                pd = alu_peak_derived(clk["sm_mhz"] or 1965.0)
-                alu[p] = {"bound": "alu", "kernel": kname, "achieved": kach / 1e9, "peak": int_peak / 1e9,
-                          "unit": "Gbutterfly/s", "frac": kach / int_peak, "achieved_path": ach / 1e9,
-                          "peak_derived": pd / 1e9, "frac_of_derived": kach / pd,
-                          "butterflies_per_ct": butterflies_per_ct(cfg, p),
-                          "peak_source": "measured int_peak_kernel (K11), lazy Shoup butterflies; peak_derived: "
-                                         "148 SMs x sm_mhz x 64 lanes/clk / 15 fma- or alu-pipe ops per butterfly"}
+        sm_mhz = clk["sm_mhz"] or 1965.0
+        for p, kname in (("zinc_ntt", "zinc_ntt_kernel"), ("vanilla_ntt", "vanilla_kernel"),
+                         ("vanilla_coeff", "vanilla_kernel")):
+            if p not in seg:
+                continue
+            nf, ni = path_transforms(cfg, p)
+            # the path's own peak: its forward and inverse butterflies at their K11 rates
+            peak_p = (nf + ni) / (nf / k11[fwd_v] + ni / k11[3])
+            pd = (nf + ni) / (nf / alu_peak_derived(sm_mhz, BFLY[fwd_v][2]) + ni / alu_peak_derived(sm_mhz, BFLY[3][2]))
+            kms = prof_path[p].get(kname, (0.0, 0))[0]
+            bpc = butterflies_per_ct(cfg, p)
+            ach = bpc * B / (seg[p] / 1e3)
+            kach = bpc * B / (kms / 1e3) if kms else ach
+            alu[p] = {"bound": "alu", "kernel": kname, "achieved": kach / 1e9, "peak": peak_p / 1e9,
+                      "unit": "Gbutterfly/s", "frac": kach / peak_p, "achieved_path": ach / 1e9,
+                      "frac_path": ach / peak_p, "peak_derived": pd / 1e9, "frac_of_derived": kach / pd,
+                      "butterflies_per_ct": bpc, "transforms_per_ct": {"forward": nf, "inverse": ni},
+                      "peak_source": f"measured K11 int_peak_kernel with the path's own butterflies: {nf} x "
+                                     f"{BFLY[fwd_v][0]} + {ni} x {BFLY[3][0]} per ct (harmonic mix); peak_derived: "
+                                     f"148 SMs x sm_mhz x 64 fma-pipe lanes/clk / SASS fma ops per butterfly "
+                                     f"({BFLY[fwd_v][2]} {BFLY[fwd_v][0]}, {BFLY[3][2]} {BFLY[3][0]})"}
         result = {
             "metric": METRIC,
             "value": path_out["zinc_coeff"]["ct_per_s"] if "zinc_coeff" in path_out else None,
@@ -564,6 +599,7 @@ def main():
             "hbm_frac_step": (bpc * B / (seg["zinc_coeff"] / 1e3) / 1e9) / peak if "zinc_coeff" in seg else None,
             "roofline": roof,
             "roofline_alu": alu,
+            "k11_gbfly": {BFLY[v][0]: r / 1e9 for v, r in k11.items()},
             "kernels": {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
                         for k, v in prof.items()},
             "gpu_launches": launches,
@@ -576,9 +612,21 @@ def main():
         # batched decrypt + decode (Eq. 10, CRT check on every limb) of the
         # step's last output (vanilla COEFF form), device-timed like the paths
         dms = _timed(torch, lambda: Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct), 3)
+        Z.profile_enable(True)
+        Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct)
+        torch.cuda.synchronize()
+        dk = Z.profile_read().get("decrypt_kernel", (0.0, 0))[0]
+        Z.profile_enable(False)
+        dpeak = 2 / (1 / k11[2] + 1 / k11[3])
+        dbf = butterflies_per_ct(cfg, "decrypt_coeff")
         result["decrypt_decode"] = {"form": "COEFF", "ms": dms, "ct_per_s": B / (dms / 1e3),
                                     "transforms_per_ct": 2 * cfg.L,
                                     "note": "x = c1 + c2 s on every limb (NTT + INTT per limb), CRT check, FP64 decode"}
+        result["roofline_alu"]["decrypt_coeff"] = {
+            "bound": "alu", "kernel": "decrypt_kernel", "achieved": dbf * B / (dk / 1e3) / 1e9 if dk else None,
+            "peak": dpeak / 1e9, "unit": "Gbutterfly/s", "frac": dbf * B / (dk / 1e3) / dpeak if dk else None,
+            "butterflies_per_ct": dbf, "transforms_per_ct": {"forward": cfg.L, "inverse": cfg.L},
+            "peak_source": "measured K11 with the kernel's butterflies: L x ct_bfly_a + L x gs_bfly per ct"}
     if rank == 0:
         # aggregation of the whole batch (Eq. 2, HBM-bound read of every ciphertext)
         agg = ctx.empty_key()

@@ -196,24 +196,33 @@ zinc_status zinc_debug_sample(const zinc_ctx *ctx, int tag, uint64_t seed, uint6
                               int limb, size_t n, void *out, zinc_stream_t stream);
 
 /* Integer-peak microkernel: `iters` rounds of 8 independent
- * register-resident lazy Shoup butterflies per thread with limb 0's modulus,
- * grid = blocks x 256 threads; writes a checksum to sink[0] (device uint64).
+ * register-resident butterflies per thread with limb 0's modulus, grid = blocks x
+ * 256 threads; writes a checksum to sink[0] (device uint64).  `variant` is the
+ * butterfly the transform kernels run (PAPER.md:308-317 prices a transform in
+ * butterflies): 0 lazy Harvey forward (exact Shoup quotient), 1 lazy-free forward
+ * (the CKKS forward transforms when every q < 2^58; needs q_0 < 2^58), 2 forward
+ * with one conditional subtraction (q up to 2^60), 3 inverse Gentleman-Sande.
  * *butterflies (host) receives the number of butterflies launched. */
-zinc_status zinc_int_peak(const zinc_ctx *ctx, int blocks, int iters, uint64_t *sink,
+zinc_status zinc_int_peak(const zinc_ctx *ctx, int variant, int blocks, int iters, uint64_t *sink,
                           double *butterflies, zinc_stream_t stream);
 
 /* Host-buffer encryption (end-to-end API): the same result as
  * zinc_encrypt_batch / ckks_encrypt_batch (path 0 = Zinc with `key` = cache,
  * path 1 = vanilla with `key` = pk_ntt, both device pointers) but pt and ct are
- * HOST pointers.  The batch is pipelined in chunks of `chunk` messages over two
- * internal streams: H2D of the plaintexts, the kernels, D2H of the ciphertexts,
- * overlapped.  Host buffers should be pinned (cudaHostAlloc / torch
- * pin_memory) for full bandwidth.  Blocks the calling thread until the last
- * ciphertext has reached the host. */
+ * HOST pointers.  The batch is pipelined in chunks of `chunk` messages (0: 256)
+ * over two streams the call creates and destroys: H2D of the plaintexts, the
+ * kernels, D2H of the ciphertexts, overlapped.  Device staging buffers come from
+ * the device's stream-ordered pool and are released before the call returns.
+ * Ordering: the first copy waits for the work already queued on `stream` (e.g.
+ * the zinc_precompute_cache / zinc_keygen that produced `key`).  Host buffers
+ * should be pinned (cudaHostAlloc / torch pin_memory) for full bandwidth.
+ * Blocks the calling thread until the last ciphertext has reached the host; on
+ * any error both internal streams are drained before returning, so no copy
+ * still references the caller's buffers. */
 zinc_status zinc_encrypt_batch_host(const zinc_ctx *ctx, int path, const uint64_t *key,
                                     zinc_form form, zinc_pt_kind kind, const void *pt_host,
                                     size_t batch, uint64_t seed, uint64_t msg_base,
-                                    uint64_t *ct_host, size_t chunk);
+                                    uint64_t *ct_host, size_t chunk, zinc_stream_t stream);
 
 /* Kernel tracing.  Ids of the library's kernels: */
 enum {
@@ -227,14 +236,12 @@ enum {
   ZINC_K_NTT = 7,
   ZINC_K_SAMPLE = 8,
   ZINC_K_INT_PEAK = 9,
-  ZINC_K_ZINC_FUSED = 10, /* encode of chunk k+1 fused with Zinc add/inject of chunk k */
-  ZINC_K_BFV_SCALE = 11, /* BFV decryption: round(t.x/Q) mod t from the RNS residues */
-  ZINC_K_CT_ADD = 12,    /* batched ciphertext addition (Eq. 2) */
-  ZINC_K_CT_SUM = 13,    /* aggregation of a batch */
-  ZINC_K_LIFT = 14,      /* 128-bit plaintexts -> RNS residues */
-  ZINC_K_PT_ADD = 15,    /* c1 += plaintext residues */
-  ZINC_K_ZINC_PIPE = 16,  /* persistent encode -> Zinc COEFF pipeline (ZINC_TUNE_OVERLAP = 3) */
-  ZINC_K_COUNT = 17
+  ZINC_K_BFV_SCALE = 10, /* BFV decryption: round(t.x/Q) mod t from the RNS residues */
+  ZINC_K_CT_ADD = 11,    /* batched ciphertext addition (Eq. 2) */
+  ZINC_K_CT_SUM = 12,    /* aggregation of a batch */
+  ZINC_K_LIFT = 13,      /* 128-bit plaintexts -> RNS residues */
+  ZINC_K_PT_ADD = 14,    /* c1 += plaintext residues */
+  ZINC_K_COUNT = 15
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */
@@ -253,33 +260,17 @@ void zinc_launch_count_reset(void);
 /* Process-wide tuning knobs (launch geometry only; results never change):
  *  ZINC_TUNE_COEFF_MSGS_PER_CTA   messages per CTA of the COEFF-form Zinc kernel (default 2)
  *  ZINC_TUNE_ENCODE_CHUNK_BYTES   bytes of int64 plaintexts encoded per chunk when the input is slots
- *                                 (default 32 MiB: the chunk stays resident in the 126 MB L2)
- *  ZINC_TUNE_OVERLAP              how slot encodes meet the COEFF-form Zinc kernel: 0 (default)
- *                                 serial chunks on the caller's stream; 1: encode chunk k+1 on an
- *                                 internal high-priority stream; 2: one fused launch per chunk carries
- *                                 the encode of chunk k+1 and the add/inject of chunk k (real slots,
- *                                 N <= 2^14, L <= 8; otherwise serial); 3: one persistent
- *                                 cooperative launch for the whole batch in which encoder CTAs fill
- *                                 an L2-resident ring of plaintexts that streamer CTAs consume
- *                                 (real slots, Zinc COEFF form, C1/C2/C3 shapes; otherwise serial)
- *  ZINC_TUNE_COEFF_SMEM_PAD       extra bytes of dynamic shared memory requested by the COEFF-form
- *                                 Zinc kernel (limits how many of its CTAs share an SM with the
- *                                 overlapped encode; default 0)
- *  ZINC_TUNE_PDL                  1 (default): the serial encode -> Zinc chunk pipeline chains its
+ *                                 and the path is Zinc COEFF form (default 32 MiB: the chunk stays
+ *                                 resident in the 126 MB L2 between the encode and the add/inject)
+ *  ZINC_TUNE_PDL                  1 (default): the serial encode -> path chunk pipeline chains its
  *                                 launches with programmatic dependent launch; 0: plain stream order
- *  ZINC_TUNE_PIPE_ENC_CTAS        encoder CTAs per SM of the persistent pipeline (OVERLAP = 3; default 1;
- *                                 0: only the CTAs the streamers leave over)
- *  ZINC_TUNE_PIPE_VARIANT         persistent pipeline geometry: 0 (default) 3 CTAs/SM, radix-8 encode
- *                                 passes; 1: 3 CTAs/SM, radix-16; 2: 2 CTAs/SM, radix-16
- *  ZINC_TUNE_L2_PREFETCH          1 (default): in the serial chunk pipeline, each Zinc COEFF launch
- *                                 prefetches the next chunk's slots into L2 for its encode; 0: off
- *  ZINC_TUNE_ENCODE_LITE          real-slot encode variant: 1 (default) the 68 KiB shared-memory encode
- *                                 on the side stream (OVERLAP = 1) only; 2 everywhere; 0 never
+ *  ZINC_TUNE_L2_PREFETCH          1 (default): in the Zinc COEFF chunk pipeline, each add/inject
+ *                                 launch prefetches the next chunk's slots into L2 for its encode
+ *  ZINC_TUNE_NTT_CHUNK_MSGS       messages per chunk when slots feed a transform path (Zinc NTT form,
+ *                                 vanilla): 0 (default) = 16 waves of the path kernel's CTAs
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
-enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_OVERLAP = 2,
-       ZINC_TUNE_COEFF_SMEM_PAD = 3, ZINC_TUNE_PDL = 4, ZINC_TUNE_PIPE_ENC_CTAS = 5, ZINC_TUNE_PIPE_VARIANT = 6,
-       ZINC_TUNE_L2_PREFETCH = 7, ZINC_TUNE_ENCODE_LITE = 8,
-       ZINC_TUNE_COUNT = 9 };
+enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_PDL = 2,
+       ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_COUNT = 5 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

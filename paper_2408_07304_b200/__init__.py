@@ -24,7 +24,8 @@ __all__ = [
     "zinc_keygen", "zinc_precompute_cache", "zinc_encrypt_batch", "ckks_encrypt_batch",
     "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
     "zinc_debug_sample", "zinc_int_peak", "zinc_ct_add_batch", "zinc_ct_sum_batch", "zinc_encrypt_batch_host", "launch_count",
-    "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_OVERLAP", "TUNE_COEFF_SMEM_PAD", "TUNE_PDL", "TUNE_PIPE_ENC_CTAS", "TUNE_PIPE_VARIANT", "TUNE_L2_PREFETCH", "TUNE_ENCODE_LITE", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
+    "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_PDL", "TUNE_L2_PREFETCH",
+    "TUNE_NTT_CHUNK_MSGS", "BFLY_CT", "BFLY_CT_NR", "BFLY_CT_A", "BFLY_GS", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
 ]
 
 NTT, COEFF = 0, 1
@@ -45,8 +46,9 @@ EXPORTED_SYMBOLS = (
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
                 "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel", "lift_kernel",
-                "pt_add_kernel", "zinc_pipe_kernel")
+                "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel", "lift_kernel", "pt_add_kernel")
+# zinc_int_peak butterfly variants (include/zinc.h)
+BFLY_CT, BFLY_CT_NR, BFLY_CT_A, BFLY_GS = 0, 1, 2, 3
 
 
 class ZincError(RuntimeError):
@@ -69,8 +71,8 @@ _SIGS = {
     "zinc_ntt_forward": [_vp, _vp, _sz, _vp],
     "zinc_ntt_inverse": [_vp, _vp, _sz, _vp],
     "zinc_debug_sample": [_vp, _i32, _u64, _u64, _i32, _sz, _vp, _vp],
-    "zinc_int_peak": [_vp, _i32, _i32, _vp, _c.POINTER(_c.c_double), _vp],
-    "zinc_encrypt_batch_host": [_vp, _i32, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _sz],
+    "zinc_int_peak": [_vp, _i32, _i32, _i32, _vp, _c.POINTER(_c.c_double), _vp],
+    "zinc_encrypt_batch_host": [_vp, _i32, _vp, _i32, _i32, _vp, _sz, _u64, _u64, _vp, _sz, _vp],
     "zinc_profile_enable": [_i32],
     "zinc_profile_read": [_c.POINTER(_c.c_double), _c.POINTER(_u64)],
     "zinc_tune": [_i32, _c.c_longlong, _c.POINTER(_c.c_longlong)],
@@ -315,21 +317,25 @@ def zinc_debug_sample(ctx: Context, tag: int, seed: int, msg: int, limb: int, n:
     return out
 
 
-def zinc_int_peak(ctx: Context, blocks: int, iters: int, sink: torch.Tensor, stream=None) -> float:
+def zinc_int_peak(ctx: Context, blocks: int, iters: int, sink: torch.Tensor, variant: int = BFLY_CT,
+                  stream=None) -> float:
+    """K11: launch `blocks` x 256 threads of `iters` x 8 register-resident butterflies of
+    `variant` (BFLY_*); returns the number of butterflies launched."""
     bf = ctypes.c_double()
-    _check(lib().zinc_int_peak(ctx.handle, blocks, iters, _ptr(sink), ctypes.byref(bf), _stream(stream)),
+    _check(lib().zinc_int_peak(ctx.handle, variant, blocks, iters, _ptr(sink), ctypes.byref(bf), _stream(stream)),
            "zinc_int_peak")
     return bf.value
 
 
 def zinc_encrypt_batch_host(ctx: Context, path: int, key: torch.Tensor, form: int, pt_host: torch.Tensor,
-                            seed: int, msg_base: int, ct_host: torch.Tensor, chunk: int = 256):
-    """Host-buffer (end-to-end) encryption: pt_host / ct_host are CPU tensors (pinned for speed)."""
+                            seed: int, msg_base: int, ct_host: torch.Tensor, chunk: int = 256, stream=None):
+    """Host-buffer (end-to-end) encryption: pt_host / ct_host are CPU tensors (pinned for speed).
+    The call orders itself after the work queued on `stream` (default: torch's current stream)."""
     pt_host = _as_pt(pt_host)
     if pt_host.is_cuda or ct_host.is_cuda:
         raise ZincError("zinc_encrypt_batch_host takes host tensors")
     _check(lib().zinc_encrypt_batch_host(ctx.handle, path, _ptr(key), form, _kind_of(pt_host), _ptr(pt_host),
-                                         pt_host.shape[0], seed, msg_base, _ptr(ct_host), chunk),
+                                         pt_host.shape[0], seed, msg_base, _ptr(ct_host), chunk, _stream(stream)),
            "zinc_encrypt_batch_host")
     return ct_host
 
@@ -348,8 +354,7 @@ def profile_read() -> dict:
     return {KERNEL_NAMES[i]: (float(ms[i]), int(cnt[i])) for i in range(n) if cnt[i]}
 
 
-TUNE_COEFF_MSGS_PER_CTA, TUNE_ENCODE_CHUNK_BYTES, TUNE_OVERLAP, TUNE_COEFF_SMEM_PAD, TUNE_PDL = 0, 1, 2, 3, 4
-TUNE_PIPE_ENC_CTAS, TUNE_PIPE_VARIANT, TUNE_L2_PREFETCH, TUNE_ENCODE_LITE = 5, 6, 7, 8
+TUNE_COEFF_MSGS_PER_CTA, TUNE_ENCODE_CHUNK_BYTES, TUNE_PDL, TUNE_L2_PREFETCH, TUNE_NTT_CHUNK_MSGS = 0, 1, 2, 3, 4
 
 
 def tune(knob: int, value: int) -> int:

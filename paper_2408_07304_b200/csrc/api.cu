@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/zinc.h"
 #include "kernels.h"
 
@@ -51,9 +53,8 @@ static uint64_t g_trace_n[ZINC_K_COUNT];
 static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel",
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
                                                  "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                                                 "zinc_coeff_encode_kernel", "bfv_scale_kernel", "ct_add_kernel",
-                                                 "ct_sum_kernel", "lift_kernel", "pt_add_kernel",
-                                                 "zinc_pipe_kernel"};
+                                                 "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel",
+                                                 "lift_kernel", "pt_add_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -96,11 +97,20 @@ struct TraceScope {
       return fail(ZINC_ECUDA, "launch %s failed: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
+// NVTX range around every ABI call (tracing); a no-op unless a tool
+// (nsys / ncu --nvtx) injects the NVTX library.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 // CKKS scales from 2^48 up encode slots into 128-bit coefficients (f3).
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {0}, {0}, {1}, {1}, {0}, {1}, {1}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {1}, {1}, {0}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -116,16 +126,9 @@ struct zinc_ctx {
   double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr, *d_post_tw = nullptr;
   double2 *d_twist_split = nullptr;
   int *d_perm = nullptr;
-  // host-API pipeline buffers (grow-only, guarded)
-  std::mutex host_mu;
-  void *h_pt_d[2] = {nullptr, nullptr};
-  uint64_t *h_ct_d[2] = {nullptr, nullptr};
-  size_t h_pt_bytes = 0, h_ct_bytes = 0;
-  cudaStream_t h_streams[2] = {nullptr, nullptr};
-  // side stream: slot encodes overlap the previous chunk's path kernel
-  std::mutex side_mu;
-  cudaStream_t side = nullptr;
   uint64_t qmin = 0;
+  // Immutable after zinc_ctx_create: calls only read the context, so calls on
+  // different streams (or threads) may overlap.
 };
 
 // ------------------------------------------------------------------ number theory (host)
@@ -281,12 +284,6 @@ zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
   cudaFree(ctx->d_twist_split);
   cudaFree(ctx->d_fft_tw_h);
   cudaFree(ctx->d_perm);
-  if (ctx->side) cudaStreamDestroy(ctx->side);
-  for (int k = 0; k < 2; ++k) {
-    cudaFree(ctx->h_pt_d[k]);
-    cudaFree(ctx->h_ct_d[k]);
-    if (ctx->h_streams[k]) cudaStreamDestroy(ctx->h_streams[k]);
-  }
   delete ctx;
   return ZINC_OK;
 }
@@ -439,14 +436,6 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     zinc_ctx_destroy(c);
     return fail(ZINC_ECUDA, "device attribute query failed");
   }
-  // the side stream gets the highest priority so the block scheduler hands freed
-  // SM slots to the (short) encode CTAs ahead of the streaming kernel's backlog
-  int prio_lo = 0, prio_hi = 0;
-  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
-    zinc_ctx_destroy(c);
-    return fail(ZINC_ECUDA, "side stream creation failed");
-  }
   // stream-ordered scratch (slot encodes) comes from the default pool: keep it
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -516,10 +505,9 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
 }
 
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
-                               cudaStream_t s, bool wide = false, bool lite = false) {
+                               cudaStream_t s, bool wide = false) {
   EncodeArgs a = encode_args(c, kind, slots, m);
   a.wide = wide ? 1 : 0;
-  a.lite = (lite || g_tune[ZINC_TUNE_ENCODE_LITE].load() == 2) ? 1 : 0;
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
@@ -553,7 +541,7 @@ static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, c
   return a;
 }
 static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
-  size_t want = 2 * 148;
+  size_t want = 2 * (size_t)c->num_sms;
   if (batch >= want) return c->L;
   int groups = (int)std::min<size_t>((size_t)c->L, (want + batch - 1) / batch);
   return (c->L + groups - 1) / groups;
@@ -569,7 +557,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     int threads = 256;
     while (threads > 32 && zinc_coeff_smem(c->L, threads) > 72 * 1024) threads /= 2;
     const size_t gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
-    LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, (size_t)g_tune[ZINC_TUNE_COEFF_SMEM_PAD].load(), s));
+    LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, 0, s));
     return ZINC_OK;
   }
   const int lpc = limbs_per_cta(c, batch);
@@ -608,7 +596,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
 // to RNS residues (-> NTT in NTT form), run the path with m = 0 and add the
 // residues into c1.  Same ciphertext bits as adding m inside the path kernels
 // (all arithmetic is exact); costs one more pass over c1.
-static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int form, int kind, const void *pt,
+static zinc_status encrypt_wide(const zinc_ctx *c, int path, const uint64_t *key, int form, int kind, const void *pt,
                                 size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s) {
   const bool slots = kind != ZINC_PT_COEFF_I128;
   const bool direct = path == PATH_ZINC && form == ZINC_FORM_COEFF;  // kernel reads 128-bit m itself
@@ -654,139 +642,62 @@ static zinc_status encrypt_wide(zinc_ctx *c, int path, const uint64_t *key, int 
 }
 
 // Encryption with any plaintext kind: int64 plaintexts go straight to the path
-// kernel; slots are encoded chunk by chunk into stream-ordered scratch sized to
-// stay resident in L2 between the encode and the path kernel.  The encodes run
-// on the context's side stream, double-buffered, so chunk k+1 is encoded while
-// the path kernel of chunk k streams its ciphertexts out (events order the
-// buffers; the caller's stream sees the whole call as one ordered operation).
-static zinc_status encrypt_any(const zinc_ctx *cc, int path, const uint64_t *key, int form, int kind,
+// kernel; slots are encoded chunk by chunk into stream-ordered scratch
+// (double-buffered) on the caller's stream, and the launches of the chain
+// (encode 0, path 0, encode 1, path 1, ...) are programmatic dependent launches:
+// each kernel's prologue (TMA staging, sampling, the encode's FFT) overlaps the
+// tail of the kernel before it, and only its reads of the previous kernel's
+// output (and the encode's scratch stores) wait (griddepcontrol.wait).
+//  - Zinc COEFF form (HBM-bound): 32 MiB chunks, so the encoded plaintexts are
+//    still in L2 when the add/inject kernel reads them; each add/inject launch
+//    also warms the next chunk's slots into L2.
+//  - transform paths (Zinc NTT form, vanilla; integer-bound): chunks of whole
+//    waves of the path kernel, large enough that its last partial wave is a
+//    small fraction of the chunk.
+static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key, int form, int kind,
                                const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
                                cudaStream_t s) {
-  zinc_ctx *c = const_cast<zinc_ctx *>(cc);
   if (kind == ZINC_PT_COEFF_I64) return run_path(c, path, key, form, (const int64_t *)pt, batch, seed, msg_base, ct, s);
   if (kind == ZINC_PT_COEFF_I128 || c->wide) return encrypt_wide(c, path, key, form, kind, pt, batch, seed, msg_base, ct, s);
   const size_t per_msg = (size_t)c->n * 8;
-  const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());
-  const size_t chunk = std::max<size_t>(1, std::min(batch, chunk_bytes / per_msg));
-  const long long mode = g_tune[ZINC_TUNE_OVERLAP].load();
-  const bool fused = mode == 2 && path == PATH_ZINC && form == ZINC_FORM_COEFF && kind == ZINC_PT_SLOTS_F64 &&
-                     fused_supported(c->log_n, c->L);
-  const bool pipe = mode == 3 && path == PATH_ZINC && form == ZINC_FORM_COEFF && kind == ZINC_PT_SLOTS_F64 &&
-                    c->scheme == ZINC_SCHEME_CKKS && pipe_supported(c->log_n, c->L) && batch < (1ull << 31) &&
-                    chunk >= std::min<size_t>(batch, (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load()));
-  const bool overlap = mode == 1 && batch > chunk;
-  const int nbuf = (overlap || (fused && batch > chunk)) ? 2 : 1;
-  // serial chunks chained with programmatic dependent launches (knob ZINC_TUNE_PDL) double-buffer
-  const bool pdl = !pipe && !overlap && !fused && g_tune[ZINC_TUNE_PDL].load() != 0 &&
-                   (kind == ZINC_PT_SLOTS_F64 || kind == ZINC_PT_SLOTS_C128) &&
-                   path == PATH_ZINC && form == ZINC_FORM_COEFF;
-  const int nb = (nbuf == 2 || (pdl && batch > chunk)) ? 2 : 1;
+  const bool coeff_zinc = path == PATH_ZINC && form == ZINC_FORM_COEFF;
+  size_t chunk;
+  if (coeff_zinc) {
+    const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());
+    chunk = chunk_bytes / per_msg;
+  } else {
+    const long long knob = g_tune[ZINC_TUNE_NTT_CHUNK_MSGS].load();
+    // 16 waves of two message-CTA groups per SM (the transform kernels' residency)
+    chunk = knob > 0 ? (size_t)knob : (size_t)16 * 2 * c->num_sms;
+  }
+  chunk = std::max<size_t>(1, std::min(batch, chunk));
+  const bool pdl = g_tune[ZINC_TUNE_PDL].load() != 0;
+  const int nb = batch > chunk ? 2 : 1;
   ScratchBuf mbuf(s);
   CUDA_TRY(mbuf.alloc(nb * chunk * per_msg));
   int64_t *m = mbuf.as<int64_t>();
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_stride = (size_t)2 * c->L * c->n;
   zinc_status st = ZINC_OK;
-  if (pipe) {
-    // one persistent launch: the ring is the scratch (chunk messages), plus its sync words
-    ScratchBuf sync(s);
-    const int ring = (int)chunk;
-    const size_t sync_bytes = pipe_sync_words(ring, c->n / 512) * sizeof(uint32_t);
-    CUDA_TRY(sync.alloc(sync_bytes));
-    CUDA_TRY(cudaMemsetAsync(sync.p, 0, sync_bytes, s));
-    PipeArgs pa{};
-    pa.z = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
-    pa.e = encode_args(c, kind, pt, m);
-    pa.sync = sync.as<uint32_t>();
-    pa.ring = ring;
-    pa.enc_per_sm = (int)std::min<long long>(8, g_tune[ZINC_TUNE_PIPE_ENC_CTAS].load());
-    pa.tiles = c->n / 512;
-    cudaError_t e;
-    {
-      TraceScope ts(ZINC_K_ZINC_PIPE, s);
-      e = launch_zinc_pipe(c->log_n, pa, (int)g_tune[ZINC_TUNE_PIPE_VARIANT].load(), c->num_sms, s);
-    }
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (e != cudaSuccess) st = fail(ZINC_ECUDA, "persistent encode/zinc launch: %s", cudaGetErrorString(e));
-    return st;
-  }
-  if (fused) {
-    // launch k: encode chunk k (k < nch) into m[k % 2] | add/inject chunk k-1 from m[(k-1) % 2]
-    const size_t nch = (batch + chunk - 1) / chunk;
-    for (size_t k = 0; k <= nch && st == ZINC_OK; ++k) {
-      const size_t enc = k < nch ? std::min(chunk, batch - k * chunk) : 0;
-      const size_t zc = k > 0 ? std::min(chunk, batch - (k - 1) * chunk) : 0;
-      int64_t *m_enc = m + (size_t)(k % nbuf) * chunk * c->n;
-      const int64_t *m_z = m + (size_t)((k + nbuf - 1) % nbuf) * chunk * c->n;
-      const EncodeArgs ea = encode_args(c, kind, (const char *)pt + (enc ? k * chunk : 0) * in_stride, m_enc);
-      const size_t zoff = k > 0 ? (k - 1) * chunk : 0;
-      ZincCoeffArgs za = zinc_coeff_args(c, key, m_z, zc, seed, msg_base + zoff, ct + zoff * ct_stride);
-      za.discard_m = 1;
-      const int gy = (int)((zc + za.msgs_per_cta - 1) / za.msgs_per_cta);
-      cudaError_t e;
-      {
-        TraceScope ts(ZINC_K_ZINC_FUSED, s);
-        e = launch_zinc_coeff_encode(c->log_n, za, gy, ea, (int)enc, s);
-      }
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-      if (e != cudaSuccess) st = fail(ZINC_ECUDA, "fused encode/zinc launch: %s", cudaGetErrorString(e));
-    }
-    return st;
-  }
-  if (!overlap) {
-    // serial chunks; with PDL each kernel's prologue overlaps the previous kernel's tail
-    size_t k = 0;
-    for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
-      const size_t cnt = std::min(chunk, batch - off);
-      int64_t *mb = m + (size_t)(k % nb) * chunk * c->n;
-      {
-        // the first launch keeps a full dependency on whatever produced the inputs (its
-        // loads precede its griddepcontrol.wait); later ones chain on this pipeline's kernels
-        PdlScope pdl_scope(pdl && k > 0);
-        st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
-      }
-      PdlScope pdl_scope(pdl);
-      // the Zinc kernel of this chunk warms the next chunk's slots into L2 for its encode
-      const size_t nxt = std::min(chunk, batch - std::min(batch, off + chunk));
-      const bool pf = g_tune[ZINC_TUNE_L2_PREFETCH].load() != 0 && nxt > 0 && aligned16(pt) && in_stride % 16 == 0;
-      g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + chunk) * in_stride, nxt * in_stride} : L2Prefetch{};
-      if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
-      g_l2_prefetch = L2Prefetch{};
-    }
-    return st;
-  }
-  // side-stream overlap: events order the double-buffered scratch between the two streams
-  std::lock_guard<std::mutex> lock(c->side_mu);
-  struct Events {
-    cudaEvent_t ev[5] = {};
-    ~Events() {
-      for (cudaEvent_t e : ev)
-        if (e) cudaEventDestroy(e);
-    }
-  } E;
-  for (cudaEvent_t &e : E.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  cudaEvent_t ev_in = E.ev[0], *ev_enc = E.ev + 1, *ev_use = E.ev + 3;
-  CUDA_TRY(cudaEventRecord(ev_in, s));  // inputs and the scratch allocation are ready
-  CUDA_TRY(cudaStreamWaitEvent(c->side, ev_in, 0));
-  cudaError_t ce = cudaSuccess;
   size_t k = 0;
-  for (size_t off = 0; off < batch && st == ZINC_OK && ce == cudaSuccess; off += chunk, ++k) {
-    const int buf = (int)(k & 1);
+  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
     const size_t cnt = std::min(chunk, batch - off);
-    int64_t *mb = m + (size_t)buf * chunk * c->n;
-    if (k >= 2 && (ce = cudaStreamWaitEvent(c->side, ev_use[buf], 0)) != cudaSuccess) break;  // chunk k-2 read mb
-    // the light encode fits beside two streaming CTAs per SM (with ZINC_TUNE_COEFF_SMEM_PAD)
-    const bool lite = g_tune[ZINC_TUNE_ENCODE_LITE].load() != 0;
-    if ((st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, c->side, false, lite)) != ZINC_OK) break;
-    if ((ce = cudaEventRecord(ev_enc[buf], c->side)) != cudaSuccess) break;
-    if ((ce = cudaStreamWaitEvent(s, ev_enc[buf], 0)) != cudaSuccess) break;
-    if ((st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true))) break;
-    ce = cudaEventRecord(ev_use[buf], s);
+    int64_t *mb = m + (size_t)(k % nb) * chunk * c->n;
+    {
+      // the first launch keeps a full dependency on whatever produced the inputs (its
+      // loads precede its griddepcontrol.wait); later ones chain on this pipeline's kernels
+      PdlScope pdl_scope(pdl && k > 0);
+      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
+    }
+    PdlScope pdl_scope(pdl);
+    // the Zinc COEFF kernel of this chunk warms the next chunk's slots into L2 for its encode
+    const size_t nxt = std::min(chunk, batch - std::min(batch, off + chunk));
+    const bool pf = coeff_zinc && g_tune[ZINC_TUNE_L2_PREFETCH].load() != 0 && nxt > 0 && aligned16(pt) &&
+                    in_stride % 16 == 0;
+    g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + chunk) * in_stride, nxt * in_stride} : L2Prefetch{};
+    if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
+    g_l2_prefetch = L2Prefetch{};
   }
-  // the caller's stream (and the scratch release on it) stays after everything on the side stream
-  cudaEventRecord(ev_in, c->side);
-  cudaStreamWaitEvent(s, ev_in, 0);
-  if (ce != cudaSuccess && st == ZINC_OK) st = fail(ZINC_ECUDA, "side-stream ordering: %s", cudaGetErrorString(ce));
   return st;
 }
 
@@ -804,6 +715,7 @@ static zinc_status check_encrypt(const zinc_ctx *c, const uint64_t *key, int for
 // ------------------------------------------------------------------ ABI calls
 zinc_status zinc_keygen(const zinc_ctx *c, uint64_t seed, uint64_t *sk_ntt, int8_t *sk_coeff, uint64_t *pk_ntt,
                         zinc_stream_t stream) {
+  NvtxRange nr("zinc_keygen");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_ptrs({sk_ntt, pk_ntt}))) return st;
@@ -822,6 +734,7 @@ zinc_status zinc_keygen(const zinc_ctx *c, uint64_t seed, uint64_t *sk_ntt, int8
 
 zinc_status zinc_precompute_cache(const zinc_ctx *c, const uint64_t *pk_ntt, uint64_t seed, zinc_form form,
                                   uint64_t *cache, zinc_stream_t stream) {
+  NvtxRange nr("zinc_precompute_cache");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_form(form)) || (st = check_ptrs({pk_ntt, cache}))) return st;
@@ -833,6 +746,7 @@ zinc_status zinc_precompute_cache(const zinc_ctx *c, const uint64_t *pk_ntt, uin
 zinc_status zinc_encrypt_batch(const zinc_ctx *c, const uint64_t *cache, zinc_form form, zinc_pt_kind kind,
                                const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
                                zinc_stream_t stream) {
+  NvtxRange nr("zinc_encrypt_batch");
   if (batch == 0) return ZINC_OK;
   zinc_status st = check_encrypt(c, cache, form, kind, pt, ct);
   if (st) return st;
@@ -842,6 +756,7 @@ zinc_status zinc_encrypt_batch(const zinc_ctx *c, const uint64_t *cache, zinc_fo
 zinc_status ckks_encrypt_batch(const zinc_ctx *c, const uint64_t *pk_ntt, zinc_form form, zinc_pt_kind kind,
                                const void *pt, size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct,
                                zinc_stream_t stream) {
+  NvtxRange nr("ckks_encrypt_batch");
   if (batch == 0) return ZINC_OK;
   zinc_status st = check_encrypt(c, pk_ntt, form, kind, pt, ct);
   if (st) return st;
@@ -855,6 +770,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
 zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_form form, const uint64_t *ct,
                                size_t batch, double *slots_out, int64_t *coeff_out, int32_t *status_out,
                                zinc_stream_t stream) {
+  NvtxRange nr("ckks_decrypt_batch");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (c->wide && coeff_out)
     return fail(ZINC_EINVAL, "log_scale >= 48: coefficients are 128-bit, use ckks_decrypt_batch_wide");
@@ -865,6 +781,7 @@ zinc_status ckks_decrypt_batch(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_f
 zinc_status ckks_decrypt_batch_wide(const zinc_ctx *c, const uint64_t *sk_ntt, zinc_form form, const uint64_t *ct,
                                     size_t batch, double *slots_out, int64_t *coeff128_out, int32_t *status_out,
                                     zinc_stream_t stream) {
+  NvtxRange nr("ckks_decrypt_batch_wide");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (c->scheme != ZINC_SCHEME_CKKS) return fail(ZINC_EINVAL, "wide decryption is for CKKS contexts");
   if (c->L < 2) return fail(ZINC_EINVAL, "wide decryption needs at least two limbs");
@@ -950,6 +867,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
 
 zinc_status zinc_ct_add_batch(const zinc_ctx *c, const uint64_t *x, const uint64_t *y, size_t batch, uint64_t *out,
                               zinc_stream_t stream) {
+  NvtxRange nr("zinc_ct_add_batch");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (batch == 0) return ZINC_OK;
   zinc_status st;
@@ -969,6 +887,7 @@ zinc_status zinc_ct_add_batch(const zinc_ctx *c, const uint64_t *x, const uint64
 
 zinc_status zinc_ct_sum_batch(const zinc_ctx *c, const uint64_t *ct, size_t batch, uint64_t *out,
                               zinc_stream_t stream) {
+  NvtxRange nr("zinc_ct_sum_batch");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_ptrs({out})) || (batch && (st = check_ptrs({ct})))) return st;
@@ -986,6 +905,7 @@ zinc_status zinc_ct_sum_batch(const zinc_ctx *c, const uint64_t *ct, size_t batc
 
 zinc_status ckks_encode_batch_wide(const zinc_ctx *c, zinc_pt_kind kind, const void *slots, size_t batch,
                                    int64_t *m_out, zinc_stream_t stream) {
+  NvtxRange nr("ckks_encode_batch_wide");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (batch == 0) return ZINC_OK;
   if (kind != ZINC_PT_SLOTS_F64 && kind != ZINC_PT_SLOTS_C128) return fail(ZINC_EINVAL, "encode needs a slot kind");
@@ -997,6 +917,7 @@ zinc_status ckks_encode_batch_wide(const zinc_ctx *c, zinc_pt_kind kind, const v
 
 zinc_status ckks_encode_batch(const zinc_ctx *c, zinc_pt_kind kind, const void *slots, size_t batch, int64_t *m_out,
                               zinc_stream_t stream) {
+  NvtxRange nr("ckks_encode_batch");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (batch == 0) return ZINC_OK;
   if (kind != ZINC_PT_SLOTS_F64 && kind != ZINC_PT_SLOTS_C128) return fail(ZINC_EINVAL, "encode needs a slot kind");
@@ -1022,14 +943,17 @@ static zinc_status ntt_dir(const zinc_ctx *c, uint64_t *data, size_t count, int 
   return ZINC_OK;
 }
 zinc_status zinc_ntt_forward(const zinc_ctx *c, uint64_t *data, size_t count, zinc_stream_t stream) {
+  NvtxRange nr("zinc_ntt_forward");
   return ntt_dir(c, data, count, 0, stream);
 }
 zinc_status zinc_ntt_inverse(const zinc_ctx *c, uint64_t *data, size_t count, zinc_stream_t stream) {
+  NvtxRange nr("zinc_ntt_inverse");
   return ntt_dir(c, data, count, 1, stream);
 }
 
 zinc_status zinc_debug_sample(const zinc_ctx *c, int tag, uint64_t seed, uint64_t msg, int limb, size_t n, void *out,
                               zinc_stream_t stream) {
+  NvtxRange nr("zinc_debug_sample");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (tag < 1 || tag > 8) return fail(ZINC_EINVAL, "bad tag %d", tag);
   if (limb < 0 || limb >= c->L) return fail(ZINC_EINVAL, "bad limb %d", limb);
@@ -1049,10 +973,13 @@ zinc_status zinc_debug_sample(const zinc_ctx *c, int tag, uint64_t seed, uint64_
   return ZINC_OK;
 }
 
-zinc_status zinc_int_peak(const zinc_ctx *c, int blocks, int iters, uint64_t *sink, double *butterflies,
-                          zinc_stream_t stream) {
+zinc_status zinc_int_peak(const zinc_ctx *c, int variant, int blocks, int iters, uint64_t *sink,
+                          double *butterflies, zinc_stream_t stream) {
+  NvtxRange nr("zinc_int_peak");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (blocks < 1 || iters < 1) return fail(ZINC_EINVAL, "blocks and iters must be positive");
+  if (variant < 0 || variant > 3) return fail(ZINC_EINVAL, "bad butterfly variant %d", variant);
+  if (variant == 1 && c->q[0] >= (1ull << 58)) return fail(ZINC_EINVAL, "lazy-free butterflies need q < 2^58");
   zinc_status st;
   if ((st = check_ptrs({sink}))) return st;
   CUDA_TRY(cudaSetDevice(c->device));
@@ -1062,62 +989,70 @@ zinc_status zinc_int_peak(const zinc_ctx *c, int blocks, int iters, uint64_t *si
   a.wp = shoup(c->psi[0], c->q[0]);
   a.iters = iters;
   a.sink = sink;
-  LAUNCH(ZINC_K_INT_PEAK, (cudaStream_t)stream, launch_int_peak(a, blocks, (cudaStream_t)stream));
+  LAUNCH(ZINC_K_INT_PEAK, (cudaStream_t)stream, launch_int_peak(a, variant, blocks, (cudaStream_t)stream));
   if (butterflies) *butterflies = (double)blocks * 256.0 * 8.0 * (double)iters;
   return ZINC_OK;
 }
 
-zinc_status zinc_encrypt_batch_host(const zinc_ctx *cc, int path, const uint64_t *key, zinc_form form,
+zinc_status zinc_encrypt_batch_host(const zinc_ctx *c, int path, const uint64_t *key, zinc_form form,
                                     zinc_pt_kind kind, const void *pt_host, size_t batch, uint64_t seed,
-                                    uint64_t msg_base, uint64_t *ct_host, size_t chunk) {
-  zinc_ctx *c = const_cast<zinc_ctx *>(cc);
+                                    uint64_t msg_base, uint64_t *ct_host, size_t chunk, zinc_stream_t stream) {
+  NvtxRange nr("zinc_encrypt_batch_host");
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   if (batch == 0) return ZINC_OK;
   if (path != PATH_ZINC && path != PATH_VANILLA) return fail(ZINC_EINVAL, "bad path %d", path);
   zinc_status st;
   if ((st = check_form(form)) || (st = check_kind(kind)) || (st = check_ptrs({key, pt_host, ct_host}))) return st;
+  if (c->scheme != ZINC_SCHEME_CKKS && kind != ZINC_PT_COEFF_I64)
+    return fail(ZINC_EINVAL, "BFV / BGV contexts take integer plaintext coefficients (ZINC_PT_COEFF_I64)");
   if (chunk == 0) chunk = 256;
   chunk = std::min(chunk, batch);
-  std::lock_guard<std::mutex> lock(c->host_mu);
   CUDA_TRY(cudaSetDevice(c->device));
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_words = (size_t)2 * c->L * c->n;
-  if (c->h_pt_bytes < chunk * in_stride || c->h_ct_bytes < chunk * ct_words * 8) {
-    for (int k = 0; k < 2; ++k) {
-      cudaFree(c->h_pt_d[k]);
-      cudaFree(c->h_ct_d[k]);
-      c->h_pt_d[k] = nullptr;
-      c->h_ct_d[k] = nullptr;
+  // Per-call resources (the context stays immutable): two streams, an event ordering them
+  // after the caller's stream, and pool-allocated staging buffers on each stream.
+  struct Res {
+    cudaStream_t h[2] = {nullptr, nullptr};
+    cudaEvent_t ready = nullptr;
+    void *pt[2] = {nullptr, nullptr};
+    uint64_t *ct[2] = {nullptr, nullptr};
+    ~Res() {
+      for (int k = 0; k < 2; ++k) {
+        if (h[k]) {
+          if (pt[k]) cudaFreeAsync(pt[k], h[k]);
+          if (ct[k]) cudaFreeAsync(ct[k], h[k]);
+          cudaStreamSynchronize(h[k]);
+          cudaStreamDestroy(h[k]);
+        }
+      }
+      if (ready) cudaEventDestroy(ready);
     }
-    c->h_pt_bytes = c->h_ct_bytes = 0;
-    for (int k = 0; k < 2; ++k) {
-      if (cudaMalloc(&c->h_pt_d[k], chunk * in_stride) != cudaSuccess ||
-          cudaMalloc((void **)&c->h_ct_d[k], chunk * ct_words * 8) != cudaSuccess)
-        return fail(ZINC_ENOMEM, "host pipeline buffers (%zu messages)", chunk);
-    }
-    c->h_pt_bytes = chunk * in_stride;
-    c->h_ct_bytes = chunk * ct_words * 8;
+  } R;
+  CUDA_TRY(cudaEventCreateWithFlags(&R.ready, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(R.ready, (cudaStream_t)stream));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&R.h[k], cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamWaitEvent(R.h[k], R.ready, 0));
+    if (cudaMallocAsync(&R.pt[k], chunk * in_stride, R.h[k]) != cudaSuccess ||
+        cudaMallocAsync((void **)&R.ct[k], chunk * ct_words * 8, R.h[k]) != cudaSuccess)
+      return fail(ZINC_ENOMEM, "host pipeline buffers (%zu messages)", chunk);
   }
-  for (int k = 0; k < 2; ++k)
-    if (!c->h_streams[k]) CUDA_TRY(cudaStreamCreateWithFlags(&c->h_streams[k], cudaStreamNonBlocking));
-  // two streams alternate chunks; on any error both are drained before returning so that no
-  // copy still references the caller's host buffers
+  // the two streams alternate chunks: H2D, kernels, D2H
   size_t idx = 0;
   cudaError_t ce = cudaSuccess;
-  st = ZINC_OK;
   for (size_t off = 0; off < batch; off += chunk, ++idx) {
     const int k = (int)(idx & 1);
-    cudaStream_t s = c->h_streams[k];
+    cudaStream_t s = R.h[k];
     const size_t cnt = std::min(chunk, batch - off);
-    ce = cudaMemcpyAsync(c->h_pt_d[k], (const char *)pt_host + off * in_stride, cnt * in_stride,
-                         cudaMemcpyHostToDevice, s);
+    ce = cudaMemcpyAsync(R.pt[k], (const char *)pt_host + off * in_stride, cnt * in_stride, cudaMemcpyHostToDevice, s);
     if (ce != cudaSuccess) break;
-    if ((st = encrypt_any(c, path, key, form, kind, c->h_pt_d[k], cnt, seed, msg_base + off, c->h_ct_d[k], s))) break;
-    ce = cudaMemcpyAsync(ct_host + off * ct_words, c->h_ct_d[k], cnt * ct_words * 8, cudaMemcpyDeviceToHost, s);
+    if ((st = encrypt_any(c, path, key, form, kind, R.pt[k], cnt, seed, msg_base + off, R.ct[k], s))) break;
+    ce = cudaMemcpyAsync(ct_host + off * ct_words, R.ct[k], cnt * ct_words * 8, cudaMemcpyDeviceToHost, s);
     if (ce != cudaSuccess) break;
   }
   for (int k = 0; k < 2; ++k) {
-    const cudaError_t e = cudaStreamSynchronize(c->h_streams[k]);
+    const cudaError_t e = cudaStreamSynchronize(R.h[k]);
     if (ce == cudaSuccess) ce = e;
   }
   if (st == ZINC_OK && ce != cudaSuccess) st = fail(ZINC_ECUDA, "host pipeline: %s", cudaGetErrorString(ce));

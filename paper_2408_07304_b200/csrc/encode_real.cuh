@@ -154,46 +154,4 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   encode_real_post<LOGM, WIDE, THREADS>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf, sptw);
 }
 
-// Shared memory bytes of the lighter encode role of the persistent pipeline
-// (FFT buffer only: twiddles are read through L1).
-template <int LOGM> constexpr size_t encode_real_lite_smem() {
-  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16) * sizeof(double2);
-}
-
-// The same encode for the persistent pipeline (k_pipe.cu): slots are read
-// straight into registers (two halves, no in-place permutation, no TMA), the
-// FFT twiddles come through L1, and the plaintext goes to ring slot `b_out`
-// after `before_store()` (which waits until that slot is free) returns.
-template <int LOGM, int NPASS, class Hook>
-ZINC_DEV void encode_real_lite_body(const EncodeArgs &a, size_t b, size_t b_out, double2 *buf, Hook before_store) {
-  constexpr int M = 1 << LOGM, LH = LOGM - 1;
-  constexpr int THREADS = 256, PER = M / THREADS, HALF = PER / 2;
-  double *bufd = reinterpret_cast<double *>(buf);
-  const int tid = threadIdx.x;
-  constexpr uint32_t MASK = 4u * M - 1u;  // mod 2N
-  uint32_t g = pow5_mod_pow2((uint32_t)tid, MASK);
-  const uint32_t step = pow5_mod_pow2((uint32_t)THREADS, MASK);
-  const double *src = a.slots + b * M + tid;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    double zv[HALF];
-#pragma unroll
-    for (int i = 0; i < HALF; ++i) zv[i] = __ldg(src + (half * HALF + i) * THREADS);
-#pragma unroll
-    for (int i = 0; i < HALF; ++i) {
-      const uint32_t h = g >> 2;  // h_k = (g_k - 1) / 4
-      const int pos = (int)(__brev(h >> 1) >> (32 - LH));
-      bufd[2 * pad16(pos) + (h & 1)] = zv[i];
-      g = (g * step) & MASK;
-    }
-  }
-  __syncthreads();
-  auto lds = [&](int i) { return buf[pad16(i)]; };
-  auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
-  encode_fft<LH, THREADS, NPASS, false>(a.fft_tw_h, lds, sts);
-  __syncthreads();
-  before_store();
-  encode_real_post<LOGM, false, THREADS, false>(a, a.m_out + b_out * (2 * M), buf, a.post_tw);
-}
-
 }  // namespace zinc

@@ -94,15 +94,6 @@ __global__ void __launch_bounds__(256, (LOGM <= 13 ? 2 : 1)) encode_real_kernel(
   encode_real_body<LOGM, WIDE>(a, blockIdx.x, buf);
 }
 
-// The light variant (encode_real_lite_body): FFT buffer only in shared memory (68 KiB at
-// N = 2^14), radix-8 passes within 80 registers, so one encode CTA fits on an SM beside
-// two streaming Zinc COEFF CTAs (the side-stream overlap, ZINC_TUNE_OVERLAP = 1).
-template <int LOGM>
-__global__ void __launch_bounds__(256, 3) encode_real_lite_kernel(EncodeArgs a) {
-  extern __shared__ __align__(16) double2 buf[];
-  encode_real_lite_body<LOGM, 4>(a, blockIdx.x, blockIdx.x, buf, [] { __syncthreads(); });
-}
-
 // ============================================================ decode (C-10)
 // Mirror image of encode.  Split at M = 2^14: the first DIF stage (pairs j,
 // j + M/2) is computed by each CTA for its half straight from the global
@@ -157,10 +148,6 @@ template <int LOGM> static size_t fft_smem() {
 template <int LOGM>
 static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
   if (!a.complex_slots) {
-    if constexpr (LOGM >= 11 && LOGM <= 13) {
-      if (a.lite && !a.wide)
-        return launch_ex(encode_real_lite_kernel<LOGM>, dim3((unsigned)batch), 256, encode_real_lite_smem<LOGM>(), 1, s, a);
-    }
     if (a.wide) return launch_ex(encode_real_kernel<LOGM, true>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
     return launch_ex(encode_real_kernel<LOGM, false>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
   }

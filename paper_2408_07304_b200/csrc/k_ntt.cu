@@ -48,6 +48,10 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
     sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ZINC_E2);
   }
   __syncthreads();
+  // chained after the encode that wrote m (programmatic dependent launch): the prologue
+  // above overlapped its tail; m is read only after its grid completed
+  pdl_trigger();
+  pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];

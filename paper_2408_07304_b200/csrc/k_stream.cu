@@ -120,8 +120,14 @@ __global__ void sample_kernel(SampleArgs a) {
 }
 
 // ============================================================ integer peak (K11)
-// 8 independent register-resident lazy Shoup butterflies per iteration, the
-// same instruction mix as the NTT passes, no memory traffic.
+// 8 independent register-resident butterflies per thread per iteration, no memory
+// traffic: the measured integer peak the transform kernels are held to.  VARIANT
+// selects the butterfly the kernels actually run (common.cuh):
+//  0 ct_bfly     lazy Harvey forward butterfly, exact Shoup quotient (4 partial products)
+//  1 ct_bfly_nr  lazy-free forward butterfly (q < 2^58: every CKKS forward transform here)
+//  2 ct_bfly_a   forward butterfly with one conditional subtraction (q up to 2^60)
+//  3 gs_bfly     inverse Gentleman-Sande butterfly (every inverse transform)
+template <int VARIANT>
 __global__ void __launch_bounds__(256) int_peak_kernel(IntPeakArgs a) {
   const uint64_t q = a.q, two_q = 2 * a.q;
   uint64_t v[16];
@@ -130,7 +136,12 @@ __global__ void __launch_bounds__(256) int_peak_kernel(IntPeakArgs a) {
   uint64_t w = a.w, wp = a.wp;
   for (int it = 0; it < a.iters; ++it) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) ct_bfly(v[r], v[r + 8], w, wp, q, two_q);
+    for (int r = 0; r < 8; ++r) {
+      if constexpr (VARIANT == 0) ct_bfly(v[r], v[r + 8], w, wp, q, two_q);
+      else if constexpr (VARIANT == 1) ct_bfly_nr(v[r], v[r + 8], w, wp, q, two_q);
+      else if constexpr (VARIANT == 2) ct_bfly_a(v[r], v[r + 8], w, wp, q, 2 * two_q);
+      else gs_bfly(v[r], v[r + 8], w, wp, q, 2 * two_q);
+    }
     w += (v[0] & 1);  // keep w loop-variant so the compiler cannot hoist
   }
   uint64_t acc = 0;
@@ -159,8 +170,13 @@ cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_int_peak(const IntPeakArgs &a, int blocks, cudaStream_t s) {
-  int_peak_kernel<<<blocks, 256, 0, s>>>(a);
+cudaError_t launch_int_peak(const IntPeakArgs &a, int variant, int blocks, cudaStream_t s) {
+  switch (variant) {
+    case 0: int_peak_kernel<0><<<blocks, 256, 0, s>>>(a); break;
+    case 1: int_peak_kernel<1><<<blocks, 256, 0, s>>>(a); break;
+    case 2: int_peak_kernel<2><<<blocks, 256, 0, s>>>(a); break;
+    default: int_peak_kernel<3><<<blocks, 256, 0, s>>>(a); break;
+  }
   return cudaGetLastError();
 }
 

@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
   sample_cbd_smem<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1);
   sample_cbd_smem<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2);
   __syncthreads();
+  pdl_trigger();  // chained after the encode that wrote m: wait before reading it
+  pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
@@ -154,6 +156,8 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
   sample_cbd_parity<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1, r);
   sample_cbd_parity<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2, r);
   __syncthreads();
+  pdl_trigger();  // chained after the encode that wrote m: wait before reading it
+  pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];

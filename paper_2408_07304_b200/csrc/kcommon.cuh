@@ -184,57 +184,6 @@ inline cudaError_t set_smem(K kernel, size_t bytes) {
 
 // Programmatic dependent launch (PdlScope in kernels.h): kernels trigger their dependents
 // early and wait for their prerequisite grid before touching its outputs.
-// ---------------------------------------------------------------- inter-CTA flags
-// (the persistent pipeline's ring and the lookahead chunk chain's per-chunk counters)
-ZINC_DEV uint32_t ld_acquire(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-ZINC_DEV void st_release(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-ZINC_DEV void red_release_add(uint32_t *p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-ZINC_DEV uint64_t global_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-ZINC_DEV ulonglong2 ld2_cg(const void *p) {
-  ulonglong2 v;
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
-  return v;
-}
-
-ZINC_DEV uint32_t ld_relaxed(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Spin (one thread) until *p >= want, then acquire; on a 2 s timeout set *flag and
-// give up.  The poll is a relaxed load: an acquire load per poll invalidates the
-// SM's whole L1 (CCTL.IVALL) every iteration, which starves the encoders' twiddle
-// reads on the same SM; one acquire after the poll succeeds is enough.
-ZINC_DEV void wait_geq(const uint32_t *p, uint32_t want, uint32_t *flag) {
-  if (ld_relaxed(p) < want) {
-    const uint64_t t0 = global_ns();
-    unsigned ns = 64;
-    while (ld_relaxed(p) < want) {
-      if (ld_relaxed(flag)) return;
-      if (global_ns() - t0 > 2000000000ull) {
-        atomicExch(flag, 1u);
-        return;
-      }
-      __nanosleep(ns);
-      if (ns < 1024) ns *= 2;
-    }
-  }
-  (void)ld_acquire(p);
-}
-
 ZINC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 ZINC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 

@@ -110,7 +110,6 @@ struct EncodeArgs {
   const double2 *post_tw;   // real-slot split step: [A | B | A5 | B5] (encode_real_post)
   const double2 *twist_split;  // complex-slot twist zeta^-j = A'[j >> 6] B[j & 63], j < M: [A' | B]
   int wide;                 // m_out holds 128-bit coefficients (int64 pairs)
-  int lite;                 // real slots: the 68 KiB shared-memory encode (twiddles through L1)
   double scale;
   int64_t *m_out;
 };
@@ -148,16 +147,6 @@ struct SampleArgs {
   size_t n;
   void *out;
 };
-// Persistent encode -> Zinc COEFF pipeline (k_pipe.cu).  z.m and e.m_out are the
-// ring of `ring` int64 plaintext slots; sync holds pipe_sync_words(ring) zeroed words.
-struct PipeArgs {
-  ZincCoeffArgs z;
-  EncodeArgs e;
-  uint32_t *sync;
-  int ring, tiles;
-  int enc_per_sm;  // encoder CTAs per SM (0: only the CTAs left over by the streamers)
-  int streamers;   // set by the launcher: a multiple of tiles
-};
 struct IntPeakArgs {
   uint64_t q, w, wp;
   int iters;
@@ -166,14 +155,6 @@ struct IntPeakArgs {
 
 size_t zinc_coeff_smem(int L, int threads);
 cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, size_t smem_pad, cudaStream_t s);
-// encode chunk k+1 (enc_ctas real-slot messages) fused with Zinc COEFF of chunk k
-// (gy message groups, 256-thread tiles); see k_fused.cu
-bool fused_supported(int log_n, int L);
-cudaError_t launch_zinc_coeff_encode(int log_n, const ZincCoeffArgs &za, int gy, const EncodeArgs &ea, int enc_ctas,
-                                     cudaStream_t s);
-bool pipe_supported(int log_n, int L);
-size_t pipe_sync_words(int ring, int tiles);
-cudaError_t launch_zinc_pipe(int log_n, const PipeArgs &p, int variant, int num_sms, cudaStream_t s);
 cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                            cudaStream_t s);
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s);
@@ -188,6 +169,6 @@ cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaS
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
 cudaError_t launch_ct_add(const CtAddArgs &a, cudaStream_t s);
 cudaError_t launch_ct_sum(const CtSumArgs &a, cudaStream_t s);
-cudaError_t launch_int_peak(const IntPeakArgs &a, int blocks, cudaStream_t s);
+cudaError_t launch_int_peak(const IntPeakArgs &a, int variant, int blocks, cudaStream_t s);
 
 }  // namespace zinc

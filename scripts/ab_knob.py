@@ -11,7 +11,21 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2408_07304_b200 as Z  # noqa: E402
 from workloads import CONFIGS, slots_batch  # noqa: E402
-from sweep_zinc import timeit  # noqa: E402
+
+
+def timeit(fn, reps=5, warm=1):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
 
 knob, v0, v1 = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
 cfg = CONFIGS[sys.argv[4] if len(sys.argv) > 4 else "C3"]

@@ -1,7 +1,7 @@
 """Small end-to-end run of every kernel for compute-sanitizer (one tool per
 gpurun call): C1 (N=2^12) and a 2-message N=2^15 batch (the cluster-split
 kernels), CKKS / BFV / BGV, both forms, encode / decrypt / decode, Eq. 2 kernels,
-the encode-fused Zinc pipeline.  Exits non-zero on any library error."""
+the PDL-chained encode -> path chunk pipelines.  Exits non-zero on any library error."""
 import os
 import sys
 
@@ -30,12 +30,15 @@ def run(cfg, B, scheme=0, t=0):
             assert int(st.sum()) == 0
             Z.zinc_ct_sum_batch(ctx, Z.zinc_ct_add_batch(ctx, ct, ct))
     if scheme == 0:
-        for mode in (0, 1, 2, 3):
-            Z.tune(Z.TUNE_OVERLAP, mode)
+        for pdl in (0, 1):  # multi-chunk chains (double-buffered scratch), with and without PDL
+            Z.tune(Z.TUNE_PDL, pdl)
             Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, 1 << 16)
+            Z.tune(Z.TUNE_NTT_CHUNK_MSGS, 1)
             Z.zinc_encrypt_batch(ctx, Z.zinc_precompute_cache(ctx, pk, 2, Z.COEFF), Z.COEFF, pt, 3, 0)
-        Z.tune(Z.TUNE_OVERLAP, 0)
+            Z.ckks_encrypt_batch(ctx, pk, Z.NTT, pt, 3, 0)
+        Z.tune(Z.TUNE_PDL, 1)
         Z.tune(Z.TUNE_ENCODE_CHUNK_BYTES, 32 << 20)
+        Z.tune(Z.TUNE_NTT_CHUNK_MSGS, 0)
     torch.cuda.synchronize()
     ctx.close()
 

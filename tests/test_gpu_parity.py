@@ -310,106 +310,109 @@ def test_full_size_c3_bench_launch_sampled(Z, orc, path):
         assert np.array_equal(got[b], want), b
 
 
-def test_int_peak_kernel_runs(Z, orc):
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_int_peak_kernel_runs(Z, orc, variant):
     s = setup_for(Z, orc, "C3")
     sink = torch.zeros(2, dtype=torch.uint64, device="cuda")
-    bf = Z.zinc_int_peak(s.ctx, 148 * 4, 100, sink)
+    bf = Z.zinc_int_peak(s.ctx, 148 * 4, 100, sink, variant=variant)
     torch.cuda.synchronize()
     assert bf == 148 * 4 * 256 * 8 * 100
+    with pytest.raises(Z.ZincError):
+        Z.zinc_int_peak(s.ctx, 1, 1, sink, variant=4)
 
 
-@pytest.mark.parametrize("knobs", [{0: 1, 1: 1 << 20, 2: 1, 3: 0}, {0: 7, 1: 3 << 20, 2: 0, 3: 12 << 10},
-                                   {0: 2, 1: 1 << 20, 2: 1, 3: 12 << 10}, {0: 3, 1: 1 << 20, 2: 0, 4: 0, 7: 0},
-                                   {0: 2, 1: 2 << 20, 2: 2, 4: 1}, {8: 2}, {2: 1, 3: 12 << 10, 8: 1}])
+@pytest.mark.parametrize("knobs", [
+    {0: 1, 1: 1 << 20, 2: 1},                 # 8-message chunks, PDL chain over 9 chunks
+    {0: 7, 1: 3 << 20, 2: 0, 3: 0},           # plain stream order, no prefetch
+    {0: 2, 1: 1 << 20, 3: 0},
+    {4: 7},                                   # transform paths: 7-message chunks, PDL chain
+    {4: 5, 2: 0},                             # transform paths: 5-message chunks, stream order
+    {4: 1},                                   # one message per chunk
+])
 def test_tuning_knobs_never_change_results(Z, orc, knobs):
-    """Launch geometry (messages per CTA, encode chunk, side-stream / fused overlap, smem
-    reservation, programmatic dependent launch) changes timing only: ciphertexts stay
-    bit-identical (the default reference uses PDL-chained chunks)."""
+    """Launch geometry (messages per CTA, encode chunk sizes, programmatic dependent launch,
+    L2 prefetch) changes timing only: ciphertexts stay bit-identical to the default
+    configuration, across chains of many chunks (the double-buffered scratch is reused)."""
     s = setup_for(Z, orc, "C3")
     z = torch.from_numpy(slots_batch(s.cfg, 0, 70)).cuda()
-    ref = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 3, 10)
-    ref_v = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z[:9], 3, 10)
-    old = {k: Z.tune(k, v) for k, v in knobs.items()}
-    try:
-        got = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 3, 10)
-        got_v = Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z[:9], 3, 10)
-        torch.cuda.synchronize()
-    finally:
-        for k, v in old.items():
-            Z.tune(k, v)
-    assert torch.equal(ref, got) and torch.equal(ref_v, got_v)
-
-
-@pytest.mark.parametrize("name,batch,ring,enc,mpc,variant", [
-    ("C3", 70, 256, 1, 2, 0), ("C3", 70, 2, 0, 2, 0), ("C3", 33, 3, 2, 3, 1), ("C3", 1, 256, 1, 2, 2),
-    ("C3", 300, 16, 2, 1, 0), ("C1", 257, 4, 0, 2, 0), ("C2", 129, 8, 5, 4, 2), ("C2", 40, 40, 1, 8, 1)])
-def test_persistent_pipeline_bit_exact(Z, orc, name, batch, ring, enc, mpc, variant):
-    """The persistent encode -> Zinc COEFF pipeline (ZINC_TUNE_OVERLAP = 3: encoder CTAs fill a
-    ring of L2-resident plaintexts that streamer CTAs consume) gives the serial path's
-    ciphertexts bit for bit, including a ring as small as one work item (many laps per slot),
-    only the leftover CTAs encoding, more encoders than messages, and ragged batches; and the
-    oracle's."""
-    s = setup_for(Z, orc, name)
-    z = torch.from_numpy(slots_batch(s.cfg, 0, batch)).cuda()
-    ref = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 5, 1000)
-    knobs = {Z.TUNE_OVERLAP: 3, Z.TUNE_ENCODE_CHUNK_BYTES: ring * s.cfg.n * 8, Z.TUNE_PIPE_ENC_CTAS: enc,
-             Z.TUNE_COEFF_MSGS_PER_CTA: mpc, Z.TUNE_PIPE_VARIANT: variant}
-    old = {k: Z.tune(k, v) for k, v in knobs.items()}
-    try:
-        Z.launch_count_reset()
-        got = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 5, 1000)
-        torch.cuda.synchronize()
-        launches = Z.launch_count()
-    finally:
-        for k, v in old.items():
-            Z.tune(k, v)
-    assert launches == 1                      # one persistent launch for the whole batch
-    assert torch.equal(ref, got)
-    m = Z.ckks_encode_batch(s.ctx, z[-1:]).cpu().numpy()[0]
-    want = orc.zinc_encrypt(s.P, orc.precompute_cache(s.P, s.o_pk, s.cfg.cache_seed, COEFF), COEFF, m, 5,
-                            1000 + batch - 1)
-    assert np.array_equal(got[-1].cpu().numpy(), want)
-
-
-@pytest.mark.parametrize("name", ["C3", "C4"])
-def test_persistent_pipeline_falls_back_where_unsupported(Z, orc, name):
-    """With ZINC_TUNE_OVERLAP = 3, calls the persistent kernel does not cover (complex slots,
-    int64 plaintexts, NTT form, the vanilla path, the host-buffer call's chunks) give the
-    default path's ciphertexts."""
-    s = setup_for(Z, orc, name)
-    z = slots_batch(s.cfg, 0, 9)
-    if s.cfg.complex_slots:
-        z = np.stack([z.real, z.imag], axis=-1)
-    z = torch.from_numpy(np.ascontiguousarray(z)).cuda()
-    m = Z.ckks_encode_batch(s.ctx, z)
-    calls = [lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 4, 7),
-             lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, m, 4, 7),
-             lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, z, 4, 7),
-             lambda: Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, z[:3], 4, 7)]
+    calls = [lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, 3, 10),
+             lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, z[:23], 3, 10),
+             lambda: Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z[:17], 3, 10),
+             lambda: Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, z[:11], 3, 10)]
     ref = [f() for f in calls]
-    old = Z.tune(Z.TUNE_OVERLAP, 3)
+    old = {k: Z.tune(k, v) for k, v in knobs.items()}
     try:
         got = [f() for f in calls]
         torch.cuda.synchronize()
     finally:
-        Z.tune(Z.TUNE_OVERLAP, old)
+        for k, v in old.items():
+            Z.tune(k, v)
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
 
 
-def test_persistent_pipeline_through_host_call(Z, orc):
-    """The host-buffer call (pinned in/out, two streams) with the persistent kernel per chunk
-    gives the device call's ciphertexts (ragged last chunk)."""
+def test_c4_complex_slot_chain_bit_exact(Z, orc):
+    """C4 complex slots (2-CTA cluster encode at N = 2^15) through a multi-chunk chain:
+    2-message encode chunks, PDL on and off, equal to one another and to the oracle's
+    encryption of the GPU-encoded plaintexts (first, middle and last chunk)."""
+    s = setup_for(Z, orc, "C4")
+    z = slots_batch(s.cfg, 0, 9)
+    zz = torch.from_numpy(np.ascontiguousarray(np.stack([z.real, z.imag], axis=-1))).cuda()
+    m = np64(Z.ckks_encode_batch(s.ctx, zz))
+    outs = []
+    for pdl in (1, 0):
+        old = {k: Z.tune(k, v) for k, v in {Z.TUNE_ENCODE_CHUNK_BYTES: 2 * s.cfg.n * 8, Z.TUNE_PDL: pdl}.items()}
+        try:
+            outs.append(Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, zz, 21, 300))
+            torch.cuda.synchronize()
+        finally:
+            for k, v in old.items():
+                Z.tune(k, v)
+    assert torch.equal(outs[0], outs[1])
+    _check_msgs(orc, s, "zinc", COEFF, m, np64(outs[0]), 21, 300, [0, 1, 4, 8])
+
+
+def _full_size_slots_check(Z, orc, path, form, idx_fn):
+    """Full C3 (16384 messages x 8192 slots, the A13 mix) from slots with the default
+    launch configuration (the bench's timed call): sampled messages of the first, middle
+    and last chunks bit-exact against the oracle's encryption of the GPU-encoded m."""
     s = setup_for(Z, orc, "C3")
-    zh = torch.from_numpy(np.ascontiguousarray(slots_batch(s.cfg, 0, 21))).pin_memory()
-    ref = Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, zh.cuda(), 6, 50).cpu()
-    out = torch.empty(ref.shape, dtype=torch.uint64).pin_memory()
-    old = Z.tune(Z.TUNE_OVERLAP, 3)
-    try:
-        Z.zinc_encrypt_batch_host(s.ctx, Z.PATH_ZINC, s.cache[COEFF], COEFF, zh, 6, 50, out, chunk=8)
-    finally:
-        Z.tune(Z.TUNE_OVERLAP, old)
-    assert torch.equal(ref, out)
+    cfg = s.cfg
+    B = cfg.batch
+    z = slots_batch(cfg, 0, B)
+    zd = torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    seed = cfg.enc_seed
+    if path == "zinc":
+        ct = Z.zinc_encrypt_batch(s.ctx, s.cache[form], form, zd, seed, 0)
+    else:
+        ct = Z.ckks_encrypt_batch(s.ctx, s.pk, form, zd, seed, 0)
+    torch.cuda.synchronize()
+    idx = idx_fn(B)
+    got = {b: ct[b].cpu().numpy() for b in idx}
+    m = np64(Z.ckks_encode_batch(s.ctx, zd[idx].contiguous()))
+    del ct, zd
+    torch.cuda.empty_cache()
+    key = s.o_pk if path == "vanilla" else orc.precompute_cache(s.P, s.o_pk, cfg.cache_seed, form)
+    for k, b in enumerate(idx):
+        if path == "vanilla":
+            want = orc.vanilla_encrypt(s.P, key, m[k], seed, b, form)
+        else:
+            want = orc.zinc_encrypt(s.P, key, form, m[k], seed, b)
+        assert np.array_equal(got[b], want), (path, form, b)
+
+
+def test_full_size_c3_slots_zinc_coeff_every_region(Z, orc):
+    """The headline timed path: Zinc COEFF from slots, 64 PDL-chained 256-message chunks."""
+    chunk = 256
+    _full_size_slots_check(Z, orc, "zinc", COEFF, lambda B: [0, 1, chunk - 1, chunk, 31 * chunk + 7, 32 * chunk,
+                                                             B // 2 - 1, B // 2, B - chunk, B - 2, B - 1])
+
+
+@pytest.mark.parametrize("path,form", [("zinc", NTT), ("vanilla", NTT), ("vanilla", COEFF)])
+def test_full_size_c3_slots_transform_paths(Z, orc, path, form):
+    """Zinc NTT form and vanilla (both forms) from slots at full C3: chunks of 16 waves
+    (4736 messages on 148 SMs), sampled in the first, middle and last chunk."""
+    _full_size_slots_check(Z, orc, path, form, lambda B: [0, 4735, 4736, 8191, 9472, B - 1])
 
 
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
