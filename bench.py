@@ -567,13 +567,13 @@ def main():
             peak_p = (nf + ni) / (nf / k11[fwd_v] + ni / k11[3])
             pd = (nf + ni) / (nf / alu_peak_derived(sm_mhz, BFLY[fwd_v][2]) + ni / alu_peak_derived(sm_mhz, BFLY[3][2]))
             kms = prof_path[p].get(kname, (0.0, 0))[0]
-            bpc = butterflies_per_ct(cfg, p)
-            ach = bpc * B / (seg[p] / 1e3)
-            kach = bpc * B / (kms / 1e3) if kms else ach
+            bfc = butterflies_per_ct(cfg, p)
+            ach = bfc * B / (seg[p] / 1e3)
+            kach = bfc * B / (kms / 1e3) if kms else ach
             alu[p] = {"bound": "alu", "kernel": kname, "achieved": kach / 1e9, "peak": peak_p / 1e9,
                       "unit": "Gbutterfly/s", "frac": kach / peak_p, "achieved_path": ach / 1e9,
                       "frac_path": ach / peak_p, "peak_derived": pd / 1e9, "frac_of_derived": kach / pd,
-                      "butterflies_per_ct": bpc, "transforms_per_ct": {"forward": nf, "inverse": ni},
+                      "butterflies_per_ct": bfc, "transforms_per_ct": {"forward": nf, "inverse": ni},
                       "peak_source": f"measured K11 int_peak_kernel with the path's own butterflies: {nf} x "
                                      f"{BFLY[fwd_v][0]} + {ni} x {BFLY[3][0]} per ct (harmonic mix); peak_derived: "
                                      f"148 SMs x sm_mhz x 64 fma-pipe lanes/clk / SASS fma ops per butterfly "

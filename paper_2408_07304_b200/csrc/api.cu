@@ -110,7 +110,7 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {1}, {1}, {0}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {1}, {1}, {0}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -540,6 +540,8 @@ static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, c
   a.msgs_per_cta = (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load());
   return a;
 }
+// The S-CTA cluster transform kernels (k_split.cu) serve N = 2^14 and 2^15.
+static bool use_split(const zinc_ctx *c) { return c->log_n >= 14 && g_tune[ZINC_TUNE_SPLIT].load() != 0; }
 static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
   size_t want = 2 * (size_t)c->num_sms;
   if (batch >= want) return c->L;
@@ -573,7 +575,10 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
-    LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, kernel_mode(c), batch, groups, s));
+    if (use_split(c))
+      LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt_split(c->log_n, a, kernel_mode(c), batch, groups, s));
+    else
+      LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, kernel_mode(c), batch, groups, s));
     return ZINC_OK;
   }
   VanillaArgs a{};
@@ -587,7 +592,10 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
-  LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, kernel_mode(c), batch, groups, s));
+  if (use_split(c))
+    LAUNCH(ZINC_K_VANILLA, s, launch_vanilla_split(c->log_n, a, form, kernel_mode(c), batch, groups, s));
+  else
+    LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, kernel_mode(c), batch, groups, s));
   return ZINC_OK;
 }
 
@@ -828,7 +836,8 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
     cudaError_t e;
     {
       TraceScope ts(ZINC_K_DECRYPT, s);
-      e = launch_decrypt(c->log_n, a, form, batch, s);
+      e = use_split(c) ? launch_decrypt_split(c->log_n, a, form, kernel_mode(c) == 0, batch, s)
+                       : launch_decrypt(c->log_n, a, form, batch, s);
     }
     g_launches.fetch_add(1);
     if (e != cudaSuccess) st = fail(ZINC_ECUDA, "decrypt launch: %s", cudaGetErrorString(e));

@@ -1,0 +1,418 @@
+// k_split.cu -- the transform paths at N = 2^14 and 2^15 on S-CTA thread-block clusters
+// (ntt.cuh, ntt_forward_split / ntt_inverse_split): Zinc NTT form,
+// vanilla encryption in both forms (Eq. 8) and decryption (Eq. 10,
+// PAPER.md:224-227).  Every CTA holds 2^12 words of one limb (34 KiB + samples + 4 KiB of
+// staged twiddles, 256 threads), three CTAs per SM.
+#include "kcommon.cuh"
+
+namespace zinc {
+
+// ============================================================ samplers (C-4) on a share
+// CBD samples of the coefficients x = S i + r (the forward split's subsequence), at i.
+template <int THREADS>
+ZINC_DEV void sample_cbd_sub(int8_t *dst, int nl, int S, int r, uint64_t seed, uint64_t msg, uint32_t tag) {
+  for (int i = threadIdx.x; i < nl; i += THREADS) {
+    const int x = S * i + r;
+    const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)(x >> 1));
+    dst[i] = (int8_t)((x & 1) ? cbd_hi(w) : cbd_lo(w));
+  }
+}
+// Ternary samples of x = S i + r (S >= 4: word r & 3 of block x >> 2), packed 2 bits at i.
+template <int THREADS>
+ZINC_DEV void sample_ternary_sub(uint8_t *dst, int nl, int S, int r, uint64_t seed, uint64_t msg, uint32_t tag) {
+  const int wsel = r & 3;
+  for (int i4 = threadIdx.x; i4 < nl / 4; i4 += THREADS) {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int x = S * (4 * i4 + h) + r;
+      const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)(x >> 2));
+      const uint32_t word = wsel == 0 ? w.x : wsel == 1 ? w.y : wsel == 2 ? w.z : w.w;
+      packed |= (uint32_t)(tern(word) + 1) << (2 * h);
+    }
+    dst[i4] = (uint8_t)packed;
+  }
+}
+// CBD samples of the inverse split's outputs: positions j + c NL, j in [r NL/S, (r+1) NL/S),
+// stored at c (NL/S) + (j - r NL/S).  Pairs of adjacent coefficients share a Philox block.
+template <int THREADS>
+ZINC_DEV void sample_cbd_inv(int8_t *dst, int nl, int S, int r, uint64_t seed, uint64_t msg, uint32_t tag) {
+  const int span = nl / S;
+  for (int l2 = threadIdx.x; l2 < nl / 2; l2 += THREADS) {
+    const int l = 2 * l2, c = l / span, jj = l % span;
+    const int x = c * nl + r * span + jj;  // even
+    const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)(x >> 1));
+    dst[l] = (int8_t)cbd_lo(w);
+    dst[l + 1] = (int8_t)cbd_hi(w);
+  }
+}
+// index of output position x in the sample_cbd_inv layout of CTA r
+template <int LOGN>
+ZINC_DEV int inv_sample_idx(int x, int r) {
+  using G = SplitGeo<LOGN>;
+  constexpr int span = G::NL / G::S;
+  return (x >> G::LL) * span + (x & (G::NL - 1)) - r * span;
+}
+
+template <int LOGN> struct SplitSmem {
+  using G = SplitGeo<LOGN>;
+  static constexpr size_t DATA = SmemWords<G::LL>::value * sizeof(uint64_t);  // 34816
+  static constexpr size_t TW = G::STW * sizeof(Tw);                          // 4096
+};
+
+// ============================================================ Zinc, NTT form
+// c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2'): both transforms through one copy of
+// the transform code (t at run time); the exchange streams cache-added words to HBM.
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
+  constexpr bool INTS = MODE == 2, NR = MODE == 0;
+  using G = SplitGeo<LOGN>;
+  constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
+  int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
+  __shared__ __align__(8) uint64_t tw_mbar;
+  TwStager tws{&tw_mbar, 0};
+  const size_t b = blockIdx.x / S;
+  const int r = (int)cluster_rank();
+  const uint64_t msg = a.msg_base + b;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  tws.init();
+  __syncthreads();
+  tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
+  sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
+  sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ZINC_E2);
+  __syncthreads();
+  pdl_trigger();  // chained after the encode that wrote m: wait before reading it
+  pdl_wait();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    tws.wait();
+#pragma unroll 1
+    for (int t = 0; t < 2; ++t) {
+      const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
+      uint64_t *ctt = ct0 + (size_t)t * L * N;
+      ntt_forward_split<LOGN, NR>(sm, tw, q, ZincTLoad<INTS, G::LOGS>{m, t ? se2 : se1, c, t},
+          [&](int x0, uint64_t (&v)[S]) {
+#pragma unroll
+            for (int u = 0; u < S; u += 2) {
+              const ulonglong2 zz = ld2_nc(z + x0 + u);
+              st2_cs(ctt + x0 + u, add_mod(zz.x, canon(v[u]), q), add_mod(zz.y, canon(v[u + 1]), q));
+            }
+          },
+          stw, [&]() {
+            if (t == 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
+          });
+    }
+  }
+}
+
+// ============================================================ vanilla, NTT form
+// NTT(m + e1) -> ct0, NTT(e2) -> ct1, NTT(u) -> ct0 += pk1 u^, ct1 += pk2 u^ (Eq. 8, A1).
+// The three transforms of a limb run through one copy of the transform code; every
+// exchange thread re-reads only the ciphertext words it wrote itself.
+template <bool INTS, int SHIFT>
+struct VanTLoad {
+  const int64_t *m;
+  const int8_t *se1, *se2;
+  const uint8_t *su;
+  const LimbConst &c;
+  int t;
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? __ldg(m + x) : 0; }
+  ZINC_DEV uint64_t lift(int64_t raw, int x) const {
+    const int i = x >> SHIFT;
+    return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
+                                                             : reduce_small(tern_at(su, i), c.q);
+  }
+  ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
+};
+
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a) {
+  constexpr bool INTS = MODE == 2, NR = MODE == 0;
+  using G = SplitGeo<LOGN>;
+  constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
+  int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
+  uint8_t *su = reinterpret_cast<uint8_t *>(se2 + NL);
+  __shared__ __align__(8) uint64_t tw_mbar;
+  TwStager tws{&tw_mbar, 0};
+  const size_t b = blockIdx.x / S;
+  const int r = (int)cluster_rank();
+  const uint64_t msg = a.msg_base + b;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  tws.init();
+  __syncthreads();
+  tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
+  sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
+  sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
+  sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N;
+    const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    tws.wait();
+#pragma unroll 1
+    for (int t = 0; t < 3; ++t) {
+      ntt_forward_split<LOGN, NR>(sm, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t},
+          [&](int x0, uint64_t (&v)[S]) {
+            if (t < 2) {
+              uint64_t *dst = (t ? ct1 : ct0) + x0;
+#pragma unroll
+              for (int u = 0; u < S; u += 2) st2(dst + u, canon(v[u]), canon(v[u + 1]));
+            } else {
+#pragma unroll
+              for (int u = 0; u < S; u += 2) {
+                const uint64_t u0 = canon(v[u]), u1 = canon(v[u + 1]);
+                const ulonglong2 p1 = ld2_nc(pk1 + x0 + u), p2 = ld2_nc(pk2 + x0 + u);
+                uint64_t a0, a1, b0, b1;
+                ld2(ct0 + x0 + u, a0, a1);
+                ld2(ct1 + x0 + u, b0, b1);
+                st2_cs(ct0 + x0 + u, add_mod(a0, mul_mod(p1.x, u0, c), q), add_mod(a1, mul_mod(p1.y, u1, c), q));
+                st2_cs(ct1 + x0 + u, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
+              }
+            }
+          },
+          stw, [&]() {
+            if (t == 2 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
+          });
+    }
+  }
+}
+
+// ============================================================ vanilla, COEFF form
+// NTT(u) (forward split; its exchange reads every input first, so it can write the
+// pointwise product pk1 u^ straight into this CTA's share, and pk2 u^ to ct1 as a
+// temporary); INTT(pk1 u^) + e1 + m -> ct0; INTT(ct1) + e2 -> ct1.  The forward output
+// range of a CTA is its inverse input range: no data moves between CTAs in between.
+template <int LOGN, int MODE>
+__global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs a) {
+  constexpr bool INTS = MODE == 2, NR = MODE == 0;
+  using G = SplitGeo<LOGN>;
+  constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
+  extern __shared__ __align__(16) uint64_t sm[];
+  Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
+  int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
+  uint8_t *su = reinterpret_cast<uint8_t *>(se2 + NL);
+  __shared__ __align__(8) uint64_t tw_mbar;
+  TwStager tws{&tw_mbar, 0};
+  const size_t b = blockIdx.x / S;
+  const int r = (int)cluster_rank();
+  const uint64_t msg = a.msg_base + b;
+  const int L = a.L;
+  const int lo = blockIdx.y * a.limbs_per_cta;
+  const int hi = min(L, lo + a.limbs_per_cta);
+  tws.init();
+  __syncthreads();
+  tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
+  sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
+  sample_cbd_inv<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
+  sample_cbd_inv<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  const int64_t *m = a.m ? a.m + b * N : nullptr;
+  for (int i = lo; i < hi; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const Tw *tw = a.tw + (size_t)i * N, *itw = a.itw + (size_t)i * N;
+    const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
+    uint64_t *ct1 = ct0 + (size_t)L * N;
+    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    tws.wait();
+    ntt_forward_split<LOGN, NR, true>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> G::LOGS), q); },
+        [&](int x0, uint64_t (&v)[S]) {
+#pragma unroll
+          for (int u = 0; u < S; u += 2) {
+            const uint64_t u0 = canon(v[u]), u1 = canon(v[u + 1]);
+            const ulonglong2 p1 = ld2_nc(pk1 + x0 + u), p2 = ld2_nc(pk2 + x0 + u);
+            st2(ct1 + x0 + u, mul_mod(p2.x, u0, c), mul_mod(p2.y, u1, c));  // temporary: pk2 u^
+            sm[pad16(x0 + u - r * NL)] = mul_mod(p1.x, u0, c);             // this CTA's inverse input
+            sm[pad16(x0 + u + 1 - r * NL)] = mul_mod(p1.y, u1, c);
+          }
+        },
+        stw, [&]() {
+          if (i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
+        });
+    ntt_inverse_split<LOGN, false>(sm, itw, c, [](int, uint64_t (&)[16]) {},
+        [&](int x, uint64_t v) {
+          const uint64_t e = pt_plus_e<INTS>(m ? __ldg(m + x) : 0, se1[inv_sample_idx<LOGN>(x, r)], c);
+          __stcs(ct0 + x, add_mod(csub(v, q), e, q));
+        });
+    ntt_inverse_split<LOGN, true>(sm, itw, c,
+        [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+          for (int u = 0; u < 16; u += 2) ld2(ct1 + base + u, v[u], v[u + 1]);
+        },
+        [&](int x, uint64_t v) {
+          __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[inv_sample_idx<LOGN>(x, r)], c), q));
+        });
+  }
+}
+
+// ============================================================ decrypt (Eq. 10)
+// x^(i) = [c1 + c2 s]_{q_i} per limb, limbs in order; limb 0 writes x0 = the centred
+// residue mod q_0, every other limb checks x0 mod q_i == x^(i) (C-10); BGV / BFV / wide
+// CKKS as decrypt_kernel (k_ntt.cu).  COEFF form: forward split of c2 (its exchange writes
+// c2^ s straight into this CTA's share), inverse split, + c1.  NTT form: inverse split of
+// c1 + c2 s read from global memory.  Each output position is handled by the same thread
+// in every limb, so the CRT check re-reads only words the thread wrote itself.
+template <int LOGN, int FORM, bool NR>
+__global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
+  using G = SplitGeo<LOGN>;
+  constexpr int N = 1 << LOGN, S = G::S, NL = G::NL;
+  extern __shared__ __align__(16) uint64_t sm[];
+  __shared__ int bad_flag;
+  const size_t b = blockIdx.x / S;
+  const int r = (int)cluster_rank();
+  const int L = a.L;
+  int bad = 0;
+  int64_t *x0 = a.coeff_out + b * N;
+  const uint64_t q0 = a.limbs[0].q;
+  for (int i = 0; i < L; ++i) {
+    const LimbConst c = a.limbs[i];
+    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t *c1 = a.ct + b * 2 * L * N + (size_t)i * N;
+    const uint64_t *c2 = c1 + (size_t)L * N;
+    const uint64_t *s = a.sk_ntt + (size_t)i * N;
+    const Tw *itw = a.itw + (size_t)i * N;
+    auto epilogue = [&](int x, uint64_t v) {
+      uint64_t xi = csub(v, q);
+      if (FORM == 1) xi = add_mod(xi, __ldg(c1 + x), q);
+      if (c.scheme == SCHEME_BFV) {
+        a.xl_out[(b * L + i) * N + x] = xi;
+        return;
+      }
+      if (a.x128_out) {  // wide CKKS: x from limbs 0 and 1, checked on the others
+        int64_t *xw = a.x128_out + (b * N + x) * 2;
+        if (i == 0) {
+          xw[0] = (int64_t)xi;
+        } else if (i == 1) {
+          const uint64_t xa = (uint64_t)xw[0];
+          const uint64_t x0r = reduce_i64q((int64_t)xa, q, c.mu64);
+          const uint64_t k = mul_mod(add_mod(xi, x0r ? q - x0r : 0, q), a.q0inv_q1, c);
+          unsigned __int128 X = (unsigned __int128)k * q0 + xa;
+          const unsigned __int128 Q2 = (unsigned __int128)q0 * q;
+          __int128 Xs = (X > Q2 / 2) ? (__int128)X - (__int128)Q2 : (__int128)X;
+          xw[0] = (int64_t)(uint64_t)Xs;
+          xw[1] = (int64_t)(Xs >> 64);
+        } else if (reduce_i128(xw[1], (uint64_t)xw[0], c) != xi) {
+          bad = 1;
+        }
+        return;
+      }
+      if (i == 0) {
+        x0[x] = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
+      } else {
+        if (reduce_i64(x0[x], c) != xi) bad = 1;
+      }
+      if (c.scheme == SCHEME_BGV && i == L - 1) x0[x] = (int64_t)mod_t(x0[x], c.t, c.t_mu);
+    };
+    if (FORM == 0) {
+      ntt_inverse_split<LOGN, true>(sm, itw, c,
+          [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              v[u] = add_mod(__ldg(c1 + base + u), mul_mod(__ldg(c2 + base + u), __ldg(s + base + u), c), q);
+          },
+          epilogue);
+    } else {
+      const Tw *tw = a.tw + (size_t)i * N;
+      // the forward split reads its early-pass twiddles from global memory here (stw = tw)
+      ntt_forward_split<LOGN, NR, true>(sm, tw, q, [&](int x) { return __ldg(c2 + x); },
+          [&](int x0g, uint64_t (&v)[S]) {
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+              const uint64_t w = NR ? reduce64(v[u], q, c.mu64) : canon8(v[u], q, two_q);
+              sm[pad16(x0g + u - r * NL)] = mul_mod(w, __ldg(s + x0g + u), c);
+            }
+          },
+          tw);
+      ntt_inverse_split<LOGN, false>(sm, itw, c, [](int, uint64_t (&)[16]) {}, epilogue);
+    }
+  }
+  bad = __syncthreads_or(bad);
+  // the cluster's verdict: every CTA publishes its flag, rank 0 reads them over DSMEM
+  if (threadIdx.x == 0) bad_flag = bad;
+  cluster_sync_all();
+  if (threadIdx.x == 0 && r == 0 && a.status_out) {
+    int any = 0;
+    for (int cc = 0; cc < S; ++cc) any |= *peer_smem(&bad_flag, (uint32_t)cc);
+    a.status_out[b] = any;
+  }
+  cluster_sync_all();
+}
+
+// ============================================================ launchers
+template <int LOGN> static size_t split_smem(int extra) {
+  return SplitSmem<LOGN>::DATA + SplitSmem<LOGN>::TW + (size_t)extra;
+}
+template <int LOGN>
+static cudaError_t launch_zinc_ntt_split_t(const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
+  using G = SplitGeo<LOGN>;
+  const dim3 grid((unsigned)(batch * G::S), groups);
+  const size_t smem = split_smem<LOGN>(2 * G::NL);
+  if (mode == 2) return launch_ex(zinc_ntt_split_kernel<LOGN, 2>, grid, G::THREADS, smem, G::S, s, a);
+  if (mode == 1) return launch_ex(zinc_ntt_split_kernel<LOGN, 1>, grid, G::THREADS, smem, G::S, s, a);
+  return launch_ex(zinc_ntt_split_kernel<LOGN, 0>, grid, G::THREADS, smem, G::S, s, a);
+}
+template <int LOGN>
+static cudaError_t launch_vanilla_split_t(const VanillaArgs &a, int form, int mode, size_t batch, int groups,
+                                          cudaStream_t s) {
+  using G = SplitGeo<LOGN>;
+  const dim3 grid((unsigned)(batch * G::S), groups);
+  const size_t smem = split_smem<LOGN>(2 * G::NL + G::NL / 4);
+#define VS(K, M) launch_ex(K<LOGN, M>, grid, G::THREADS, smem, G::S, s, a)
+  if (form == 0) return mode == 2 ? VS(vanilla_ntt_split_kernel, 2) : mode == 1 ? VS(vanilla_ntt_split_kernel, 1)
+                                                                            : VS(vanilla_ntt_split_kernel, 0);
+  return mode == 2 ? VS(vanilla_coeff_split_kernel, 2) : mode == 1 ? VS(vanilla_coeff_split_kernel, 1)
+                                                               : VS(vanilla_coeff_split_kernel, 0);
+#undef VS
+}
+template <int LOGN>
+static cudaError_t launch_decrypt_split_t(const DecryptArgs &a, int form, bool nr, size_t batch, cudaStream_t s) {
+  using G = SplitGeo<LOGN>;
+  const dim3 grid((unsigned)(batch * G::S));
+  const size_t smem = SplitSmem<LOGN>::DATA;
+  if (form == 0) return launch_ex(decrypt_split_kernel<LOGN, 0, false>, grid, G::THREADS, smem, G::S, s, a);
+  if (nr) return launch_ex(decrypt_split_kernel<LOGN, 1, true>, grid, G::THREADS, smem, G::S, s, a);
+  return launch_ex(decrypt_split_kernel<LOGN, 1, false>, grid, G::THREADS, smem, G::S, s, a);
+}
+
+cudaError_t launch_zinc_ntt_split(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
+  if (log_n == 14) return launch_zinc_ntt_split_t<14>(a, mode, batch, groups, s);
+  if (log_n == 15) return launch_zinc_ntt_split_t<15>(a, mode, batch, groups, s);
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_vanilla_split(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
+                                 cudaStream_t s) {
+  if (log_n == 14) return launch_vanilla_split_t<14>(a, form, mode, batch, groups, s);
+  if (log_n == 15) return launch_vanilla_split_t<15>(a, form, mode, batch, groups, s);
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_decrypt_split(int log_n, const DecryptArgs &a, int form, bool nr, size_t batch, cudaStream_t s) {
+  if (log_n == 14) return launch_decrypt_split_t<14>(a, form, nr, batch, s);
+  if (log_n == 15) return launch_decrypt_split_t<15>(a, form, nr, batch, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace zinc

@@ -170,6 +170,14 @@ struct TwStager {
       bulk_g2s(dst, src, (uint32_t)(kSmemTw * sizeof(Tw)), mbar);
     }
   }
+  // the first `count` entries only (count * 16 bytes)
+  ZINC_DEV void issue_n(Tw *dst, const Tw *src, int count) {
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(mbar, (uint32_t)(count * sizeof(Tw)));
+      bulk_g2s(dst, src, (uint32_t)(count * sizeof(Tw)), mbar);
+    }
+  }
   ZINC_DEV void wait() {
     mbar_wait(mbar, phase);
     phase ^= 1u;

@@ -158,6 +158,11 @@ cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, s
 cudaError_t launch_vanilla(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                            cudaStream_t s);
 cudaError_t launch_zinc_ntt(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s);
+// S-CTA cluster kernels for N = 2^14, 2^15 (k_split.cu)
+cudaError_t launch_zinc_ntt_split(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s);
+cudaError_t launch_vanilla_split(int log_n, const VanillaArgs &a, int form, int mode, size_t batch, int groups,
+                                 cudaStream_t s);
+cudaError_t launch_decrypt_split(int log_n, const DecryptArgs &a, int form, bool nr, size_t batch, cudaStream_t s);
 cudaError_t launch_keygen(int log_n, const KeygenArgs &a, cudaStream_t s);
 cudaError_t launch_decrypt(int log_n, const DecryptArgs &a, int form, size_t batch, cudaStream_t s);
 cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s);

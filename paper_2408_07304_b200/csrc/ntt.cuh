@@ -371,4 +371,204 @@ ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad
   }
 }
 
+
+// ---------------------------------------------------------------- S-CTA cluster transforms
+// N = 2^14 and 2^15 as S = N / 2^12 CTAs of one thread-block cluster (4 or 8), each
+// holding 2^12 words (34 KiB with padding, 256 threads, one 16-word group per thread per
+// pass): small enough for three CTAs per SM, so one CTA's barriers and memory phases
+// overlap the butterflies of two others.
+//
+// Forward (decimation in time at the top).  With F_{c,t} the (N / 2^t)-point transform of
+// the subsequence x = c (mod 2^t) of the input (C-3 order, root psi^(2^t)),
+//   F_{c,t}[2k + b] = F_{c,t+1}[k] + (-1)^b W[N / 2^(t+1) + k] F_{c + 2^t, t+1}[k],
+// because the (N / 2^t)-point table is the first N / 2^t entries of W (brv_N(i) =
+// 2^t brv_{N/2^t}(i)).  CTA c (cluster rank) runs the ordinary passes on its subsequence
+// x = S i + c, then the last log2 S levels combine the S CTAs' values at one local index k
+// into the S contiguous outputs a^[S k .. S k + S) (one register-resident radix-S block per
+// k, inputs read over distributed shared memory).  CTA r finishes k in [r NL/S, (r+1) NL/S),
+// i.e. the contiguous output range [r NL, (r+1) NL).
+//
+// Inverse (decimation in frequency at the top, the mirror image).  CTA r takes input
+// positions [r NL, (r+1) NL) (bit-reversed order) and runs the GS stages LOGN-1 .. s
+// locally (their blocks never straddle a share: twiddle base tb = S + r); stages s-1 .. 0
+// pair positions j + c NL across CTAs: stage t pairs c and c + 2^(s-t-1) under
+// W^-1[2^t + (c >> (s - t))], stage 0 with N^-1 folded in.  CTA r finishes j in
+// [r NL/S, (r+1) NL/S) and stores the natural-order outputs j + c NL.
+//
+// The forward output range of CTA r is exactly the inverse input range of CTA r, so a
+// forward transform, a pointwise product and an inverse transform chain without moving
+// data between CTAs (vanilla COEFF form, decryption).
+template <int LOGN> struct SplitGeo {
+  static constexpr int LL = 12, NL = 1 << LL, S = 1 << (LOGN - LL), LOGS = LOGN - LL;
+  static constexpr int THREADS = Plan<LL>::THREADS;   // 256
+  static constexpr int KPT = NL / S / THREADS;        // exchange indices per thread (4 or 2)
+  static constexpr int STW = 1 << (Plan<LL>::KA + Plan<LL>::KB);  // smem-staged twiddles W[0, 256)
+  static_assert(KPT >= 1 && NL % (S * THREADS) == 0, "split tiling");
+};
+
+// Radix-S combine of the forward transform (register-resident, see above): v[c] = F_{c,s}[k]
+// in, v[m] = a^[S k + m] out.  Level t maps the pair (v[p], v[p + S/2]) to (v'[2p], v'[2p+1])
+// with twiddle W[N / 2^(t+1) + 2^(s-t-1) k + (p mod 2^(s-t-1))].
+template <int LOGN, bool NR>
+ZINC_DEV void split_fwd_combine(uint64_t (&v)[SplitGeo<LOGN>::S], int k, const Tw *tw, uint64_t q) {
+  using G = SplitGeo<LOGN>;
+  constexpr int S = G::S, N = 1 << LOGN;
+  const uint64_t two_q = 2 * q;
+#pragma unroll
+  for (int t = G::LOGS - 1; t >= 0; --t) {
+    const int span = 1 << (G::LOGS - t - 1);  // 2^(s-t-1)
+    uint64_t o[S];
+    Tw w[S / 2];
+#pragma unroll
+    for (int p = 0; p < S / 2; ++p) w[p] = ldtw(tw + (N >> (t + 1)) + span * k + (p & (span - 1)));
+#pragma unroll
+    for (int p = 0; p < S / 2; ++p) {
+      uint64_t X = v[p], Y = v[p + S / 2];
+      if constexpr (NR) ct_bfly_nr(X, Y, w[p].x, w[p].y, q, two_q);
+      else ct_bfly_a(X, Y, w[p].x, w[p].y, q, 2 * two_q);
+      o[2 * p] = X;
+      o[2 * p + 1] = Y;
+    }
+#pragma unroll
+    for (int p = 0; p < S; ++p) v[p] = o[p];
+  }
+}
+
+// Forward NTT of one limb by the S-CTA cluster.  `load` as ntt_forward (global coefficient
+// index x -> value; a TwoPhase load is used as such); `out(x0, v[S])` receives the S
+// contiguous outputs at global positions x0 .. x0 + S - 1 (values < 2^64 with NR, [0, 8q)
+// otherwise).  With LOAD_ALL the exchange first reads all of the CTA's inputs into
+// registers and passes a cluster barrier before any `out` call, so `out` may write this
+// CTA's shared memory (the inverse input of a following ntt_inverse_split).
+// stw: shared copy of W[0, SplitGeo::STW); after_b() runs once pass B no longer reads it.
+template <int LOGN, bool NR, bool LOAD_ALL = false, class Load, class Out, class AfterB = NoHook>
+ZINC_DEV void ntt_forward_split(uint64_t *sm, const Tw *tw, uint64_t q, Load load, Out out, const Tw *stw,
+                                AfterB after_b = AfterB()) {
+  using G = SplitGeo<LOGN>;
+  using P = Plan<G::LL>;
+  constexpr int LL = G::LL, S = G::S, THREADS = G::THREADS;
+  constexpr int SB = P::KA, SC = P::KA + P::KB;
+  auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
+  auto sld = [&](int i) { return sm[pad16(i)]; };
+  const int r = (int)cluster_rank();
+  __syncthreads();  // the previous transform may still read sm
+  if constexpr (TwoPhase<Load>::value) {
+    struct Sub {  // local index i -> coefficient S i + r
+      const Load &l;
+      int r;
+      ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
+      ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
+    };
+    ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst);
+  } else {
+    ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, [&](int i) { return load(S * i + r); }, sst);
+  }
+  __syncthreads();
+  ct_pass<LL, SB, P::KB, THREADS, false, true, NR>(stw, q, 1, sld, sst);
+  __syncthreads();
+  after_b();
+  ct_pass<LL, SC, P::KC, THREADS, true, false, NR>(tw, q, 1, sld, [&](int base, uint64_t (&v)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sm[pad16(base + j)] = v[j];
+  });
+  cluster_sync_all();  // every CTA's sub-transform complete
+  const uint64_t *peer[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) peer[c] = peer_smem(sm, (uint32_t)c);
+  const int k0 = r * (G::NL / S) + threadIdx.x;
+  if constexpr (LOAD_ALL) {
+    uint64_t v[G::KPT][S];
+#pragma unroll
+    for (int u = 0; u < G::KPT; ++u)
+#pragma unroll
+      for (int c = 0; c < S; ++c) v[u][c] = peer[c][pad16(k0 + u * THREADS)];
+    cluster_sync_all();  // every CTA has read its inputs: shared memory is free
+#pragma unroll
+    for (int u = 0; u < G::KPT; ++u) {
+      const int k = k0 + u * THREADS;
+      split_fwd_combine<LOGN, NR>(v[u], k, tw, q);
+      out(S * k, v[u]);
+    }
+  } else {
+    constexpr int U = G::KPT >= 2 ? 2 : 1;
+#pragma unroll 1
+    for (int u0 = 0; u0 < G::KPT; u0 += U) {
+      uint64_t v[U][S];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < S; ++c) v[u][c] = peer[c][pad16(k0 + (u0 + u) * THREADS)];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + (u0 + u) * THREADS;
+        split_fwd_combine<LOGN, NR>(v[u], k, tw, q);
+        out(S * k, v[u]);
+      }
+    }
+    cluster_sync_all();  // the peers finished reading this CTA's buffer
+  }
+}
+
+// Inverse NTT of one limb by the S-CTA cluster.  With GLOBAL_IN, `gload(base, v[16])`
+// supplies the 16 contiguous inputs at global position base (in [r NL, (r+1) NL)) in
+// [0, 2q); otherwise the CTA's inputs are already in its shared memory (local position
+// i = global - r NL, in [0, 4q)).  `store(x, v)` gets the natural-order output x in [0, 2q).
+// Every store happens after all S CTAs consumed their inputs.
+template <int LOGN, bool GLOBAL_IN, class GLoad, class Store>
+ZINC_DEV void ntt_inverse_split(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad gload, Store store) {
+  using G = SplitGeo<LOGN>;
+  using P = Plan<G::LL>;
+  constexpr int LL = G::LL, S = G::S, THREADS = G::THREADS, NL = G::NL;
+  constexpr int SB = P::KA, SC = P::KA + P::KB;
+  auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
+  auto sld = [&](int i) { return sm[pad16(i)]; };
+  const int r = (int)cluster_rank();
+  const int tb = S + r;
+  __syncthreads();
+  if constexpr (GLOBAL_IN) {
+    gs_pass<LL, SC, P::KC, THREADS, true>(itw, c, tb, [&](int base, uint64_t (&v)[16]) { gload(base + r * NL, v); },
+                                          sst);
+  } else {
+    gs_pass<LL, SC, P::KC, THREADS>(itw, c, tb, sld, sst);
+  }
+  __syncthreads();
+  gs_pass<LL, SB, P::KB, THREADS>(itw, c, tb, sld, sst);
+  __syncthreads();
+  gs_pass<LL, 0, P::KA, THREADS, false, false>(itw, c, tb, sld, sst);
+  cluster_sync_all();  // every share transformed, every input consumed
+  const uint64_t *peer[S];
+#pragma unroll
+  for (int cc = 0; cc < S; ++cc) peer[cc] = peer_smem(sm, (uint32_t)cc);
+  const uint64_t q = c.q, four_q = 2 * c.two_q;
+  // the S - 1 cross-share twiddles: stage t uses W^-1[2^t + beta], beta < 2^t
+  Tw w[S];
+#pragma unroll
+  for (int i = 1; i < S; ++i) w[i] = ldtw(itw + i);
+#pragma unroll 1
+  for (int j = r * (NL / S) + threadIdx.x; j < (r + 1) * (NL / S); j += THREADS) {
+    uint64_t x[S];
+#pragma unroll
+    for (int cc = 0; cc < S; ++cc) x[cc] = peer[cc][pad16(j)];
+#pragma unroll
+    for (int t = G::LOGS - 1; t >= 1; --t) {
+      const int d = 1 << (G::LOGS - t - 1);
+#pragma unroll
+      for (int cc = 0; cc < S; ++cc)
+        if ((cc & d) == 0) {
+          const Tw ww = w[(1 << t) + (cc >> (G::LOGS - t))];
+          gs_bfly(x[cc], x[cc + d], ww.x, ww.y, q, four_q);
+        }
+    }
+#pragma unroll
+    for (int cc = 0; cc < S / 2; ++cc) {  // stage 0: pairs (c, c + S/2), N^-1 folded in
+      const uint64_t X = x[cc], Y = x[cc + S / 2];
+      x[cc] = mul_shoup_lazy(X + Y, c.ninv, c.ninv_sh, q);
+      x[cc + S / 2] = mul_shoup_lazy(X - Y + four_q, c.ninv_w, c.ninv_w_sh, q);
+    }
+#pragma unroll
+    for (int cc = 0; cc < S; ++cc) store(j + cc * NL, x[cc]);
+  }
+  cluster_sync_all();  // the peers finished reading this CTA's buffer
+}
+
 }  // namespace zinc

@@ -40,6 +40,9 @@ def main():
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
     only = set(sys.argv[3].split(",")) if len(sys.argv) > 3 else None
     cfg = CONFIGS[name]
+    split = os.environ.get("ZINC_SPLIT")
+    if split is not None:
+        Z.tune(Z.TUNE_SPLIT, int(split))
     ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
     sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
     cache = Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, Z.NTT)
@@ -50,7 +53,7 @@ def main():
     peaks = {v: k11(ctx, v, sink) for v in (0, 1, 2, 3) if v != 1 or nr_ok}
     fwd = peaks[1] if nr_ok else peaks[2]      # the CKKS forward butterfly at this modulus
     half = cfg.n // 2 * cfg.log_n
-    res = {"config": name, "batch": B, "k11_Gbfly": {k: v / 1e9 for k, v in peaks.items()}}
+    res = {"config": name, "batch": B, "split": split, "k11_Gbfly": {k: v / 1e9 for k, v in peaks.items()}}
 
     def mix(n_fwd, n_inv, fwd_peak):
         return (n_fwd + n_inv) / (n_fwd / fwd_peak + n_inv / peaks[3])
