@@ -71,8 +71,9 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
   extern __shared__ __align__(16) uint64_t sm[];
   Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
   int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
-  __shared__ __align__(8) uint64_t tw_mbar;
+  __shared__ __align__(8) uint64_t tw_mbar, cl_mbar[2];
   TwStager tws{&tw_mbar, 0};
+  ClusterBar cb{cl_mbar, 0};
   const size_t b = blockIdx.x / S;
   const int r = (int)cluster_rank();
   const uint64_t msg = a.msg_base + b;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
   tws.init();
-  __syncthreads();
+  cb.init<S>();
   tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
   sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ZINC_E2);
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
     for (int t = 0; t < 2; ++t) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
-      ntt_forward_split<LOGN, NR>(sm, tw, q, ZincTLoad<INTS, G::LOGS>{m, t ? se2 : se1, c, t},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoad<INTS, G::LOGS>{m, t ? se2 : se1, c, t},
           [&](int x0, uint64_t (&v)[S]) {
 #pragma unroll
             for (int u = 0; u < S; u += 2) {
@@ -143,8 +144,9 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
   Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
   int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
   uint8_t *su = reinterpret_cast<uint8_t *>(se2 + NL);
-  __shared__ __align__(8) uint64_t tw_mbar;
+  __shared__ __align__(8) uint64_t tw_mbar, cl_mbar[2];
   TwStager tws{&tw_mbar, 0};
+  ClusterBar cb{cl_mbar, 0};
   const size_t b = blockIdx.x / S;
   const int r = (int)cluster_rank();
   const uint64_t msg = a.msg_base + b;
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
   tws.init();
-  __syncthreads();
+  cb.init<S>();
   tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
   sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
     tws.wait();
 #pragma unroll 1
     for (int t = 0; t < 3; ++t) {
-      ntt_forward_split<LOGN, NR>(sm, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t},
           [&](int x0, uint64_t (&v)[S]) {
             if (t < 2) {
               uint64_t *dst = (t ? ct1 : ct0) + x0;
@@ -212,8 +214,9 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
   Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
   int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
   uint8_t *su = reinterpret_cast<uint8_t *>(se2 + NL);
-  __shared__ __align__(8) uint64_t tw_mbar;
+  __shared__ __align__(8) uint64_t tw_mbar, cl_mbar[2];
   TwStager tws{&tw_mbar, 0};
+  ClusterBar cb{cl_mbar, 0};
   const size_t b = blockIdx.x / S;
   const int r = (int)cluster_rank();
   const uint64_t msg = a.msg_base + b;
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
   tws.init();
-  __syncthreads();
+  cb.init<S>();
   tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
   sample_cbd_inv<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
     uint64_t *ct1 = ct0 + (size_t)L * N;
     auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
     tws.wait();
-    ntt_forward_split<LOGN, NR, true>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> G::LOGS), q); },
+    ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> G::LOGS), q); },
         [&](int x0, uint64_t (&v)[S]) {
 #pragma unroll
           for (int u = 0; u < S; u += 2) {
@@ -253,12 +256,12 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
         stw, [&]() {
           if (i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
         });
-    ntt_inverse_split<LOGN, false>(sm, itw, c, [](int, uint64_t (&)[16]) {},
+    ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {},
         [&](int x, uint64_t v) {
           const uint64_t e = pt_plus_e<INTS>(m ? __ldg(m + x) : 0, se1[inv_sample_idx<LOGN>(x, r)], c);
           __stcs(ct0 + x, add_mod(csub(v, q), e, q));
         });
-    ntt_inverse_split<LOGN, true>(sm, itw, c,
+    ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
           for (int u = 0; u < 16; u += 2) ld2(ct1 + base + u, v[u], v[u + 1]);
@@ -282,6 +285,9 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL;
   extern __shared__ __align__(16) uint64_t sm[];
   __shared__ int bad_flag;
+  __shared__ __align__(8) uint64_t cl_mbar[2];
+  ClusterBar cb{cl_mbar, 0};
+  cb.init<S>();
   const size_t b = blockIdx.x / S;
   const int r = (int)cluster_rank();
   const int L = a.L;
@@ -328,7 +334,7 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
       if (c.scheme == SCHEME_BGV && i == L - 1) x0[x] = (int64_t)mod_t(x0[x], c.t, c.t_mu);
     };
     if (FORM == 0) {
-      ntt_inverse_split<LOGN, true>(sm, itw, c,
+      ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int u = 0; u < 16; ++u)
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
     } else {
       const Tw *tw = a.tw + (size_t)i * N;
       // the forward split reads its early-pass twiddles from global memory here (stw = tw)
-      ntt_forward_split<LOGN, NR, true>(sm, tw, q, [&](int x) { return __ldg(c2 + x); },
+      ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return __ldg(c2 + x); },
           [&](int x0g, uint64_t (&v)[S]) {
 #pragma unroll
             for (int u = 0; u < S; ++u) {
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
             }
           },
           tw);
-      ntt_inverse_split<LOGN, false>(sm, itw, c, [](int, uint64_t (&)[16]) {}, epilogue);
+      ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {}, epilogue);
     }
   }
   bad = __syncthreads_or(bad);

@@ -398,6 +398,57 @@ ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad
 // The forward output range of CTA r is exactly the inverse input range of CTA r, so a
 // forward transform, a pointwise product and an inverse transform chain without moving
 // data between CTAs (vanilla COEFF form, decryption).
+// Cluster-wide rendezvous of the S CTAs on mbarriers (two, alternating; each expects S
+// arrivals per phase).  arrive(): a CTA barrier (which drains this CTA's shared-memory
+// stores), then one remote arrive on every CTA's barrier; wait(): this CTA's barrier.
+// Unlike barrier.cluster (release/acquire at cluster scope: MEMBAR.GPU + ERRBAR on arrive,
+// CCTL.IVALL on wait, flushing L1 and draining every outstanding global store), the
+// CTA-scope arrive / wait compile to bare SYNCS operations.  The exchanges only pass
+// shared-memory data (DSMEM reads of a peer's buffer after its rendezvous), so that is all
+// the ordering they need.  Two alternating barriers make a fast CTA's next arrivals land in
+// the other barrier, never in a phase a slow CTA has not completed.
+struct ClusterBar {
+  uint64_t *mbar;  // [2], this CTA's shared memory
+  uint32_t k;
+  template <int S>
+  ZINC_DEV void init() {
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(mbar + j)),
+                     "r"(S));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    k = 0;
+    // every CTA's barriers are initialised before anyone arrives remotely (once per kernel)
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  template <int S>
+  ZINC_DEV void arrive() {
+    __syncthreads();
+    if (threadIdx.x < S) {
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                   : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(mbar + (k & 1))), "r"((uint32_t)threadIdx.x));
+      asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+    }
+  }
+  ZINC_DEV void wait() {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar + (k & 1)), par = (k >> 1) & 1u;
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(a), "r"(par) : "memory");
+    }
+    ++k;
+  }
+  template <int S>
+  ZINC_DEV void sync() {
+    arrive<S>();
+    wait();
+  }
+};
+
 template <int LOGN> struct SplitGeo {
   static constexpr int LL = 12, NL = 1 << LL, S = 1 << (LOGN - LL), LOGS = LOGN - LL;
   static constexpr int THREADS = Plan<LL>::THREADS;   // 256
@@ -442,8 +493,8 @@ ZINC_DEV void split_fwd_combine(uint64_t (&v)[SplitGeo<LOGN>::S], int k, const T
 // CTA's shared memory (the inverse input of a following ntt_inverse_split).
 // stw: shared copy of W[0, SplitGeo::STW); after_b() runs once pass B no longer reads it.
 template <int LOGN, bool NR, bool LOAD_ALL = false, class Load, class Out, class AfterB = NoHook>
-ZINC_DEV void ntt_forward_split(uint64_t *sm, const Tw *tw, uint64_t q, Load load, Out out, const Tw *stw,
-                                AfterB after_b = AfterB()) {
+ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint64_t q, Load load, Out out,
+                                const Tw *stw, AfterB after_b = AfterB()) {
   using G = SplitGeo<LOGN>;
   using P = Plan<G::LL>;
   constexpr int LL = G::LL, S = G::S, THREADS = G::THREADS;
@@ -471,7 +522,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, const Tw *tw, uint64_t q, Load loa
 #pragma unroll
     for (int j = 0; j < 16; ++j) sm[pad16(base + j)] = v[j];
   });
-  cluster_sync_all();  // every CTA's sub-transform complete
+  cb.sync<S>();  // every CTA's sub-transform complete
   const uint64_t *peer[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) peer[c] = peer_smem(sm, (uint32_t)c);
@@ -482,7 +533,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, const Tw *tw, uint64_t q, Load loa
     for (int u = 0; u < G::KPT; ++u)
 #pragma unroll
       for (int c = 0; c < S; ++c) v[u][c] = peer[c][pad16(k0 + u * THREADS)];
-    cluster_sync_all();  // every CTA has read its inputs: shared memory is free
+    cb.sync<S>();  // every CTA has read its inputs: shared memory is free
 #pragma unroll
     for (int u = 0; u < G::KPT; ++u) {
       const int k = k0 + u * THREADS;
@@ -505,7 +556,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, const Tw *tw, uint64_t q, Load loa
         out(S * k, v[u]);
       }
     }
-    cluster_sync_all();  // the peers finished reading this CTA's buffer
+    cb.sync<S>();  // the peers finished reading this CTA's buffer
   }
 }
 
@@ -515,7 +566,8 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, const Tw *tw, uint64_t q, Load loa
 // i = global - r NL, in [0, 4q)).  `store(x, v)` gets the natural-order output x in [0, 2q).
 // Every store happens after all S CTAs consumed their inputs.
 template <int LOGN, bool GLOBAL_IN, class GLoad, class Store>
-ZINC_DEV void ntt_inverse_split(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad gload, Store store) {
+ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, const LimbConst &c, GLoad gload,
+                                Store store) {
   using G = SplitGeo<LOGN>;
   using P = Plan<G::LL>;
   constexpr int LL = G::LL, S = G::S, THREADS = G::THREADS, NL = G::NL;
@@ -535,7 +587,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, const Tw *itw, const LimbConst &c,
   gs_pass<LL, SB, P::KB, THREADS>(itw, c, tb, sld, sst);
   __syncthreads();
   gs_pass<LL, 0, P::KA, THREADS, false, false>(itw, c, tb, sld, sst);
-  cluster_sync_all();  // every share transformed, every input consumed
+  cb.sync<S>();  // every share transformed, every input consumed
   const uint64_t *peer[S];
 #pragma unroll
   for (int cc = 0; cc < S; ++cc) peer[cc] = peer_smem(sm, (uint32_t)cc);
@@ -568,7 +620,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, const Tw *itw, const LimbConst &c,
 #pragma unroll
     for (int cc = 0; cc < S; ++cc) store(j + cc * NL, x[cc]);
   }
-  cluster_sync_all();  // the peers finished reading this CTA's buffer
+  cb.sync<S>();  // the peers finished reading this CTA's buffer
 }
 
 }  // namespace zinc
