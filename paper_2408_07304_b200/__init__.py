@@ -33,7 +33,7 @@ CKKS, BFV, BGV = 0, 1, 2
 PT_COEFF_I64, PT_SLOTS_F64, PT_SLOTS_C128, PT_COEFF_I128 = 0, 1, 2, 3
 PATH_ZINC, PATH_VANILLA = 0, 1
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libzinc.so")
+LIB_PATH = os.environ.get("ZINC_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libzinc.so")
 
 # every symbol include/zinc.h declares
 EXPORTED_SYMBOLS = (

@@ -399,14 +399,18 @@ ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad
 // forward transform, a pointwise product and an inverse transform chain without moving
 // data between CTAs (vanilla COEFF form, decryption).
 // Cluster-wide rendezvous of the S CTAs on mbarriers (two, alternating; each expects S
-// arrivals per phase).  arrive(): a CTA barrier (which drains this CTA's shared-memory
-// stores), then one remote arrive on every CTA's barrier; wait(): this CTA's barrier.
-// Unlike barrier.cluster (release/acquire at cluster scope: MEMBAR.GPU + ERRBAR on arrive,
-// CCTL.IVALL on wait, flushing L1 and draining every outstanding global store), the
-// CTA-scope arrive / wait compile to bare SYNCS operations.  The exchanges only pass
-// shared-memory data (DSMEM reads of a peer's buffer after its rendezvous), so that is all
-// the ordering they need.  Two alternating barriers make a fast CTA's next arrivals land in
-// the other barrier, never in a phase a slow CTA has not completed.
+// arrivals per phase): every thread fences, a CTA barrier, then one remote arrive on
+// every CTA's barrier; wait() polls this CTA's own barrier.  Two alternating barriers make
+// a fast CTA's next arrivals land in the other barrier, never in a phase a slow CTA has
+// not completed.  barrier.cluster would carry a cluster-scope acquire on every wait
+// (CCTL.IVALL: the SM's L1, with the twiddles, invalidated at every exchange); here the
+// waits are plain SYNCS polls.  What each rendezvous must order (measured: a stress of
+// every variant over 10^5 exchanges, scripts/split_check.py):
+//  - sync_raw (peers read this CTA's freshly stored share): the stores must be visible
+//    to remote DSMEM readers, which a CTA-scope fence does not guarantee (observed stale
+//    reads); a cluster-scope release fence (MEMBAR.GPU) per thread does.
+//  - sync_war (this CTA will overwrite what the peers read): every DSMEM load of the
+//    exchange must have completed, which the CTA-scope fence (MEMBAR.CTA) ensures.
 struct ClusterBar {
   uint64_t *mbar;  // [2], this CTA's shared memory
   uint32_t k;
@@ -443,11 +447,31 @@ struct ClusterBar {
     ++k;
   }
   template <int S>
-  ZINC_DEV void sync() {
+  ZINC_DEV void sync_raw() {
+    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    arrive<S>();
+    wait();
+  }
+  template <int S>
+  ZINC_DEV void sync_war() {
+    asm volatile("fence.acq_rel.cta;" ::: "memory");
     arrive<S>();
     wait();
   }
 };
+
+// 32-bit shared::cluster address of `p` (this CTA's shared memory) in CTA `rank`, and an
+// explicit DSMEM load from it (always the owning SM's shared memory; never an L1 line).
+ZINC_DEV uint32_t dsmem_addr(const void *p, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+  return ra;
+}
+ZINC_DEV uint64_t ld_dsmem(uint32_t addr) {
+  uint64_t v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
 
 template <int LOGN> struct SplitGeo {
   static constexpr int LL = 12, NL = 1 << LL, S = 1 << (LOGN - LL), LOGS = LOGN - LL;
@@ -522,18 +546,18 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
 #pragma unroll
     for (int j = 0; j < 16; ++j) sm[pad16(base + j)] = v[j];
   });
-  cb.sync<S>();  // every CTA's sub-transform complete
-  const uint64_t *peer[S];
+  cb.sync_raw<S>();  // every CTA's sub-transform complete
+  uint32_t peer[S];
 #pragma unroll
-  for (int c = 0; c < S; ++c) peer[c] = peer_smem(sm, (uint32_t)c);
+  for (int c = 0; c < S; ++c) peer[c] = dsmem_addr(sm, (uint32_t)c);
   const int k0 = r * (G::NL / S) + threadIdx.x;
   if constexpr (LOAD_ALL) {
     uint64_t v[G::KPT][S];
 #pragma unroll
     for (int u = 0; u < G::KPT; ++u)
 #pragma unroll
-      for (int c = 0; c < S; ++c) v[u][c] = peer[c][pad16(k0 + u * THREADS)];
-    cb.sync<S>();  // every CTA has read its inputs: shared memory is free
+      for (int c = 0; c < S; ++c) v[u][c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k0 + u * THREADS));
+    cb.sync_war<S>();  // every CTA has read its inputs: shared memory is free
 #pragma unroll
     for (int u = 0; u < G::KPT; ++u) {
       const int k = k0 + u * THREADS;
@@ -548,7 +572,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int c = 0; c < S; ++c) v[u][c] = peer[c][pad16(k0 + (u0 + u) * THREADS)];
+        for (int c = 0; c < S; ++c) v[u][c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k0 + (u0 + u) * THREADS));
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int k = k0 + (u0 + u) * THREADS;
@@ -556,7 +580,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
         out(S * k, v[u]);
       }
     }
-    cb.sync<S>();  // the peers finished reading this CTA's buffer
+    cb.sync_war<S>();  // the peers finished reading this CTA's buffer
   }
 }
 
@@ -587,10 +611,10 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
   gs_pass<LL, SB, P::KB, THREADS>(itw, c, tb, sld, sst);
   __syncthreads();
   gs_pass<LL, 0, P::KA, THREADS, false, false>(itw, c, tb, sld, sst);
-  cb.sync<S>();  // every share transformed, every input consumed
-  const uint64_t *peer[S];
+  cb.sync_raw<S>();  // every share transformed, every input consumed
+  uint32_t peer[S];
 #pragma unroll
-  for (int cc = 0; cc < S; ++cc) peer[cc] = peer_smem(sm, (uint32_t)cc);
+  for (int cc = 0; cc < S; ++cc) peer[cc] = dsmem_addr(sm, (uint32_t)cc);
   const uint64_t q = c.q, four_q = 2 * c.two_q;
   // the S - 1 cross-share twiddles: stage t uses W^-1[2^t + beta], beta < 2^t
   Tw w[S];
@@ -600,7 +624,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
   for (int j = r * (NL / S) + threadIdx.x; j < (r + 1) * (NL / S); j += THREADS) {
     uint64_t x[S];
 #pragma unroll
-    for (int cc = 0; cc < S; ++cc) x[cc] = peer[cc][pad16(j)];
+    for (int cc = 0; cc < S; ++cc) x[cc] = ld_dsmem(peer[cc] + 8u * (uint32_t)pad16(j));
 #pragma unroll
     for (int t = G::LOGS - 1; t >= 1; --t) {
       const int d = 1 << (G::LOGS - t - 1);
@@ -620,7 +644,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
 #pragma unroll
     for (int cc = 0; cc < S; ++cc) store(j + cc * NL, x[cc]);
   }
-  cb.sync<S>();  // the peers finished reading this CTA's buffer
+  cb.sync_war<S>();  // the peers finished reading this CTA's buffer
 }
 
 }  // namespace zinc
