@@ -241,7 +241,8 @@ enum {
   ZINC_K_CT_SUM = 12,    /* aggregation of a batch */
   ZINC_K_LIFT = 13,      /* 128-bit plaintexts -> RNS residues */
   ZINC_K_PT_ADD = 14,    /* c1 += plaintext residues */
-  ZINC_K_COUNT = 15
+  ZINC_K_SHOUP_PREP = 15, /* Shoup companions of pk / sk for the pointwise key products */
+  ZINC_K_COUNT = 16
 };
 /* on != 0: clear the trace and bracket every following kernel launch with CUDA
  * events recorded on the launch's own stream; on == 0: stop recording. */

@@ -46,7 +46,8 @@ EXPORTED_SYMBOLS = (
 )
 KERNEL_NAMES = ("zinc_coeff_kernel", "zinc_ntt_kernel", "vanilla_kernel", "keygen_kernel", "encode_kernel",
                 "decrypt_kernel", "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
-                "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel", "lift_kernel", "pt_add_kernel")
+                "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel", "lift_kernel", "pt_add_kernel",
+                "shoup_prep_kernel")
 # zinc_int_peak butterfly variants (include/zinc.h)
 BFLY_CT, BFLY_CT_NR, BFLY_CT_A, BFLY_GS = 0, 1, 2, 3
 

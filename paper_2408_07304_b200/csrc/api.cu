@@ -54,7 +54,7 @@ static const char *kKernelNames[ZINC_K_COUNT] = {"zinc_coeff_kernel", "zinc_ntt_
                                                  "keygen_kernel", "encode_kernel", "decrypt_kernel",
                                                  "decode_kernel", "ntt_kernel", "sample_kernel", "int_peak_kernel",
                                                  "bfv_scale_kernel", "ct_add_kernel", "ct_sum_kernel",
-                                                 "lift_kernel", "pt_add_kernel"};
+                                                 "lift_kernel", "pt_add_kernel", "shoup_prep_kernel"};
 static cudaEvent_t pool_event() {
   cudaEvent_t e = nullptr;
   if (!g_event_pool.empty()) {
@@ -350,6 +350,23 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     lc.ninv_w = mulm(lc.ninv, itw[(size_t)i * n + 1].x, q);
     lc.ninv_w_sh = shoup(lc.ninv_w, q);
     lc.r64 = (uint64_t)(((u128)1 << 64) % q);
+    // reduce_fold: q = 2^b - c; one fold maps x < 2^64 below 2^b + (2^(64-b) - 1) c + (2^b - 1)
+    {
+      const uint64_t fc = (1ull << lc.b) - q;
+      lc.fold_mask = (lc.b >= 64) ? ~0ull : (1ull << lc.b) - 1;
+      lc.fold_c = (uint32_t)fc;
+      lc.fold_n = 0;
+      if (lc.b >= 33 && lc.b <= 63 && fc < (1ull << 32)) {
+        const u128 two_q = (u128)2 * q;
+        const u128 b1 = (u128)lc.fold_mask + (u128)(~0ull >> lc.b) * fc;  // bound after one fold
+        const u128 b2 = (u128)lc.fold_mask + (u128)(b1 >> lc.b) * fc;    // after two
+        if (b1 < two_q) lc.fold_n = 1;
+        else if ((b1 >> lc.b) < (1ull << 32) && b2 < two_q) lc.fold_n = 2;
+      }
+      const u128 qinv = ~(u128)0 / q;  // floor((2^128 - 1) / q) = floor(2^128 / q) for q not a power of 2
+      lc.qinv_hi = (uint64_t)(qinv >> 64);
+      lc.qinv_lo = (uint64_t)qinv;
+    }
     // scheme constants (section 4.2)
     lc.scheme = (uint32_t)scheme;
     if (c->t) {
@@ -581,11 +598,17 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
       LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, kernel_mode(c), batch, groups, s));
     return ZINC_OK;
   }
+  // Shoup companions of pk: the pointwise products pk u^ become Shoup products
+  ScratchBuf pk_sh(s);
+  const size_t key_words = (size_t)2 * c->L * c->n;
+  CUDA_TRY(pk_sh.alloc(key_words * 8));
+  LAUNCH(ZINC_K_SHOUP_PREP, s, launch_shoup_prep(c->d_limbs, key, pk_sh.as<uint64_t>(), key_words, c->log_n, c->L, s));
   VanillaArgs a{};
   a.limbs = c->d_limbs;
   a.tw = c->d_tw;
   a.itw = c->d_itw;
   a.pk = key;
+  a.pk_sh = pk_sh.as<uint64_t>();
   a.m = m;
   a.ct = ct;
   a.seed = seed;
@@ -809,7 +832,9 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
   if (c->scheme != ZINC_SCHEME_CKKS && slots_out)
     return fail(ZINC_EINVAL, "BFV / BGV decryption has no slot decoding (slots_out must be NULL)");
   CUDA_TRY(cudaSetDevice(c->device));
-  ScratchBuf xb(s), xwb(s), xlb(s);
+  ScratchBuf xb(s), xwb(s), xlb(s), skb(s);
+  CUDA_TRY(skb.alloc((size_t)c->L * c->n * 8));
+  LAUNCH(ZINC_K_SHOUP_PREP, s, launch_shoup_prep(c->d_limbs, sk_ntt, skb.as<uint64_t>(), (size_t)c->L * c->n, c->log_n, c->L, s));
   if (!coeff_out) CUDA_TRY(xb.alloc(batch * (size_t)c->n * 8));
   if (wide && !coeff128_out) CUDA_TRY(xwb.alloc(batch * (size_t)c->n * 16));
   int64_t *x = coeff_out ? coeff_out : xb.as<int64_t>();
@@ -819,6 +844,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
   a.tw = c->d_tw;
   a.itw = c->d_itw;
   a.sk_ntt = sk_ntt;
+  a.sk_sh = skb.as<uint64_t>();
   a.ct = ct;
   a.coeff_out = x;
   a.status_out = status_out;

@@ -35,6 +35,11 @@ struct LimbConst {
   uint64_t dec_i;    // BFV decrypt: floor(t Q~_i / q_i) mod t, Q~_i = (Q/q_i)^-1 mod q_i
   uint64_t dec_f;    // BFV decrypt: round(frac(t Q~_i / q_i) 2^64)
   uint64_t r64;      // 2^64 mod q (128-bit plaintext residues)
+  // q = 2^b - fold_c with fold_c < 2^32 (the C-1 primes sit just below 2^b): reduce_fold
+  uint64_t fold_mask;  // 2^b - 1
+  uint32_t fold_c;
+  uint32_t fold_n;     // folds that bring any 64-bit value below 2q (1 or 2); 0: use reduce64
+  uint64_t qinv_hi, qinv_lo;  // floor(2^128 / q): Shoup companions on the device (shoup_prep_kernel)
 };
 enum : uint32_t { SCHEME_CKKS = 0, SCHEME_BFV = 1, SCHEME_BGV = 2 };
 
@@ -60,6 +65,11 @@ ZINC_DEV uint64_t mul_mod(uint64_t a, uint64_t b, const LimbConst &c) {
   uint64_t r = lo - q3 * c.q;
   r = csub(r, c.q);
   return csub(r, c.q);
+}
+// [a + w y]_q for canonical a, a key word w < q with Shoup companion wp, and any y < 2^64
+// (the lazy output of a transform): the Shoup product is in [0, 2q), the sum below 3q.
+ZINC_DEV uint64_t add_shoup(uint64_t a, uint64_t y, uint64_t w, uint64_t wp, uint64_t q) {
+  return csub(csub(a + mul_shoup_lazy(y, w, wp, q), 2 * q), q);
 }
 // Canonical residue of a signed 64-bit integer (reading A15); mu = floor(2^64/q).
 ZINC_DEV uint64_t reduce_i64q(int64_t v, uint64_t q, uint64_t mu) {
@@ -217,6 +227,16 @@ ZINC_DEV void ct_bfly_nr(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint
 }
 // Any 64-bit value -> [0, q) (mu = floor(2^64 / q)): the end of a lazy-free transform.
 ZINC_DEV uint64_t reduce64(uint64_t x, uint64_t q, uint64_t mu) { return csub(x - __umul64hi(x, mu) * q, q); }
+// Any 64-bit value -> [0, q) for q = 2^b - c: 2^b = c (mod q), so x = xh 2^b + xl = xh c + xl.
+// One fold is one IMAD.WIDE.U32 (xh c with the masked x as its addend) plus a shift and a
+// mask; fold_n folds leave a value below 2q (checked on the host), one csub finishes.
+// About half the instructions of reduce64's 64 x 64 high product, mostly off the fma pipe.
+ZINC_DEV uint64_t reduce_fold(uint64_t x, const LimbConst &c) {
+  if (c.fold_n == 0) return reduce64(x, c.q, c.mu64);
+  x = (x & c.fold_mask) + (uint64_t)(uint32_t)(x >> c.b) * c.fold_c;
+  if (c.fold_n == 2) x = (x & c.fold_mask) + (uint64_t)(uint32_t)(x >> c.b) * c.fold_c;
+  return csub(x, c.q);
+}
 
 // ------------------------------------------------------------------ Philox4x32-10
 // Salmon et al., SC'11.  Counter (block, msg_lo, msg_hi, tag<<16|limb),

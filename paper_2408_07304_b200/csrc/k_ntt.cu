@@ -55,12 +55,12 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N;
     const uint64_t *z1 = a.cache + (size_t)i * N, *z2 = a.cache + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    // the lazy transform output plus the canonical cache word stays below 2^64
     tws.wait();
     if constexpr (G::DIT) {
       // both transforms through one copy of the transform code (the kernel is instruction-
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
         ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, ZincTLoad<INTS>{m, t ? se2 : se1, c, t},
             [&](int x, uint64_t v0, uint64_t v1) {
               const ulonglong2 zz = ld2_nc(z + x);
-              st2_cs(ctt + x, add_mod(zz.x, canon(v0), q), add_mod(zz.y, canon(v1), q));
+              st2_cs(ctt + x, reduce_fold(zz.x + v0, c), reduce_fold(zz.y + v1, c));
             },
             stw, [&]() {
               if (t == 1 && i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
         uint64_t *ctt = t ? ct1 : ct0;
         auto out = [&](int x, uint64_t v0, uint64_t v1) {
           const ulonglong2 zz = ld2_nc(z + x);
-          st2_cs(ctt + x, add_mod(zz.x, canon(v0), q), add_mod(zz.y, canon(v1), q));
+          st2_cs(ctt + x, reduce_fold(zz.x + v0, c), reduce_fold(zz.y + v1, c));
         };
         if constexpr (ONE) {
           ntt_forward<LOGN, true, NR>(sm, tw, q, ZincTLoad<INTS, 0>{m, t ? se2 : se1, c, t}, to_smem<LOGN>(sm), stw);
@@ -168,10 +168,10 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) d
   const uint64_t q0 = a.limbs[0].q;
   for (int i = 0; i < L; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const uint64_t *c1 = a.ct + b * 2 * L * N + (size_t)i * N;
     const uint64_t *c2 = c1 + (size_t)L * N;
-    const uint64_t *s = a.sk_ntt + (size_t)i * N;
+    const uint64_t *s = a.sk_ntt + (size_t)i * N, *ssh = a.sk_sh + (size_t)i * N;
     const Tw *itw = a.itw + (size_t)i * N;
     auto epilogue = [&](int x, uint64_t v) {
       uint64_t xi = csub(v, q);
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) d
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int r = 0; r < 16; ++r)
-              v[r] = add_mod(__ldg(c1 + base + r), mul_mod(__ldg(c2 + base + r), __ldg(s + base + r), c), q);
+              v[r] = __ldg(c1 + base + r) + mul_shoup_lazy(__ldg(c2 + base + r), __ldg(s + base + r), __ldg(ssh + base + r), q);
           },
           epilogue);
     } else {
@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(Geo<LOGN, 13>::THREADS, Geo<LOGN, 13>::MINB) d
       ntt_forward<LOGN, false, false, 13>(sm, tw, q, [&](int x) { return __ldg(c2 + x); },
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-            for (int r = 0; r < 16; ++r) sm[pad16(base - loff + r)] = mul_mod(canon8(v[r], q, two_q), __ldg(s + base + r), c);
+            for (int r = 0; r < 16; ++r)
+              sm[pad16(base - loff + r)] = mul_shoup_lazy(v[r], __ldg(s + base + r), __ldg(ssh + base + r), q);
           });
       ntt_inverse<LOGN, false, 13>(sm, itw, c,
           [&](int base, uint64_t (&v)[16]) {

@@ -91,10 +91,9 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
     tws.wait();
 #pragma unroll 1
     for (int t = 0; t < 2; ++t) {
@@ -104,8 +103,8 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
           [&](int x0, uint64_t (&v)[S]) {
 #pragma unroll
             for (int u = 0; u < S; u += 2) {
-              const ulonglong2 zz = ld2_nc(z + x0 + u);
-              st2_cs(ctt + x0 + u, add_mod(zz.x, canon(v[u]), q), add_mod(zz.y, canon(v[u + 1]), q));
+              const ulonglong2 zz = ld2_nc(z + x0 + u);  // lazy output + canonical cache word < 2^64
+              st2_cs(ctt + x0 + u, reduce_fold(zz.x + v[u], c), reduce_fold(zz.y + v[u + 1], c));
             }
           },
           stw, [&]() {
@@ -165,12 +164,13 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N;
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    const uint64_t *pk1s = a.pk_sh + (size_t)i * N, *pk2s = a.pk_sh + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     tws.wait();
 #pragma unroll 1
     for (int t = 0; t < 3; ++t) {
@@ -183,13 +183,13 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
             } else {
 #pragma unroll
               for (int u = 0; u < S; u += 2) {
-                const uint64_t u0 = canon(v[u]), u1 = canon(v[u + 1]);
                 const ulonglong2 p1 = ld2_nc(pk1 + x0 + u), p2 = ld2_nc(pk2 + x0 + u);
+                const ulonglong2 s1 = ld2_nc(pk1s + x0 + u), s2 = ld2_nc(pk2s + x0 + u);
                 uint64_t a0, a1, b0, b1;
                 ld2(ct0 + x0 + u, a0, a1);
                 ld2(ct1 + x0 + u, b0, b1);
-                st2_cs(ct0 + x0 + u, add_mod(a0, mul_mod(p1.x, u0, c), q), add_mod(a1, mul_mod(p1.y, u1, c), q));
-                st2_cs(ct1 + x0 + u, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
+                st2_cs(ct0 + x0 + u, add_shoup(a0, v[u], p1.x, s1.x, q), add_shoup(a1, v[u + 1], p1.y, s1.y, q));
+                st2_cs(ct1 + x0 + u, add_shoup(b0, v[u], p2.x, s2.x, q), add_shoup(b1, v[u + 1], p2.y, s2.y, q));
               }
             }
           },
@@ -235,22 +235,24 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N, *itw = a.itw + (size_t)i * N;
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    const uint64_t *pk1s = a.pk_sh + (size_t)i * N, *pk2s = a.pk_sh + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     tws.wait();
     ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> G::LOGS), q); },
         [&](int x0, uint64_t (&v)[S]) {
 #pragma unroll
           for (int u = 0; u < S; u += 2) {
-            const uint64_t u0 = canon(v[u]), u1 = canon(v[u + 1]);
             const ulonglong2 p1 = ld2_nc(pk1 + x0 + u), p2 = ld2_nc(pk2 + x0 + u);
-            st2(ct1 + x0 + u, mul_mod(p2.x, u0, c), mul_mod(p2.y, u1, c));  // temporary: pk2 u^
-            sm[pad16(x0 + u - r * NL)] = mul_mod(p1.x, u0, c);             // this CTA's inverse input
-            sm[pad16(x0 + u + 1 - r * NL)] = mul_mod(p1.y, u1, c);
+            const ulonglong2 s1 = ld2_nc(pk1s + x0 + u), s2 = ld2_nc(pk2s + x0 + u);
+            // [0, 2q): the inverse transforms take inputs below 4q
+            st2(ct1 + x0 + u, mul_shoup_lazy(v[u], p2.x, s2.x, q), mul_shoup_lazy(v[u + 1], p2.y, s2.y, q));  // temporary
+            sm[pad16(x0 + u - r * NL)] = mul_shoup_lazy(v[u], p1.x, s1.x, q);  // this CTA's inverse input
+            sm[pad16(x0 + u + 1 - r * NL)] = mul_shoup_lazy(v[u + 1], p1.y, s1.y, q);
           }
         },
         stw, [&]() {
@@ -296,10 +298,10 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
   const uint64_t q0 = a.limbs[0].q;
   for (int i = 0; i < L; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const uint64_t *c1 = a.ct + b * 2 * L * N + (size_t)i * N;
     const uint64_t *c2 = c1 + (size_t)L * N;
-    const uint64_t *s = a.sk_ntt + (size_t)i * N;
+    const uint64_t *s = a.sk_ntt + (size_t)i * N, *ssh = a.sk_sh + (size_t)i * N;
     const Tw *itw = a.itw + (size_t)i * N;
     auto epilogue = [&](int x, uint64_t v) {
       uint64_t xi = csub(v, q);
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
             for (int u = 0; u < 16; ++u)
-              v[u] = add_mod(__ldg(c1 + base + u), mul_mod(__ldg(c2 + base + u), __ldg(s + base + u), c), q);
+              v[u] = __ldg(c1 + base + u) + mul_shoup_lazy(__ldg(c2 + base + u), __ldg(s + base + u), __ldg(ssh + base + u), q);
           },
           epilogue);
     } else {
@@ -347,10 +349,8 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
       ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return __ldg(c2 + x); },
           [&](int x0g, uint64_t (&v)[S]) {
 #pragma unroll
-            for (int u = 0; u < S; ++u) {
-              const uint64_t w = NR ? reduce64(v[u], q, c.mu64) : canon8(v[u], q, two_q);
-              sm[pad16(x0g + u - r * NL)] = mul_mod(w, __ldg(s + x0g + u), c);
-            }
+            for (int u = 0; u < S; ++u)
+              sm[pad16(x0g + u - r * NL)] = mul_shoup_lazy(v[u], __ldg(s + x0g + u), __ldg(ssh + x0g + u), q);
           },
           tw);
       ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {}, epilogue);

@@ -102,6 +102,33 @@ cudaError_t launch_pt_add(const PtAddArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ============================================================ Shoup companions of a key
+// w' = floor(w 2^64 / q) for canonical words w of a key [rows][L][N] (limb (idx >> log N) mod L),
+// so the per-message pointwise products pk u^ (vanilla) and c2 s (decryption) are Shoup
+// products (mul_shoup_lazy) instead of Barrett products of two variables.  The estimate
+// x floor(2^128 / q) / 2^64 is at most 2 short; the remainder x 2^64 - w' q (< 3q, exact in
+// 64 bits) corrects it.
+__global__ void __launch_bounds__(256) shoup_prep_kernel(const LimbConst *limbs, const uint64_t *w, uint64_t *wp,
+                                                          size_t words, int log_n, int L) {
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < words; idx += (size_t)gridDim.x * blockDim.x) {
+    const LimbConst &c = limbs[(idx >> log_n) % L];
+    const uint64_t x = w[idx];
+    uint64_t est = x * c.qinv_hi + __umul64hi(x, c.qinv_lo);
+    uint64_t r = (uint64_t)0 - est * c.q;
+    while (r >= c.q) {
+      r -= c.q;
+      ++est;
+    }
+    wp[idx] = est;
+  }
+}
+cudaError_t launch_shoup_prep(const LimbConst *limbs, const uint64_t *w, uint64_t *wp, size_t words, int log_n, int L,
+                              cudaStream_t s) {
+  const unsigned blocks = (unsigned)std::min<size_t>((words + 255) / 256, 148 * 8);
+  shoup_prep_kernel<<<blocks, 256, 0, s>>>(limbs, w, wp, words, log_n, L);
+  return cudaGetLastError();
+}
+
 // ============================================================ samplers (debug)
 __global__ void sample_kernel(SampleArgs a) {
   size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x;

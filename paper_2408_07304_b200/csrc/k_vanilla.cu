@@ -52,13 +52,14 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N;
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    const uint64_t *pk1s = a.pk_sh + (size_t)i * N, *pk2s = a.pk_sh + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     if constexpr (STW) tws.wait();
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     if (FORM == 0) {
       ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, PtLoad<INTS>{m, se1, c},
                              to_smem<LOGN, LM>(sm), stw);
@@ -78,13 +79,12 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
         if (i + 1 < hi) tws.issue(stw, tw + N);
       }
       stream_pairs<LOGN, 2, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
-        const uint64_t u0 = canon(v0), u1 = canon(v1);
-        const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
+        const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x), s1 = ld2_nc(pk1s + x), s2 = ld2_nc(pk2s + x);
         uint64_t a0, a1, b0, b1;
         ld2(ct0 + x, a0, a1);
         ld2(ct1 + x, b0, b1);
-        st2_cs(ct0 + x, add_mod(a0, mul_mod(p1.x, u0, c), q), add_mod(a1, mul_mod(p1.y, u1, c), q));
-        st2_cs(ct1 + x, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
+        st2_cs(ct0 + x, add_shoup(a0, v0, p1.x, s1.x, q), add_shoup(a1, v1, p1.y, s1.y, q));
+        st2_cs(ct1 + x, add_shoup(b0, v0, p2.x, s2.x, q), add_shoup(b1, v1, p2.y, s2.y, q));
       });
     } else {
       ntt_forward<LOGN, STW, NR, LM>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x), q); }, to_smem<LOGN, LM>(sm),
@@ -94,11 +94,11 @@ __global__ void __launch_bounds__(Geo<LOGN, vanilla_lm<FORM>()>::THREADS, Geo<LO
         if (i + 1 < hi) tws.issue(stw, tw + N);
       }
       stream_pairs<LOGN, 2, LM>(sm, [&](int x, uint64_t v0, uint64_t v1) {
-        const uint64_t u0 = canon(v0), u1 = canon(v1);
-        const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
-        st2(ct1 + x, mul_mod(p2.x, u0, c), mul_mod(p2.y, u1, c));  // temporary: pk2 u^
-        sm[pad16(x - loff)] = mul_mod(p1.x, u0, c);                 // in place: pk1 u^
-        sm[pad16(x - loff + 1)] = mul_mod(p1.y, u1, c);
+        const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x), s1 = ld2_nc(pk1s + x), s2 = ld2_nc(pk2s + x);
+        // [0, 2q): the inverse transforms take inputs below 4q
+        st2(ct1 + x, mul_shoup_lazy(v0, p2.x, s2.x, q), mul_shoup_lazy(v1, p2.y, s2.y, q));  // temporary: pk2 u^
+        sm[pad16(x - loff)] = mul_shoup_lazy(v0, p1.x, s1.x, q);                             // in place: pk1 u^
+        sm[pad16(x - loff + 1)] = mul_shoup_lazy(v1, p1.y, s1.y, q);
       });
       const Tw *itw = a.itw + (size_t)i * N;
       ntt_inverse<LOGN, false, LM>(sm, itw, c,
@@ -164,9 +164,10 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
     const uint64_t q = c.q, two_q = c.two_q;
     const Tw *tw = a.tw + (size_t)i * N;
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
+    const uint64_t *pk1s = a.pk_sh + (size_t)i * N, *pk2s = a.pk_sh + (size_t)(L + i) * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
-    auto canon = [&](uint64_t v) { return NR ? reduce64(v, q, c.mu64) : canon8(v, q, two_q); };
+    auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     tws.wait();
     // sample of coefficient x = 2 i' + r sits at i' = x >> 1
     ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c},
@@ -175,13 +176,12 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
                                      [&](int x, uint64_t v0, uint64_t v1) { st2(ct1 + x, canon(v0), canon(v1)); }, stw);
     ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> 1), q); },
         [&](int x, uint64_t v0, uint64_t v1) {
-          const uint64_t u0 = canon(v0), u1 = canon(v1);
-          const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x);
+          const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x), s1 = ld2_nc(pk1s + x), s2 = ld2_nc(pk2s + x);
           uint64_t a0, a1, b0, b1;
           ld2(ct0 + x, a0, a1);
           ld2(ct1 + x, b0, b1);
-          st2_cs(ct0 + x, add_mod(a0, mul_mod(p1.x, u0, c), q), add_mod(a1, mul_mod(p1.y, u1, c), q));
-          st2_cs(ct1 + x, add_mod(b0, mul_mod(p2.x, u0, c), q), add_mod(b1, mul_mod(p2.y, u1, c), q));
+          st2_cs(ct0 + x, add_shoup(a0, v0, p1.x, s1.x, q), add_shoup(a1, v1, p1.y, s1.y, q));
+          st2_cs(ct1 + x, add_shoup(b0, v0, p2.x, s2.x, q), add_shoup(b1, v1, p2.y, s2.y, q));
         },
         stw, [&]() {
           if (i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange

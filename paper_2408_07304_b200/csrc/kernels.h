@@ -47,6 +47,7 @@ struct VanillaArgs {
   const LimbConst *limbs;
   const Tw *tw, *itw;
   const uint64_t *pk;     // [2][L][N] NTT form
+  const uint64_t *pk_sh;  // [2][L][N] Shoup companions floor(pk 2^64 / q_i) (shoup_prep_kernel)
   const int64_t *m;       // [batch][N] or null
   uint64_t *ct;
   uint64_t seed, msg_base;
@@ -73,6 +74,7 @@ struct DecryptArgs {
   const LimbConst *limbs;
   const Tw *tw, *itw;
   const uint64_t *sk_ntt, *ct;
+  const uint64_t *sk_sh;  // [L][N] Shoup companions of sk_ntt
   int64_t *coeff_out;
   int32_t *status_out;
   uint64_t *xl_out;       // BFV: residues [B][L][N] for bfv_scale_kernel
@@ -174,6 +176,9 @@ cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaS
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
 cudaError_t launch_ct_add(const CtAddArgs &a, cudaStream_t s);
 cudaError_t launch_ct_sum(const CtSumArgs &a, cudaStream_t s);
+// w' = floor(w 2^64 / q_i) for the `words` words of keys [rows][L][N] (pk, sk)
+cudaError_t launch_shoup_prep(const LimbConst *limbs, const uint64_t *w, uint64_t *wp, size_t words, int log_n, int L,
+                              cudaStream_t s);
 cudaError_t launch_int_peak(const IntPeakArgs &a, int variant, int blocks, cudaStream_t s);
 
 }  // namespace zinc
