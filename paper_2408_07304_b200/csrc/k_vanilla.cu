@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
   const int64_t *m = a.m ? a.m + b * N : nullptr;
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
-    const uint64_t q = c.q, two_q = c.two_q;
+    const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N;
     const uint64_t *pk1 = a.pk + (size_t)i * N, *pk2 = a.pk + (size_t)(L + i) * N;
     const uint64_t *pk1s = a.pk_sh + (size_t)i * N, *pk2s = a.pk_sh + (size_t)(L + i) * N;
