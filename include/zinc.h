@@ -269,9 +269,10 @@ void zinc_launch_count_reset(void);
  *                                 launch prefetches the next chunk's slots into L2 for its encode
  *  ZINC_TUNE_NTT_CHUNK_MSGS       messages per chunk when slots feed a transform path (Zinc NTT form,
  *                                 vanilla): 0 (default) = 16 waves of the path kernel's CTAs
- *  ZINC_TUNE_SPLIT                1 (default): at N >= 2^14 the transform paths (Zinc NTT form, vanilla,
- *                                 decryption) run on S = N / 2^12 CTA clusters (2^12 words per CTA);
- *                                 0: the 2-CTA kernels
+ *  ZINC_TUNE_SPLIT                transform kernels at N >= 2^14: 1 (default) the faster family per path
+ *                                 (S = N / 2^12 CTA clusters of 2^12 words per CTA for Zinc NTT form,
+ *                                 vanilla COEFF form and decryption; 2-CTA kernels for vanilla NTT
+ *                                 form); 2: S-CTA clusters everywhere; 0: 2-CTA kernels everywhere
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_PDL = 2,
        ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_SPLIT = 5, ZINC_TUNE_COUNT = 6 };

@@ -557,8 +557,16 @@ static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, c
   a.msgs_per_cta = (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load());
   return a;
 }
-// The S-CTA cluster transform kernels (k_split.cu) serve N = 2^14 and 2^15.
-static bool use_split(const zinc_ctx *c) { return c->log_n >= 14 && g_tune[ZINC_TUNE_SPLIT].load() != 0; }
+// The S-CTA cluster transform kernels (k_split.cu) serve N = 2^14 and 2^15.  Knob 1 (auto):
+// the faster kernel family per path as measured on B200 (profiles/r02_sweep_*.jsonl): split
+// for Zinc NTT form, vanilla COEFF form and decryption; the 2-CTA parity-split kernel for
+// vanilla NTT form.  2: split everywhere; 0: 2-CTA kernels everywhere.
+enum SplitUse { SPLIT_ZINC_NTT, SPLIT_VANILLA_NTT, SPLIT_VANILLA_COEFF, SPLIT_DECRYPT };
+static bool use_split(const zinc_ctx *c, SplitUse what) {
+  const long long k = g_tune[ZINC_TUNE_SPLIT].load();
+  if (c->log_n < 14 || k == 0) return false;
+  return k == 2 || what != SPLIT_VANILLA_NTT;
+}
 static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
   size_t want = 2 * (size_t)c->num_sms;
   if (batch >= want) return c->L;
@@ -592,7 +600,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
-    if (use_split(c))
+    if (use_split(c, SPLIT_ZINC_NTT))
       LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt_split(c->log_n, a, kernel_mode(c), batch, groups, s));
     else
       LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, kernel_mode(c), batch, groups, s));
@@ -615,7 +623,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
-  if (use_split(c))
+  if (use_split(c, form == ZINC_FORM_NTT ? SPLIT_VANILLA_NTT : SPLIT_VANILLA_COEFF))
     LAUNCH(ZINC_K_VANILLA, s, launch_vanilla_split(c->log_n, a, form, kernel_mode(c), batch, groups, s));
   else
     LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, kernel_mode(c), batch, groups, s));
@@ -862,7 +870,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
     cudaError_t e;
     {
       TraceScope ts(ZINC_K_DECRYPT, s);
-      e = use_split(c) ? launch_decrypt_split(c->log_n, a, form, kernel_mode(c) == 0, batch, s)
+      e = use_split(c, SPLIT_DECRYPT) ? launch_decrypt_split(c->log_n, a, form, kernel_mode(c) == 0, batch, s)
                        : launch_decrypt(c->log_n, a, form, batch, s);
     }
     g_launches.fetch_add(1);

@@ -148,6 +148,34 @@ def test_encrypt_int64_sampled(Z, orc, name, path, form):
     _check_msgs(orc, s, path, form, m, np64(ct), seed, base, [0, 3, 19, 20, 36])
 
 
+@pytest.mark.parametrize("split", [0, 2])
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_both_transform_kernel_families_bit_exact(Z, orc, name, split):
+    """Both kernel families at N >= 2^14 (2-CTA parity split, S-CTA clusters; the default
+    picks one per path): every transform path and decryption bit-exact on a ragged batch."""
+    s = setup_for(Z, orc, name)
+    B = 21
+    m = int_plaintexts(s.cfg.log_n, B, seed=12, bound_bits=48)
+    seed, base = 0x5151, 777
+    old = Z.tune(Z.TUNE_SPLIT, split)
+    try:
+        cts = {("zinc", NTT): Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, dev_i64(m), seed, base),
+               ("vanilla", NTT): Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, dev_i64(m), seed, base),
+               ("vanilla", COEFF): Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, dev_i64(m), seed, base)}
+        dec = {f: Z.ckks_decrypt_batch(s.ctx, s.sk, f, cts[("vanilla", f)], slots=False) for f in (NTT, COEFF)}
+        torch.cuda.synchronize()
+    finally:
+        Z.tune(Z.TUNE_SPLIT, old)
+    for (path, form), ct in cts.items():
+        _check_msgs(orc, s, path, form, m, np64(ct), seed, base, [0, 10, 20])
+    for f, (coeff, st, _) in dec.items():
+        assert (np64(st) == 0).all()
+        c = np64(coeff)
+        for b in (0, 20):
+            x, ost = orc.decrypt(s.P, s.o_sk_ntt, np64(cts[("vanilla", f)][b]), f)
+            assert ost == 0 and np.array_equal(c[b], x)
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_encode_within_one(Z, orc, name):
     s = setup_for(Z, orc, name)
