@@ -191,6 +191,58 @@ def cpu_model():
     return "unknown"
 
 
+ORACLE_SUBSETS = (("C1", 256), ("C2", 256), ("C3", 64), ("C4", 16), ("C5", 64))
+ORACLE_ITEMS = ("zinc_coeff", "zinc_ntt", "vanilla_ntt", "vanilla_coeff")
+
+
+def oracle_suite(thread_counts, cap_s: float = 1.5, subsets=ORACLE_SUBSETS):
+    """SURVEY.md 8(d) "oracle beside it": the oracle as it stands, on the host's cores, for
+    every config's message subset (C1/C2 256, C3/C5 64, C4 16), both paths x both forms
+    (encode + Enc from slots per message), and the cache precompute; once per thread count
+    (1 = the paper's single-threaded setting; nproc = disjoint message ranges
+    on std::thread-free Python threads over the ctypes oracle, which releases the GIL).
+    Each item runs its subset or stops after `cap_s` seconds; ct/s = messages done / wall."""
+    import oracle as O
+    out = {"cpu": cpu_model(), "nproc": os.cpu_count(), "cap_s_per_item": cap_s, "runs": {}}
+    prepared = {}
+    for name, subset in subsets:
+        cfg = CONFIGS[name]
+        P = O.Params.make(cfg.log_n, cfg.bits, cfg.log_scale)
+        _, _, pk = O.keygen(P, cfg.key_seed)
+        t0 = time.perf_counter()
+        caches = {f: O.precompute_cache(P, pk, cfg.cache_seed, f) for f in (O.COEFF, O.NTT)}
+        prepared[name] = (cfg, P, pk, caches, subset, (time.perf_counter() - t0) / 2)
+    for threads in thread_counts:
+        run = {}
+        for name, (cfg, P, pk, caches, subset, cache_s) in prepared.items():
+            slots = slots_batch(cfg, 0, subset)
+
+            def enc(b, item):
+                m = O.encode(slots[b], cfg.log_n, cfg.log_scale)
+                if item == "zinc_coeff":
+                    O.zinc_encrypt(P, caches[O.COEFF], O.COEFF, m, cfg.enc_seed, b)
+                elif item == "zinc_ntt":
+                    O.zinc_encrypt(P, caches[O.NTT], O.NTT, m, cfg.enc_seed, b)
+                elif item == "vanilla_ntt":
+                    O.vanilla_encrypt(P, pk, m, cfg.enc_seed, b, O.NTT)
+                else:
+                    O.vanilla_encrypt(P, pk, m, cfg.enc_seed, b, O.COEFF)
+
+            r = {"subset": subset, "cache_precompute_s": cache_s}
+            with cf.ThreadPoolExecutor(threads) as ex:
+                for item in ORACLE_ITEMS:
+                    done, t0 = 0, time.perf_counter()
+                    while done < subset and time.perf_counter() - t0 < cap_s:
+                        k = min(threads, subset - done)
+                        list(ex.map(lambda b: enc(b, item), range(done, done + k)))
+                        done += k
+                    w = time.perf_counter() - t0
+                    r[item] = {"ct_per_s": done / w, "messages": done, "wall_s": w}
+            run[name] = r
+        out["runs"][str(threads)] = run
+    return out
+
+
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -210,7 +262,7 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.median(wall), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": cfg.name, "N": cfg.n, "L": cfg.L, "log_scale": cfg.log_scale, "form": "COEFF",
                    "input": "slots f64", "parallelism": "host threads"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
@@ -221,14 +273,17 @@ def run_reference(args, cfg):
 
 
 # ---------------------------------------------------------------- C5: batch sweep + cache precompute
-def c5_sweep(Z, torch, ctx_cache, batches=(1, 16, 256, 4096, 65536), reps=3):
+def c5_sweep(Z, torch, dev, rank, world, batches=(1, 16, 256, 4096, 65536), reps=3):
     """BASELINE C5: N=2^14, 8 x 54-bit, Delta=2^40, uniform slots; latency and ct/s of
-    Zinc (COEFF form) and vanilla (NTT form) per batch size, device time with CUDA
-    events (1 warm-up + `reps` timed, median), and zinc_precompute_cache timed alone."""
+    Zinc (COEFF form) and vanilla (NTT form) per batch size over all ranks (batch b split
+    as [r b / P, (r+1) b / P); ranks with no message are idle and report 0 ms), device time
+    with CUDA events (1 warm-up + `reps` timed, median; job time = max over ranks), and
+    zinc_precompute_cache timed alone."""
+    from paper_2408_07304_b200.dist import max_over_ranks, shard_range
     cfg = CONFIGS["C5"]
-    ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
+    ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale, device=dev.index or 0)
     sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
-    out = {"workload": "C5", "batches": {}}
+    out = {"workload": "C5", "ranks": world, "batches": {}}
 
     def timed(fn, n):
         fn()
@@ -250,20 +305,27 @@ def c5_sweep(Z, torch, ctx_cache, batches=(1, 16, 256, 4096, 65536), reps=3):
         out[f"cache_precompute_ms_{name}"] = ms
     free = torch.cuda.mem_get_info()[0]
     for B in batches:
+        b0, b1 = shard_range(rank, world, B)
+        nb = b1 - b0
         per = 2 * cfg.L * cfg.n * 8 + cfg.n // 2 * 8
-        if B * per > 0.85 * free:
-            out["batches"][str(B)] = {"skipped": f"needs {B * per / 2**30:.0f} GiB"}
+        skip = float(nb * per > 0.85 * free)
+        if max_over_ranks([skip], device=dev)[0] > 0:
+            out["batches"][str(B)] = {"skipped": f"needs {nb * per / 2**30:.0f} GiB per rank"}
             continue
-        z = torch.from_numpy(np.ascontiguousarray(slots_batch(cfg, 0, min(B, 4096)))).cuda()
-        if B > z.shape[0]:
-            z = z.repeat((B + z.shape[0] - 1) // z.shape[0], 1)[:B].contiguous()
-        ct = ctx.empty_ct(B)
-        zc = timed(lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, z, cfg.enc_seed, 0, out=ct), reps)
-        vn = timed(lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, z, cfg.enc_seed, 0, out=ct), reps)
+        zc = vn = 0.0
+        if nb:
+            z = torch.from_numpy(np.ascontiguousarray(slots_batch(cfg, b0, min(nb, 4096)))).to(dev)
+            if nb > z.shape[0]:
+                z = z.repeat((nb + z.shape[0] - 1) // z.shape[0], 1)[:nb].contiguous()
+            ct = ctx.empty_ct(nb)
+            zc = timed(lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, z, cfg.enc_seed, b0, out=ct), reps)
+            vn = timed(lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, z, cfg.enc_seed, b0, out=ct), reps)
+            del ct, z
+            torch.cuda.empty_cache()
+        zc, vn = max_over_ranks([zc, vn], device=dev)
         out["batches"][str(B)] = {"zinc_coeff_ms": zc, "zinc_coeff_ct_per_s": B / (zc / 1e3),
-                                  "vanilla_ntt_ms": vn, "vanilla_ntt_ct_per_s": B / (vn / 1e3)}
-        del ct, z
-        torch.cuda.empty_cache()
+                                  "vanilla_ntt_ms": vn, "vanilla_ntt_ct_per_s": B / (vn / 1e3),
+                                  "ranks_active": min(world, B), "ranks_idle": max(0, world - B)}
     ctx.close()
     return out
 
@@ -386,13 +448,20 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
-    ap.add_argument("--batch", type=int, default=0, help="messages per GPU (default: the config's batch)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="messages split over all ranks as [r B/P, (r+1) B/P) (default: the config's batch; "
+                         "strong scaling, SURVEY.md 8(e))")
+    ap.add_argument("--batch", type=int, default=0, help="messages per GPU instead (weak scaling)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: CUDA tensors through the host; tests)")
     ap.add_argument("--paths", default=",".join(PATHS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-oracle-suite", action="store_true", help="skip the per-config oracle runs (8(d))")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 batch sweep")
+    ap.add_argument("--c5-batches", default="1,16,256,4096,65536", help="C5 sweep batch sizes")
     ap.add_argument("--no-others", action="store_true", help="skip the C1/C2/C4 single-GPU lines")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -403,73 +472,107 @@ def main():
     import torch.distributed as dist
 
     import paper_2408_07304_b200 as Z
-    from paper_2408_07304_b200.dist import broadcast_words, max_over_ranks
+    from paper_2408_07304_b200.dist import broadcast_words, max_over_ranks, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    gpu = local % torch.cuda.device_count()  # one rank per GPU; gloo tests may share one
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+
+    def sum_over_ranks(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t)
+        return float(t.item())
+
     paths = [p for p in args.paths.split(",") if p]
-    B = args.batch or cfg.batch
-    ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale, device=local)
+    if args.batch:
+        B_global, scaling = args.batch * world, "weak"
+    else:
+        B_global, scaling = args.global_batch or cfg.batch, "strong"
+    b0, b1 = shard_range(rank, world, B_global)
+    B = b1 - b0  # this rank's messages [b0, b1), msg_base = b0: bit-identical for any P
+    ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale, device=gpu)
     stream = torch.cuda.current_stream()
 
-    # keys + cache on rank 0, NCCL-broadcast once; every rank
-    # also regenerates them locally and checks the broadcast copies bit for bit.
+    # keys + cache on rank 0, broadcast once; every rank also regenerates
+    # them locally and checks the broadcast copies bit for bit.
     sk, _, pk_local = Z.zinc_keygen(ctx, cfg.key_seed)
     cache_local = {f: Z.zinc_precompute_cache(ctx, pk_local, cfg.cache_seed, f) for f in (Z.COEFF, Z.NTT)}
     pk = pk_local.clone()
     cache = {f: c.clone() for f, c in cache_local.items()}
-    bcast_ok = True
+    bcast_ok, bcast_ms = True, 0.0
     if world > 1:
+        if rank != 0:  # receivers start from garbage so the check is meaningful
+            for t in (pk, cache[Z.COEFF], cache[Z.NTT]):
+                t.fill_(7)
         torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
         broadcast_words([pk, cache[Z.COEFF], cache[Z.NTT]], src=0)
         torch.cuda.synchronize()
-        bcast_ok = all(torch.equal(a, b) for a, b in ((pk, pk_local), (cache[0], cache_local[0]),
-                                                       (cache[1], cache_local[1])))
+        bcast_ms = 1e3 * (time.perf_counter() - t0)
+        ok = all(torch.equal(a, b) for a, b in ((pk, pk_local), (cache[0], cache_local[0]), (cache[1], cache_local[1])))
+        bcast_ok = sum_over_ranks(0 if ok else 1) == 0
 
-    # inputs: this rank's messages [rank*B, (rank+1)*B), resident in HBM
-    base = rank * B
+    # inputs: this rank's messages, resident in HBM
     t0 = time.time()
-    slots_h = slots_batch(cfg, base, B)
+    slots_h = slots_batch(cfg, b0, B)
     if cfg.complex_slots:
         slots_h = np.stack([slots_h.real, slots_h.imag], axis=-1)
-    slots = torch.from_numpy(np.ascontiguousarray(slots_h)).to(ctx.dev())
+    slots = torch.from_numpy(np.ascontiguousarray(slots_h)).to(dev)
     ct = ctx.empty_ct(B)
-    log(f"[rank {rank}] inputs ready ({time.time() - t0:.1f}s): {B} msgs, ct buffer {ct.numel() * 8 / 2**30:.1f} GiB")
+    log(f"[rank {rank}] inputs ready ({time.time() - t0:.1f}s): messages [{b0}, {b1}), "
+        f"ct buffer {ct.numel() * 8 / 2**30:.1f} GiB")
 
     def run(path):
+        if B == 0:
+            return
         if path == "zinc_coeff":
-            Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, slots, cfg.enc_seed, base, out=ct)
+            Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, slots, cfg.enc_seed, b0, out=ct)
         elif path == "zinc_ntt":
-            Z.zinc_encrypt_batch(ctx, cache[Z.NTT], Z.NTT, slots, cfg.enc_seed, base, out=ct)
+            Z.zinc_encrypt_batch(ctx, cache[Z.NTT], Z.NTT, slots, cfg.enc_seed, b0, out=ct)
         elif path == "vanilla_ntt":
-            Z.ckks_encrypt_batch(ctx, pk, Z.NTT, slots, cfg.enc_seed, base, out=ct)
+            Z.ckks_encrypt_batch(ctx, pk, Z.NTT, slots, cfg.enc_seed, b0, out=ct)
         elif path == "vanilla_coeff":
-            Z.ckks_encrypt_batch(ctx, pk, Z.COEFF, slots, cfg.enc_seed, base, out=ct)
+            Z.ckks_encrypt_batch(ctx, pk, Z.COEFF, slots, cfg.enc_seed, b0, out=ct)
 
     # validity gate: every path's output, from the exact call the timed region
     # makes, decrypts within tolerance with a consistent CRT, sampled at the first and last
-    # message of every 256-message block -- so every chunk of every chunk chain (Zinc COEFF:
-    # 256-message chunks; transform paths: 16-wave chunks) and both halves of C3's A13 mix
+    # message of every 256-message block of every rank's shard -- so every chunk of every
+    # chunk chain (Zinc COEFF: 256-message chunks; transform paths: 16-wave chunks) and both
+    # halves of C3's A13 mix
     validity = {}
     probe_idx = sorted(set([b for k in range(0, B, 256) for b in (k, min(B, k + 256) - 1)]))
-    pidx = torch.tensor(probe_idx, device=ctx.dev())
-    ref_all = slots_h[probe_idx, :, 0] + 1j * slots_h[probe_idx, :, 1] if cfg.complex_slots else slots_h[probe_idx]
+    pidx = torch.tensor(probe_idx, dtype=torch.long, device=dev)
+    ref_all = (slots_h[probe_idx, :, 0] + 1j * slots_h[probe_idx, :, 1]) if cfg.complex_slots else slots_h[probe_idx]
+    failed = 0
     for p in paths:
         run(p)
-        form = Z.COEFF if p.endswith("coeff") else Z.NTT
-        _, st, z = Z.ckks_decrypt_batch(ctx, sk, form, ct.index_select(0, pidx).contiguous())
-        err = float(np.max(np.abs(z.cpu().numpy() - ref_all)))
-        ok = int(st.sum().item()) == 0 and err < cfg.tolerance()
-        validity[p] = {"crt_ok": int(st.sum().item()) == 0, "max_abs_err": err, "ok": ok,
-                       "tolerance": cfg.tolerance(), "sampled": len(probe_idx)}
-        if not ok:
+        ok, crt, err = True, True, 0.0
+        if probe_idx:
+            form = Z.COEFF if p.endswith("coeff") else Z.NTT
+            _, st, z = Z.ckks_decrypt_batch(ctx, sk, form, ct.index_select(0, pidx).contiguous())
+            err = float(np.max(np.abs(z.cpu().numpy() - ref_all)))
+            crt = int(st.sum().item()) == 0
+            ok = crt and err < cfg.tolerance()
+        err = max_over_ranks([err], device=dev)[0]
+        bad = sum_over_ranks(0 if ok else 1)
+        validity[p] = {"crt_ok": bad == 0 and crt, "max_abs_err": err, "ok": bad == 0, "tolerance": cfg.tolerance(),
+                       "sampled": int(sum_over_ranks(len(probe_idx)))}
+        failed += bad > 0
+        if bad:
             log(f"validity gate failed for {p}: {validity[p]}")
-            sys.exit(3)
-    validity["sampled_indices"] = probe_idx
+    if failed:
+        sys.exit(3)
+    validity["sampled_indices_rank0"] = [b0 + b for b in probe_idx] if rank == 0 else None
 
     for _ in range(args.warmup):
         for p in paths:
@@ -477,7 +580,7 @@ def main():
     torch.cuda.synchronize()
 
     # int-peak microkernel (K11) per butterfly variant: the denominators of the transform paths
-    sink = torch.zeros(2, dtype=torch.uint64, device=ctx.dev())
+    sink = torch.zeros(2, dtype=torch.uint64, device=dev)
     nr_ok = max(ctx.q) < (1 << 58)
     k11 = {}
     for v in ((1, 2, 3) if nr_ok else (2, 3)):
@@ -496,7 +599,7 @@ def main():
     # ---------------- timed region
     ev = {p: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)] for p in paths}
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -527,10 +630,10 @@ def main():
             a0, a1 = prof.get(k, (0.0, 0))
             prof[k] = (a0 + v[0] * args.steps, a1 + v[1] * args.steps)
 
-    seg = {p: sum(a.elapsed_time(b) for a, b in ev[p]) / args.steps for p in paths}  # ms per step per path
-    seg = dict(zip(paths, max_over_ranks([seg[p] for p in paths], device=ctx.dev())))
-    total_msgs = B * world
-    path_out = {p: {"ct_per_s": total_msgs / (seg[p] / 1e3), "ms": seg[p]} for p in paths}
+    seg_local = {p: sum(a.elapsed_time(b) for a, b in ev[p]) / args.steps for p in paths}  # ms per step
+    seg = dict(zip(paths, max_over_ranks([seg_local[p] for p in paths], device=dev)))
+    launches = int(sum_over_ranks(launches))
+    path_out = {p: {"ct_per_s": B_global / (seg[p] / 1e3), "ms": seg[p]} for p in paths}
 
     peak, peak_src = load_peaks()
     result = None
@@ -546,10 +649,11 @@ def main():
             roof = {"bound": "hbm", "kernel": "zinc_coeff_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                     "algorithmic_bytes_per_ct": kbytes, "msgs_per_launch": msgs_per_launch,
-                    "launch_ms": per_launch_ms, "kernel_share_of_zinc_segment": zk_ms / args.steps / seg["zinc_coeff"]
-                    if "zinc_coeff" in seg else None,
+                    "launch_ms": per_launch_ms,
+                    "kernel_share_of_zinc_segment": zk_ms / args.steps / seg_local["zinc_coeff"]
+                    if "zinc_coeff" in seg_local else None,
                     "kernel_timing": "CUDA events around each launch of one extra traced step (on the launch "
-                                     "stream), scaled to the timed steps"}
+                                     "stream), scaled to the timed steps; rank 0's own launches"}
             tr = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(tr):
                 t = json.load(open(tr)).get("zinc_coeff_kernel")
@@ -560,7 +664,7 @@ def main():
         sm_mhz = clk["sm_mhz"] or 1965.0
         for p, kname in (("zinc_ntt", "zinc_ntt_kernel"), ("vanilla_ntt", "vanilla_kernel"),
                          ("vanilla_coeff", "vanilla_kernel")):
-            if p not in seg:
+            if p not in seg_local or B == 0:
                 continue
             nf, ni = path_transforms(cfg, p)
             # the path's own peak: its forward and inverse butterflies at their K11 rates
@@ -568,7 +672,7 @@ def main():
             pd = (nf + ni) / (nf / alu_peak_derived(sm_mhz, BFLY[fwd_v][2]) + ni / alu_peak_derived(sm_mhz, BFLY[3][2]))
             kms = prof_path[p].get(kname, (0.0, 0))[0]
             bfc = butterflies_per_ct(cfg, p)
-            ach = bfc * B / (seg[p] / 1e3)
+            ach = bfc * B / (seg_local[p] / 1e3)
             kach = bfc * B / (kms / 1e3) if kms else ach
             alu[p] = {"bound": "alu", "kernel": kname, "achieved": kach / 1e9, "peak": peak_p / 1e9,
                       "unit": "Gbutterfly/s", "frac": kach / peak_p, "achieved_path": ach / 1e9,
@@ -578,25 +682,29 @@ def main():
                                      f"{BFLY[fwd_v][0]} + {ni} x {BFLY[3][0]} per ct (harmonic mix); peak_derived: "
                                      f"148 SMs x sm_mhz x 64 fma-pipe lanes/clk / SASS fma ops per butterfly "
                                      f"({BFLY[fwd_v][2]} {BFLY[fwd_v][0]}, {BFLY[3][2]} {BFLY[3][0]})"}
+        multi = "" if world == 1 else f", {world} ranks"
         result = {
             "metric": METRIC,
             "value": path_out["zinc_coeff"]["ct_per_s"] if "zinc_coeff" in path_out else None,
             "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sum(seg.values()),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (workloads.py seeded slots; paper datasets not in container)",
             "config": {"workload": cfg.name, "N": cfg.n, "L": cfg.L, "bits": list(cfg.bits),
-                       "log_scale": cfg.log_scale, "batch_per_gpu": B, "global_batch": total_msgs,
+                       "log_scale": cfg.log_scale, "global_batch": B_global, "batch_rank0": B,
+                       "shard": "rank r: messages [r B/P, (r+1) B/P), msg_base = r B/P",
                        "input": "f64 slots in HBM", "value_path": "zinc_coeff (encode + Zinc add/inject, COEFF form)",
-                       "l2": "inputs (1 GiB slots) and outputs (32 GiB ct) exceed the 126 MB L2; no flush",
-                       "parallelism": f"dp{world} (message-sharded, NCCL broadcast of pk + cache)"},
+                       "l2": "inputs and outputs (GiB) exceed the 126 MB L2; no flush",
+                       "parallelism": f"dp{world} (message-sharded, {args.backend if world > 1 else 'no'} broadcast "
+                                      f"of pk + caches{multi})"},
             "paths": path_out,
             "zinc_vs_vanilla": {
                 "coeff_form": path_out["zinc_coeff"]["ct_per_s"] / path_out["vanilla_coeff"]["ct_per_s"]
                 if {"zinc_coeff", "vanilla_coeff"} <= set(path_out) else None,
                 "ntt_form": path_out["zinc_ntt"]["ct_per_s"] / path_out["vanilla_ntt"]["ct_per_s"]
                 if {"zinc_ntt", "vanilla_ntt"} <= set(path_out) else None},
-            "hbm_frac_step": (bpc * B / (seg["zinc_coeff"] / 1e3) / 1e9) / peak if "zinc_coeff" in seg else None,
+            "hbm_frac_step": (bpc * B / (seg_local["zinc_coeff"] / 1e3) / 1e9) / peak
+            if "zinc_coeff" in seg_local and B else None,
             "roofline": roof,
             "roofline_alu": alu,
             "k11_gbfly": {BFLY[v][0]: r / 1e9 for v, r in k11.items()},
@@ -606,40 +714,52 @@ def main():
             "clocks": clk,
             "validity": validity,
             "broadcast_ok": bcast_ok,
+            "broadcast_ms": bcast_ms if world > 1 else None,
         }
+        if world > 1:
+            result["multi_gpu"] = {"backend": args.backend, "ranks": world, "hardware": "measured" if
+                                   args.backend == "nccl" else "logic test (gloo; ranks may share a GPU)"}
 
-    if rank == 0 and "vanilla_coeff" in paths:
+    if "vanilla_coeff" in paths:
         # batched decrypt + decode (Eq. 10, CRT check on every limb) of the
-        # step's last output (vanilla COEFF form), device-timed like the paths
-        dms = _timed(torch, lambda: Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct), 3)
-        Z.profile_enable(True)
-        Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct)
-        torch.cuda.synchronize()
-        dk = Z.profile_read().get("decrypt_kernel", (0.0, 0))[0]
-        Z.profile_enable(False)
-        dpeak = 2 / (1 / k11[2] + 1 / k11[3])
-        dbf = butterflies_per_ct(cfg, "decrypt_coeff")
-        result["decrypt_decode"] = {"form": "COEFF", "ms": dms, "ct_per_s": B / (dms / 1e3),
-                                    "transforms_per_ct": 2 * cfg.L,
-                                    "note": "x = c1 + c2 s on every limb (NTT + INTT per limb), CRT check, FP64 decode"}
-        result["roofline_alu"]["decrypt_coeff"] = {
-            "bound": "alu", "kernel": "decrypt_kernel", "achieved": dbf * B / (dk / 1e3) / 1e9 if dk else None,
-            "peak": dpeak / 1e9, "unit": "Gbutterfly/s", "frac": dbf * B / (dk / 1e3) / dpeak if dk else None,
-            "butterflies_per_ct": dbf, "transforms_per_ct": {"forward": cfg.L, "inverse": cfg.L},
-            "peak_source": "measured K11 with the kernel's butterflies: L x ct_bfly_a + L x gs_bfly per ct"}
+        # step's last output (vanilla COEFF form), device-timed like the paths, every rank
+        dms = _timed(torch, lambda: Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct), 3) if B else 0.0
+        dk = 0.0
+        if B:
+            Z.profile_enable(True)
+            Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct)
+            torch.cuda.synchronize()
+            dk = Z.profile_read().get("decrypt_kernel", (0.0, 0))[0]
+            Z.profile_enable(False)
+        dmax = max_over_ranks([dms], device=dev)[0]
+        if rank == 0:
+            dpeak = 2 / (1 / k11[2] + 1 / k11[3])
+            dbf = butterflies_per_ct(cfg, "decrypt_coeff")
+            result["decrypt_decode"] = {"form": "COEFF", "ms": dmax, "ct_per_s": B_global / (dmax / 1e3),
+                                        "transforms_per_ct": 2 * cfg.L,
+                                        "note": "x = c1 + c2 s on every limb (NTT + INTT per limb), CRT check, "
+                                                "FP64 decode"}
+            result["roofline_alu"]["decrypt_coeff"] = {
+                "bound": "alu", "kernel": "decrypt_kernel", "achieved": dbf * B / (dk / 1e3) / 1e9 if dk else None,
+                "peak": dpeak / 1e9, "unit": "Gbutterfly/s", "frac": dbf * B / (dk / 1e3) / dpeak if dk else None,
+                "butterflies_per_ct": dbf, "transforms_per_ct": {"forward": cfg.L, "inverse": cfg.L},
+                "peak_source": "measured K11 with the kernel's butterflies: L x ct_bfly_a + L x gs_bfly per ct"}
+    # aggregation of each rank's shard (Eq. 2, HBM-bound read of every ciphertext)
+    agg = ctx.empty_key()
+    ams = _timed(torch, lambda: Z.zinc_ct_sum_batch(ctx, ct, out=agg), 3) if B else 0.0
+    amax = max_over_ranks([ams], device=dev)[0]
     if rank == 0:
-        # aggregation of the whole batch (Eq. 2, HBM-bound read of every ciphertext)
-        agg = ctx.empty_key()
-        ams = _timed(torch, lambda: Z.zinc_ct_sum_batch(ctx, ct, out=agg), 3)
         rb = B * 2 * cfg.L * cfg.n * 8
-        result["aggregate"] = {"ms": ams, "ct_per_s": B / (ams / 1e3), "GBps": rb / (ams / 1e3) / 1e9,
-                               "frac_hbm": rb / (ams / 1e3) / 1e9 / peak, "batch": B,
-                               "note": "zinc_ct_sum_batch over the step's last output (read 2 L N 8 B per ct)"}
-    if rank == 0 and world == 1 and not args.no_c5:
+        result["aggregate"] = {"ms": amax, "ct_per_s": B_global / (amax / 1e3), "GBps_rank0": rb / (ams / 1e3) / 1e9,
+                               "frac_hbm_rank0": rb / (ams / 1e3) / 1e9 / peak, "batch_rank0": B,
+                               "note": "zinc_ct_sum_batch over each rank's last output (read 2 L N 8 B per ct)"}
+    if not args.no_c5:
         del ct
-        torch.cuda.empty_cache()
-        result["c5"] = c5_sweep(Z, torch, None)
         ct = None
+        torch.cuda.empty_cache()
+        c5 = c5_sweep(Z, torch, dev, rank, world, batches=tuple(int(x) for x in args.c5_batches.split(",") if x))
+        if rank == 0:
+            result["c5"] = c5
     if rank == 0 and world == 1 and not args.no_others:
         if ct is not None:
             del ct
@@ -649,38 +769,47 @@ def main():
         result["paper_params"] = paper_params(Z, torch)
         result["schemes"] = schemes(Z, torch)
 
-    # ---------------- end to end through the host-buffer API
+    # ---------------- end to end through the host-buffer API, every rank on its shard
     if not args.no_e2e:
         import psutil
-        per_msg = slots_h[0].nbytes + 2 * cfg.L * cfg.n * 8
+        per_msg = (slots_h[0].nbytes if B else 0) + 2 * cfg.L * cfg.n * 8
         budget = 0.6 * psutil.virtual_memory().available / max(1, world)
         Be = int(min(B, budget // per_msg))
-        pt_h = torch.from_numpy(np.ascontiguousarray(slots_h[:Be])).pin_memory()
-        ct_h = torch.empty((Be, 2, cfg.L, cfg.n), dtype=torch.uint64, pin_memory=True)
-        Z.zinc_encrypt_batch_host(ctx, 0, cache[Z.COEFF], Z.COEFF, pt_h, cfg.enc_seed, base, ct_h)
+        if Be:
+            pt_h = torch.from_numpy(np.ascontiguousarray(slots_h[:Be])).pin_memory()
+            ct_h = torch.empty((Be, 2, cfg.L, cfg.n), dtype=torch.uint64, pin_memory=True)
+            Z.zinc_encrypt_batch_host(ctx, 0, cache[Z.COEFF], Z.COEFF, pt_h, cfg.enc_seed, b0, ct_h)
         ts = []
         for _ in range(args.e2e_steps):
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
-            Z.zinc_encrypt_batch_host(ctx, 0, cache[Z.COEFF], Z.COEFF, pt_h, cfg.enc_seed, base, ct_h)
+            if Be:
+                Z.zinc_encrypt_batch_host(ctx, 0, cache[Z.COEFF], Z.COEFF, pt_h, cfg.enc_seed, b0, ct_h)
             ts.append(time.perf_counter() - t0)
-        tt = max_over_ranks([min(ts)], device=ctx.dev())[0]
+        tt = max_over_ranks([min(ts)], device=dev)[0]
+        be_tot = sum_over_ranks(Be)
         if rank == 0:
-            result["e2e"] = {"value": Be * world / tt, "unit": UNIT,
-                             "h2d_bytes_per_step": int(pt_h.numel() * 8), "d2h_bytes_per_step": int(ct_h.numel() * 8),
-                             "batch_per_gpu": Be, "api": "zinc_encrypt_batch_host (pinned host in/out, 2 streams)",
-                             "path": "zinc_coeff", "timer": "host perf_counter around the blocking call, best of "
-                             f"{args.e2e_steps}"}
-        del pt_h, ct_h
+            result["e2e"] = {"value": be_tot / tt, "unit": UNIT,
+                             "h2d_bytes_per_step": int(pt_h.numel() * 8 if Be else 0),
+                             "d2h_bytes_per_step": int(ct_h.numel() * 8 if Be else 0),
+                             "bytes_scope": "rank 0's per-step copies", "global_batch": int(be_tot),
+                             "api": "zinc_encrypt_batch_host (pinned host in/out, 2 streams)",
+                             "path": "zinc_coeff", "timer": "host perf_counter around the blocking call on every "
+                             f"rank after a barrier, max over ranks, best of {args.e2e_steps}"}
+        if Be:
+            del pt_h, ct_h
 
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # ---------------- the oracle beside it (rank 0's host cores; the other ranks wait)
+    if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         r, n, w, vr, vn = oracle_rate(cfg, args.cpu_seconds, threads)
         result["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "kind": "oracle",
                                   "sample": f"{n} {cfg.name} Zinc COEFF encryptions from slots (oracle encode + "
                                             f"Enc_z) in {w:.1f} s; vanilla NTT-form {vn} msgs: {vr:.2f} ct/s",
                                   "vanilla_ct_per_s": vr, "cpu": cpu_model()}
+        if not args.no_oracle_suite:
+            result["cpu_baseline"]["suite"] = oracle_suite(sorted({1, threads}))
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
