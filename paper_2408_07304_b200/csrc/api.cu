@@ -525,6 +525,7 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
                                cudaStream_t s, bool wide = false) {
   EncodeArgs a = encode_args(c, kind, slots, m);
   a.wide = wide ? 1 : 0;
+  a.fast = batch < (size_t)c->num_sms ? 1 : 0;  // few messages: latency, not throughput
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
@@ -584,6 +585,8 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     int threads = 256;
     while (threads > 32 && zinc_coeff_smem(c->L, threads) > 72 * 1024) threads /= 2;
     const size_t gy = (batch + a.msgs_per_cta - 1) / a.msgs_per_cta;
+    // small batches: smaller coefficient tiles, so the grid still covers every SM
+    while (threads > 32 && (size_t)(c->n / (2 * threads)) * gy < (size_t)c->num_sms) threads /= 2;
     LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff(a, threads, (int)gy, 0, s));
     return ZINC_OK;
   }
@@ -600,6 +603,8 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
+    // a handful of messages: the two transforms on separate CTAs as well
+    a.t_split = batch * (size_t)groups * 2 * ((size_t)c->n >> 12) <= 2 * (size_t)c->num_sms ? 1 : 0;
     if (use_split(c, SPLIT_ZINC_NTT))
       LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt_split(c->log_n, a, kernel_mode(c), batch, groups, s));
     else
@@ -623,10 +628,19 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
-  if (use_split(c, form == ZINC_FORM_NTT ? SPLIT_VANILLA_NTT : SPLIT_VANILLA_COEFF))
+  // a handful of messages (NTT form): the three transforms on separate CTAs, then a combine
+  const bool t_split = c->log_n >= 14 && g_tune[ZINC_TUNE_SPLIT].load() != 0 && form == ZINC_FORM_NTT &&
+                       batch * (size_t)groups * 3 * ((size_t)c->n >> 12) <= 2 * (size_t)c->num_sms;
+  ScratchBuf uhat(s);
+  if (t_split) {
+    CUDA_TRY(uhat.alloc(batch * (size_t)c->L * c->n * 8));
+    a.u_hat = uhat.as<uint64_t>();
+  }
+  if (t_split || use_split(c, form == ZINC_FORM_NTT ? SPLIT_VANILLA_NTT : SPLIT_VANILLA_COEFF))
     LAUNCH(ZINC_K_VANILLA, s, launch_vanilla_split(c->log_n, a, form, kernel_mode(c), batch, groups, s));
   else
     LAUNCH(ZINC_K_VANILLA, s, launch_vanilla(c->log_n, a, form, kernel_mode(c), batch, groups, s));
+  if (t_split) LAUNCH(ZINC_K_VANILLA, s, launch_vanilla_combine(a, batch, c->n, s));
   return ZINC_OK;
 }
 

@@ -93,6 +93,19 @@ ZINC_DEV void encode_fft(const double2 *tw, Ld lds, St sts) {
     fft_pass<LH, P::K1, P::K2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
     __syncthreads();
     fft_pass<LH, P::K1 + P::K2, P::K3, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+  } else if constexpr (NPASS == 6) {  // radix-4 passes: 1024 threads on one message (latency)
+    static_assert(LH >= 11, "six-pass plan");
+    fft_pass<LH, 0, 2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 2, 2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 4, 2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 6, 2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 8, 2, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
+    __syncthreads();
+    fft_pass<LH, 10, LH - 10, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
   } else {
     static_assert(LH >= 10, "four-pass plan");
     fft_pass<LH, 0, 3, THREADS, true, false, 1, TW_SMEM>(tw, lds, sts);
@@ -112,7 +125,7 @@ template <int LOGM, bool WIDE = false, int THREADS = 256, int NPASS = 3>
 ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   constexpr int M = 1 << LOGM, LH = LOGM - 1, H = 1 << LH;
   constexpr int PER = M / THREADS;
-  static_assert(NPASS == 4 || FftPlan<LH>::THREADS == THREADS, "plan");
+  static_assert(NPASS != 3 || FftPlan<LH>::THREADS == THREADS, "plan");
   double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2], then post tables
   double2 *sptw = stw + H / 2;
   constexpr int NPT = encode_post_tw_entries<LOGM>();

@@ -93,6 +93,16 @@ __global__ void __launch_bounds__(256, (LOGM <= 13 ? 2 : 1)) encode_real_kernel(
   extern __shared__ __align__(16) double2 buf[];
   encode_real_body<LOGM, WIDE>(a, blockIdx.x, buf);
 }
+// Latency variant for small batches (fewer messages than SMs): the same encode with up to
+// 1024 threads on one message (radix-4 passes; 512 threads with radix-8 at N = 2^13).
+template <int LOGM> struct FastEnc {
+  static constexpr int THREADS = LOGM >= 13 ? 1024 : 512, NPASS = LOGM >= 13 ? 6 : 4;
+};
+template <int LOGM, bool WIDE>
+__global__ void __launch_bounds__(FastEnc<LOGM>::THREADS, 1) encode_real_fast_kernel(EncodeArgs a) {
+  extern __shared__ __align__(16) double2 buf[];
+  encode_real_body<LOGM, WIDE, FastEnc<LOGM>::THREADS, FastEnc<LOGM>::NPASS>(a, blockIdx.x, buf);
+}
 
 // ============================================================ decode (C-10)
 // Mirror image of encode.  Split at M = 2^14: the first DIF stage (pairs j,
@@ -148,6 +158,13 @@ template <int LOGM> static size_t fft_smem() {
 template <int LOGM>
 static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
   if (!a.complex_slots) {
+    if constexpr (LOGM >= 12) {
+      if (a.fast) {
+        constexpr int T = FastEnc<LOGM>::THREADS;
+        if (a.wide) return launch_ex(encode_real_fast_kernel<LOGM, true>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
+        return launch_ex(encode_real_fast_kernel<LOGM, false>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
+      }
+    }
     if (a.wide) return launch_ex(encode_real_kernel<LOGM, true>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
     return launch_ex(encode_real_kernel<LOGM, false>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
   }

@@ -83,8 +83,10 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
   tws.init();
   cb.init<S>();
   tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
-  sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
-  sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ZINC_E2);
+  // small batches spread the two transforms over gridDim.z = 2 (t = blockIdx.z)
+  const int t_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, t_hi = gridDim.z > 1 ? t_lo + 1 : 2;
+  if (t_lo == 0) sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
+  if (t_hi == 2) sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ZINC_E2);
   __syncthreads();
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     tws.wait();
 #pragma unroll 1
-    for (int t = 0; t < 2; ++t) {
+    for (int t = t_lo; t < t_hi; ++t) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
       ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoad<INTS, G::LOGS>{m, t ? se2 : se1, c, t},
@@ -108,7 +110,7 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
             }
           },
           stw, [&]() {
-            if (t == 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
+            if (t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
           });
     }
   }
@@ -155,9 +157,12 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
   tws.init();
   cb.init<S>();
   tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
-  sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
-  sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
-  sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
+  // small batches spread the three transforms over gridDim.z = 3 (t = blockIdx.z; the u
+  // transform then writes u^ to a.u_hat and vanilla_combine_kernel forms pk u^)
+  const int t_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, t_hi = gridDim.z > 1 ? t_lo + 1 : 3;
+  if (t_hi == 3) sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
+  if (t_lo == 0) sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
+  if (t_lo <= 1 && t_hi >= 2) sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
   __syncthreads();
   pdl_trigger();
   pdl_wait();
@@ -173,11 +178,11 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
     auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     tws.wait();
 #pragma unroll 1
-    for (int t = 0; t < 3; ++t) {
+    for (int t = t_lo; t < t_hi; ++t) {
       ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t},
           [&](int x0, uint64_t (&v)[S]) {
-            if (t < 2) {
-              uint64_t *dst = (t ? ct1 : ct0) + x0;
+            if (t < 2 || gridDim.z > 1) {
+              uint64_t *dst = (t == 0 ? ct0 : t == 1 ? ct1 : a.u_hat + (b * L + i) * N) + x0;
 #pragma unroll
               for (int u = 0; u < S; u += 2) st2(dst + u, canon(v[u]), canon(v[u + 1]));
             } else {
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
             }
           },
           stw, [&]() {
-            if (t == 2 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
+            if (t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
           });
     }
   }
@@ -375,7 +380,7 @@ template <int LOGN> static size_t split_smem(int extra) {
 template <int LOGN>
 static cudaError_t launch_zinc_ntt_split_t(const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {
   using G = SplitGeo<LOGN>;
-  const dim3 grid((unsigned)(batch * G::S), groups);
+  const dim3 grid((unsigned)(batch * G::S), groups, a.t_split ? 2 : 1);
   const size_t smem = split_smem<LOGN>(2 * G::NL);
   if (mode == 2) return launch_ex(zinc_ntt_split_kernel<LOGN, 2>, grid, G::THREADS, smem, G::S, s, a);
   if (mode == 1) return launch_ex(zinc_ntt_split_kernel<LOGN, 1>, grid, G::THREADS, smem, G::S, s, a);
@@ -385,7 +390,7 @@ template <int LOGN>
 static cudaError_t launch_vanilla_split_t(const VanillaArgs &a, int form, int mode, size_t batch, int groups,
                                           cudaStream_t s) {
   using G = SplitGeo<LOGN>;
-  const dim3 grid((unsigned)(batch * G::S), groups);
+  const dim3 grid((unsigned)(batch * G::S), groups, form == 0 && a.u_hat ? 3 : 1);
   const size_t smem = split_smem<LOGN>(2 * G::NL + G::NL / 4);
 #define VS(K, M) launch_ex(K<LOGN, M>, grid, G::THREADS, smem, G::S, s, a)
   if (form == 0) return mode == 2 ? VS(vanilla_ntt_split_kernel, 2) : mode == 1 ? VS(vanilla_ntt_split_kernel, 1)

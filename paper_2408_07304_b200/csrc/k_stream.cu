@@ -110,6 +110,7 @@ cudaError_t launch_pt_add(const PtAddArgs &a, cudaStream_t s) {
 // 64 bits) corrects it.
 __global__ void __launch_bounds__(256) shoup_prep_kernel(const LimbConst *limbs, const uint64_t *w, uint64_t *wp,
                                                           size_t words, int log_n, int L) {
+  pdl_trigger();  // in a PDL chain: the next kernel may launch; this one reads only the key
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < words; idx += (size_t)gridDim.x * blockDim.x) {
     const LimbConst &c = limbs[(idx >> log_n) % L];
     const uint64_t x = w[idx];
@@ -121,12 +122,40 @@ __global__ void __launch_bounds__(256) shoup_prep_kernel(const LimbConst *limbs,
     }
     wp[idx] = est;
   }
+  pdl_wait();  // complete only after the kernel before it (the chain's order stays transitive)
 }
 cudaError_t launch_shoup_prep(const LimbConst *limbs, const uint64_t *w, uint64_t *wp, size_t words, int log_n, int L,
                               cudaStream_t s) {
   const unsigned blocks = (unsigned)std::min<size_t>((words + 255) / 256, 148 * 8);
   shoup_prep_kernel<<<blocks, 256, 0, s>>>(limbs, w, wp, words, log_n, L);
   return cudaGetLastError();
+}
+
+// ============================================================ vanilla combine (small batches)
+// After a transform-split vanilla NTT-form launch: c1 = NTT(m + e1) + pk1 u^, c2 = NTT(e2) +
+// pk2 u^ (Eq. 8) word by word, u^ from a.u_hat.  16-byte accesses.
+__global__ void __launch_bounds__(256) vanilla_combine_kernel(VanillaArgs a, size_t batch, int n) {
+  pdl_trigger();
+  pdl_wait();  // the transforms' outputs
+  const size_t ln = (size_t)a.L * n, pairs = batch * ln / 2;
+  for (size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x; p < pairs; p += (size_t)gridDim.x * blockDim.x) {
+    const size_t w = 2 * p, b = w / ln, r = w % ln;
+    const int limb = (int)(r / n);
+    const uint64_t q = __ldg(&a.limbs[limb].q);
+    uint64_t *c0 = a.ct + b * 2 * ln + r, *c1 = c0 + ln;
+    const ulonglong2 u = ld2_nc(a.u_hat + w), p1 = ld2_nc(a.pk + r), p2 = ld2_nc(a.pk + ln + r);
+    const ulonglong2 s1 = ld2_nc(a.pk_sh + r), s2 = ld2_nc(a.pk_sh + ln + r);
+    uint64_t a0, a1, b0, b1;
+    ld2(c0, a0, a1);
+    ld2(c1, b0, b1);
+    st2_cs(c0, add_shoup(a0, u.x, p1.x, s1.x, q), add_shoup(a1, u.y, p1.y, s1.y, q));
+    st2_cs(c1, add_shoup(b0, u.x, p2.x, s2.x, q), add_shoup(b1, u.y, p2.y, s2.y, q));
+  }
+}
+cudaError_t launch_vanilla_combine(const VanillaArgs &a, size_t batch, int n, cudaStream_t s) {
+  const size_t pairs = batch * (size_t)a.L * n / 2;
+  return launch_ex(vanilla_combine_kernel, dim3((unsigned)std::min<size_t>((pairs + 255) / 256, 148 * 8)), 256, 0, 1, s,
+                   a, batch, n);
 }
 
 // ============================================================ samplers (debug)

@@ -50,6 +50,7 @@ struct VanillaArgs {
   const uint64_t *pk_sh;  // [2][L][N] Shoup companions floor(pk 2^64 / q_i) (shoup_prep_kernel)
   const int64_t *m;       // [batch][N] or null
   uint64_t *ct;
+  uint64_t *u_hat;        // small batches, NTT form: the u transform's output [batch][L][N] (else null)
   uint64_t seed, msg_base;
   int L, limbs_per_cta;
 };
@@ -61,6 +62,7 @@ struct ZincNttArgs {
   uint64_t *ct;
   uint64_t seed, msg_base;
   int L, limbs_per_cta;
+  int t_split;            // small batches: the two transforms on separate CTAs (gridDim.z = 2)
 };
 struct KeygenArgs {
   const LimbConst *limbs;
@@ -112,6 +114,7 @@ struct EncodeArgs {
   const double2 *post_tw;   // real-slot split step: [A | B | A5 | B5] (encode_real_post)
   const double2 *twist_split;  // complex-slot twist zeta^-j = A'[j >> 6] B[j & 63], j < M: [A' | B]
   int wide;                 // m_out holds 128-bit coefficients (int64 pairs)
+  int fast;                 // real slots, batch below the SM count: the latency variant (more threads)
   double scale;
   int64_t *m_out;
 };
@@ -177,6 +180,8 @@ cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
 cudaError_t launch_ct_add(const CtAddArgs &a, cudaStream_t s);
 cudaError_t launch_ct_sum(const CtSumArgs &a, cudaStream_t s);
 // w' = floor(w 2^64 / q_i) for the `words` words of keys [rows][L][N] (pk, sk)
+// ct0 += pk1 u^, ct1 += pk2 u^ after a transform-split vanilla NTT-form launch (a.u_hat)
+cudaError_t launch_vanilla_combine(const VanillaArgs &a, size_t batch, int n, cudaStream_t s);
 cudaError_t launch_shoup_prep(const LimbConst *limbs, const uint64_t *w, uint64_t *wp, size_t words, int log_n, int L,
                               cudaStream_t s);
 cudaError_t launch_int_peak(const IntPeakArgs &a, int variant, int blocks, cudaStream_t s);
