@@ -273,9 +273,13 @@ void zinc_launch_count_reset(void);
  *                                 (S = N / 2^12 CTA clusters of 2^12 words per CTA for Zinc NTT form,
  *                                 vanilla COEFF form and decryption; 2-CTA kernels for vanilla NTT
  *                                 form); 2: S-CTA clusters everywhere; 0: 2-CTA kernels everywhere
+ *  ZINC_TUNE_SMALL_ENCODE         real-slot encode of fewer messages than SMs: 0 (default) the throughput
+ *                                 kernel (256 threads, radix-16: 15 us per message at N = 2^14, measured
+ *                                 fastest), 1 512 threads radix-8 (18 us), 2 1024 threads radix-4 (21 us)
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_PDL = 2,
-       ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_SPLIT = 5, ZINC_TUNE_COUNT = 6 };
+       ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_SPLIT = 5, ZINC_TUNE_SMALL_ENCODE = 6,
+       ZINC_TUNE_COUNT = 7 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

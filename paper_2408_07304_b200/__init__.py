@@ -356,7 +356,7 @@ def profile_read() -> dict:
 
 
 TUNE_COEFF_MSGS_PER_CTA, TUNE_ENCODE_CHUNK_BYTES, TUNE_PDL, TUNE_L2_PREFETCH, TUNE_NTT_CHUNK_MSGS = 0, 1, 2, 3, 4
-TUNE_SPLIT = 5
+TUNE_SPLIT, TUNE_SMALL_ENCODE = 5, 6
 
 
 def tune(knob: int, value: int) -> int:

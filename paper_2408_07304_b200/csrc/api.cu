@@ -110,7 +110,7 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {1}, {1}, {0}, {1}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -525,7 +525,8 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
                                cudaStream_t s, bool wide = false) {
   EncodeArgs a = encode_args(c, kind, slots, m);
   a.wide = wide ? 1 : 0;
-  a.fast = batch < (size_t)c->num_sms ? 1 : 0;  // few messages: latency, not throughput
+  // few messages: a latency variant with more threads per message (knob ZINC_TUNE_SMALL_ENCODE)
+  a.fast = batch < (size_t)c->num_sms ? (int)g_tune[ZINC_TUNE_SMALL_ENCODE].load() : 0;
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
@@ -611,17 +612,11 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
       LAUNCH(ZINC_K_ZINC_NTT, s, launch_zinc_ntt(c->log_n, a, kernel_mode(c), batch, groups, s));
     return ZINC_OK;
   }
-  // Shoup companions of pk: the pointwise products pk u^ become Shoup products
-  ScratchBuf pk_sh(s);
-  const size_t key_words = (size_t)2 * c->L * c->n;
-  CUDA_TRY(pk_sh.alloc(key_words * 8));
-  LAUNCH(ZINC_K_SHOUP_PREP, s, launch_shoup_prep(c->d_limbs, key, pk_sh.as<uint64_t>(), key_words, c->log_n, c->L, s));
   VanillaArgs a{};
   a.limbs = c->d_limbs;
   a.tw = c->d_tw;
   a.itw = c->d_itw;
   a.pk = key;
-  a.pk_sh = pk_sh.as<uint64_t>();
   a.m = m;
   a.ct = ct;
   a.seed = seed;
@@ -631,10 +626,17 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   // a handful of messages (NTT form): the three transforms on separate CTAs, then a combine
   const bool t_split = c->log_n >= 14 && g_tune[ZINC_TUNE_SPLIT].load() != 0 && form == ZINC_FORM_NTT &&
                        batch * (size_t)groups * 3 * ((size_t)c->n >> 12) <= 2 * (size_t)c->num_sms;
-  ScratchBuf uhat(s);
+  ScratchBuf uhat(s), pk_sh(s);
   if (t_split) {
     CUDA_TRY(uhat.alloc(batch * (size_t)c->L * c->n * 8));
     a.u_hat = uhat.as<uint64_t>();
+  } else {
+    // Shoup companions of pk: the per-message pointwise products pk u^ become Shoup products
+    // (the transform-split launch's combine kernel uses Barrett products instead)
+    const size_t key_words = (size_t)2 * c->L * c->n;
+    CUDA_TRY(pk_sh.alloc(key_words * 8));
+    LAUNCH(ZINC_K_SHOUP_PREP, s, launch_shoup_prep(c->d_limbs, key, pk_sh.as<uint64_t>(), key_words, c->log_n, c->L, s));
+    a.pk_sh = pk_sh.as<uint64_t>();
   }
   if (t_split || use_split(c, form == ZINC_FORM_NTT ? SPLIT_VANILLA_NTT : SPLIT_VANILLA_COEFF))
     LAUNCH(ZINC_K_VANILLA, s, launch_vanilla_split(c->log_n, a, form, kernel_mode(c), batch, groups, s));

@@ -93,15 +93,16 @@ __global__ void __launch_bounds__(256, (LOGM <= 13 ? 2 : 1)) encode_real_kernel(
   extern __shared__ __align__(16) double2 buf[];
   encode_real_body<LOGM, WIDE>(a, blockIdx.x, buf);
 }
-// Latency variant for small batches (fewer messages than SMs): the same encode with up to
-// 1024 threads on one message (radix-4 passes; 512 threads with radix-8 at N = 2^13).
-template <int LOGM> struct FastEnc {
-  static constexpr int THREADS = LOGM >= 13 ? 1024 : 512, NPASS = LOGM >= 13 ? 6 : 4;
+// Latency variants for small batches (fewer messages than SMs): the same encode with more
+// threads on one message: F = 1: 512 threads, radix-8 passes; F = 2: 1024 threads, radix-4
+// passes (N >= 2^14).
+template <int LOGM, int F> struct FastEnc {
+  static constexpr int THREADS = (F == 2 && LOGM >= 13) ? 1024 : 512, NPASS = THREADS == 1024 ? 6 : 4;
 };
-template <int LOGM, bool WIDE>
-__global__ void __launch_bounds__(FastEnc<LOGM>::THREADS, 1) encode_real_fast_kernel(EncodeArgs a) {
+template <int LOGM, bool WIDE, int F>
+__global__ void __launch_bounds__(FastEnc<LOGM, F>::THREADS, 1) encode_real_fast_kernel(EncodeArgs a) {
   extern __shared__ __align__(16) double2 buf[];
-  encode_real_body<LOGM, WIDE, FastEnc<LOGM>::THREADS, FastEnc<LOGM>::NPASS>(a, blockIdx.x, buf);
+  encode_real_body<LOGM, WIDE, FastEnc<LOGM, F>::THREADS, FastEnc<LOGM, F>::NPASS>(a, blockIdx.x, buf);
 }
 
 // ============================================================ decode (C-10)
@@ -159,10 +160,15 @@ template <int LOGM>
 static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
   if (!a.complex_slots) {
     if constexpr (LOGM >= 12) {
-      if (a.fast) {
-        constexpr int T = FastEnc<LOGM>::THREADS;
-        if (a.wide) return launch_ex(encode_real_fast_kernel<LOGM, true>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
-        return launch_ex(encode_real_fast_kernel<LOGM, false>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
+      if (a.fast == 1) {
+        constexpr int T = FastEnc<LOGM, 1>::THREADS;
+        if (a.wide) return launch_ex(encode_real_fast_kernel<LOGM, true, 1>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
+        return launch_ex(encode_real_fast_kernel<LOGM, false, 1>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
+      }
+      if (a.fast == 2) {
+        constexpr int T = FastEnc<LOGM, 2>::THREADS;
+        if (a.wide) return launch_ex(encode_real_fast_kernel<LOGM, true, 2>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
+        return launch_ex(encode_real_fast_kernel<LOGM, false, 2>, dim3((unsigned)batch), T, encode_real_smem<LOGM>(), 1, s, a);
       }
     }
     if (a.wide) return launch_ex(encode_real_kernel<LOGM, true>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);

@@ -143,13 +143,14 @@ __global__ void __launch_bounds__(256) vanilla_combine_kernel(VanillaArgs a, siz
     const int limb = (int)(r / n);
     const uint64_t q = __ldg(&a.limbs[limb].q);
     uint64_t *c0 = a.ct + b * 2 * ln + r, *c1 = c0 + ln;
+    const LimbConst &c = a.limbs[limb];
     const ulonglong2 u = ld2_nc(a.u_hat + w), p1 = ld2_nc(a.pk + r), p2 = ld2_nc(a.pk + ln + r);
-    const ulonglong2 s1 = ld2_nc(a.pk_sh + r), s2 = ld2_nc(a.pk_sh + ln + r);
     uint64_t a0, a1, b0, b1;
     ld2(c0, a0, a1);
     ld2(c1, b0, b1);
-    st2_cs(c0, add_shoup(a0, u.x, p1.x, s1.x, q), add_shoup(a1, u.y, p1.y, s1.y, q));
-    st2_cs(c1, add_shoup(b0, u.x, p2.x, s2.x, q), add_shoup(b1, u.y, p2.y, s2.y, q));
+    // u^ is canonical; Barrett products (no Shoup companions on this small-batch path)
+    st2_cs(c0, add_mod(a0, mul_mod(p1.x, u.x, c), q), add_mod(a1, mul_mod(p1.y, u.y, c), q));
+    st2_cs(c1, add_mod(b0, mul_mod(p2.x, u.x, c), q), add_mod(b1, mul_mod(p2.y, u.y, c), q));
   }
 }
 cudaError_t launch_vanilla_combine(const VanillaArgs &a, size_t batch, int n, cudaStream_t s) {

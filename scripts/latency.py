@@ -18,6 +18,8 @@ ctx = Z.Context(cfg.log_n, cfg.bits, cfg.log_scale)
 sk, _, pk = Z.zinc_keygen(ctx, cfg.key_seed)
 cache = {f: Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, f) for f in (Z.COEFF, Z.NTT)}
 out = {}
+if os.environ.get("ZINC_SMALL_ENCODE") is not None:
+    Z.tune(Z.TUNE_SMALL_ENCODE, int(os.environ["ZINC_SMALL_ENCODE"]))
 for B in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,16").split(",")]:
     z = torch.from_numpy(np.ascontiguousarray(slots_batch(cfg, 0, B))).cuda()
     ct = ctx.empty_ct(B)

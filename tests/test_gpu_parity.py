@@ -176,6 +176,30 @@ def test_both_transform_kernel_families_bit_exact(Z, orc, name, split):
             assert ost == 0 and np.array_equal(c[b], x)
 
 
+@pytest.mark.parametrize("name", ["C3", "C4", "C2"])
+@pytest.mark.parametrize("B", [1, 2, 5])
+def test_small_batch_latency_paths_bit_exact(Z, orc, name, B):
+    """Latency paths for a handful of messages (C5 batches 1 and 16): the 1024-thread encode,
+    the finer Zinc COEFF tiles, and the transform-split Zinc NTT / vanilla NTT launches with
+    the combine kernel -- bit-exact against the oracle on the GPU-encoded plaintexts."""
+    s = setup_for(Z, orc, name)
+    cfg = s.cfg
+    z = slots_batch(cfg, 3, B)
+    zz = np.stack([z.real, z.imag], axis=-1) if cfg.complex_slots else z
+    zd = torch.from_numpy(np.ascontiguousarray(zz)).cuda()
+    m = np64(Z.ckks_encode_batch(s.ctx, zd))
+    seed, base = 99, 4242
+    for path, form in (("zinc", COEFF), ("zinc", NTT), ("vanilla", NTT), ("vanilla", COEFF)):
+        if path == "zinc":
+            ct = Z.zinc_encrypt_batch(s.ctx, s.cache[form], form, zd, seed, base)
+        else:
+            ct = Z.ckks_encrypt_batch(s.ctx, s.pk, form, zd, seed, base)
+        _check_msgs(orc, s, path, form, m, np64(ct), seed, base, sorted({0, B - 1}))
+        _, st, zdec = Z.ckks_decrypt_batch(s.ctx, s.sk, form, ct)
+        assert (np64(st) == 0).all()
+        assert np.max(np.abs(zdec.cpu().numpy() - z)) < cfg.tolerance()
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_encode_within_one(Z, orc, name):
     s = setup_for(Z, orc, name)
