@@ -350,6 +350,7 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     lc.ninv_w = mulm(lc.ninv, itw[(size_t)i * n + 1].x, q);
     lc.ninv_w_sh = shoup(lc.ninv_w, q);
     lc.r64 = (uint64_t)(((u128)1 << 64) % q);
+    lc.r64_sh = shoup(lc.r64, q);
     // reduce_fold: q = 2^b - c; one fold maps x < 2^64 below 2^b + (2^(64-b) - 1) c + (2^b - 1)
     {
       const uint64_t fc = (1ull << lc.b) - q;

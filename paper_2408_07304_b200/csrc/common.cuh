@@ -40,6 +40,7 @@ struct LimbConst {
   uint32_t fold_c;
   uint32_t fold_n;     // folds that bring any 64-bit value below 2q (1 or 2); 0: use reduce64
   uint64_t qinv_hi, qinv_lo;  // floor(2^128 / q): Shoup companions on the device (shoup_prep_kernel)
+  uint64_t r64_sh;   // Shoup companion of r64 = 2^64 mod q
 };
 enum : uint32_t { SCHEME_CKKS = 0, SCHEME_BFV = 1, SCHEME_BGV = 2 };
 

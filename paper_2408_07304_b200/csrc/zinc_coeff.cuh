@@ -95,7 +95,11 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   }
   const uint64_t qmin = a.qmin;
   if (a.m128) {
-    // 128-bit plaintexts (f3, the paper's Delta = 2^55): the residue of hi 2^64 + lo + e1' per limb
+    // 128-bit plaintexts (f3, the paper's Delta = 2^55): per limb, [z + hi 2^64 + lo + e1']_q
+    // with hi 2^64 = hi r64 (a Shoup product by the constant r64 = 2^64 mod q) and lo folded
+    // (reduce_fold without its final subtraction); one fold of the sum finishes.  |hi| < qmin
+    // (every 128-bit plaintext the encoder produces at these scales) takes a branch-free
+    // residue; the general case reduces hi with reduce_i64q.
     pdl_wait();
     for (size_t b = b_begin; b < b_end; ++b) {
       const uint64_t msg = a.msg_base + b;
@@ -104,17 +108,33 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
       const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
       const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
       const int e0 = cbd_lo(w1), e1 = cbd_hi(w1), f0 = cbd_lo(w2), f1 = cbd_hi(w2);
+      const int64_t h0 = (int64_t)p0.y, h1 = (int64_t)p1.y;
+      const bool hsmall = (uint64_t)(h0 < 0 ? -h0 : h0) < qmin && (uint64_t)(h1 < 0 ? -h1 : h1) < qmin;
       uint64_t *out = a.ct + b * 2 * lnn + j;
-#pragma unroll 1
-      for (int i = 0; i < L; ++i) {
+      auto limb = [&](int i) {
         const LimbConst &c = a.limbs[i];
         const uint64_t q = sq[i];
         uint64_t z10, z11, z20, z21;
         ld2(tile + (size_t)i * T + jl, z10, z11);
         ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-        const uint64_t r0 = reduce_i128((int64_t)p0.y, p0.x, c), r1 = reduce_i128((int64_t)p1.y, p1.x, c);
-        st2_cs(out + (size_t)i * a.n, mod_add_signed(add_mod(z10, r0, q), e0, q), mod_add_signed(add_mod(z11, r1, q), e1, q));
+        const uint64_t r0 = hsmall ? reduce_small(h0, q) : reduce_i64q(h0, q, c.mu64);
+        const uint64_t r1 = hsmall ? reduce_small(h1, q) : reduce_i64q(h1, q, c.mu64);
+        // each term below 2q (lo folded once: < 2^b + 2^(64-b) c < 2q when fold_n == 1)
+        const uint64_t l0 = c.fold_n == 1 ? (p0.x & c.fold_mask) + (uint64_t)(uint32_t)(p0.x >> c.b) * c.fold_c
+                                          : reduce_fold(p0.x, c);
+        const uint64_t l1 = c.fold_n == 1 ? (p1.x & c.fold_mask) + (uint64_t)(uint32_t)(p1.x >> c.b) * c.fold_c
+                                          : reduce_fold(p1.x, c);
+        const uint64_t s0 = mul_shoup_lazy(r0, c.r64, c.r64_sh, q) + l0 + z10 + reduce_small(e0, q);
+        const uint64_t s1 = mul_shoup_lazy(r1, c.r64, c.r64_sh, q) + l1 + z11 + reduce_small(e1, q);
+        st2_cs(out + (size_t)i * a.n, reduce_fold(s0, c), reduce_fold(s1, c));
         st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+      };
+      if constexpr (LC > 0) {
+#pragma unroll
+        for (int i = 0; i < LC; ++i) limb(i);
+      } else {
+#pragma unroll 1
+        for (int i = 0; i < L; ++i) limb(i);
       }
     }
     return;
