@@ -401,8 +401,15 @@ def paper_params(Z, torch, reps=2, cap=4096):
         _, st, zz = Z.ckks_decrypt_batch(ctx, sk, Z.COEFF, ct[:8])
         err = float(np.max(np.abs(zz.cpu().numpy() - slots_batch(cfg, 0, 8))))
         vn = _timed(torch, lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, zd, cfg.enc_seed, 0, out=ct), reps)
-        rz, rv = B / (zc / 1e3), B / (vn / 1e3)
+        m128 = Z.ckks_encode_batch_wide(ctx, zd)  # the same plaintexts as 128-bit coefficients
+        zi = _timed(torch, lambda: Z.zinc_encrypt_batch(ctx, cache, Z.COEFF, m128, cfg.enc_seed, 0, out=ct), reps)
+        del m128
+        rz, rv, ri = B / (zc / 1e3), B / (vn / 1e3), B / (zi / 1e3)
+        peak = load_peaks()[0]
+        ctb = 2 * cfg.L * cfg.n * 8
         out[name] = {"count": cfg.batch, "timed_batch": B, "zinc_coeff_ct_per_s": rz, "vanilla_ntt_ct_per_s": rv,
+                     "zinc_coeff_hbm_frac": rz * (ctb + cfg.n // 2 * 8) / 1e9 / peak,
+                     "zinc_coeff_i128_ct_per_s": ri, "zinc_coeff_i128_hbm_frac": ri * (ctb + cfg.n * 16) / 1e9 / peak,
                      "zinc_job_s": cfg.batch / rz, "vanilla_job_s": cfg.batch / rv,
                      "paper_seal_cpu_s": {"ckks": paper_s[name][0], "zinc": paper_s[name][1]},
                      "decrypt_ok": int(st.sum().item()) == 0 and err < 1e-4, "max_abs_err_8": err}

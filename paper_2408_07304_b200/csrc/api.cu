@@ -658,18 +658,31 @@ static zinc_status encrypt_wide(const zinc_ctx *c, int path, const uint64_t *key
   const bool direct = path == PATH_ZINC && form == ZINC_FORM_COEFF;  // kernel reads 128-bit m itself
   const size_t n = c->n, L = c->L;
   const size_t per_msg = (slots ? n * 16 : 0) + (direct ? 0 : L * n * 8);
-  const size_t chunk = per_msg ? std::max<size_t>(1, std::min(batch, (size_t)(256ull << 20) / per_msg)) : batch;
+  // direct (Zinc COEFF from slots): double-buffered chunks of 4x the 64-bit chain's bytes (the
+  // wide encode needs a few hundred messages per launch to fill the GPU) chained with
+  // programmatic dependent launches, as encrypt_any's chain; otherwise 256 MiB chunks
+  const bool chain = direct && slots && g_tune[ZINC_TUNE_PDL].load() != 0;
+  const size_t budget = chain ? (size_t)std::max<long long>(per_msg, 4 * g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load())
+                              : (size_t)(256ull << 20);
+  const size_t chunk = per_msg ? std::max<size_t>(1, std::min(batch, budget / per_msg)) : batch;
+  const int nb = chain && batch > chunk ? 2 : 1;
   ScratchBuf m128b(s), resb(s);
-  if (slots) CUDA_TRY(m128b.alloc(chunk * n * 16));
+  if (slots) CUDA_TRY(m128b.alloc(nb * chunk * n * 16));
   if (!direct) CUDA_TRY(resb.alloc(chunk * L * n * 8));
   int64_t *m128 = m128b.as<int64_t>();
   uint64_t *res = resb.as<uint64_t>();
   const size_t in_stride = pt_stride_bytes(c, kind), ct_stride = 2 * L * n;
   zinc_status st = ZINC_OK;
-  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk) {
+  size_t k = 0;
+  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
     const size_t cnt = std::min(chunk, batch - off);
-    const int64_t *mw = slots ? m128 : (const int64_t *)((const char *)pt + off * in_stride);
-    if (slots && (st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, m128, s, true))) break;
+    int64_t *mk = m128 + (k % nb) * chunk * n * 2;
+    const int64_t *mw = slots ? mk : (const int64_t *)((const char *)pt + off * in_stride);
+    {
+      PdlScope pdl_scope(chain && k > 0);
+      if (slots && (st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mk, s, true))) break;
+    }
+    PdlScope pdl_scope(chain);
     if (direct) {  // the add/inject kernel reads 128-bit plaintexts itself
       ZincCoeffArgs za = zinc_coeff_args(c, key, nullptr, cnt, seed, msg_base + off, ct + off * ct_stride);
       za.m128 = mw;

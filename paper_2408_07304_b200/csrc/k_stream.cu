@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256) int_peak_kernel(IntPeakArgs a) {
   if (acc == 0x1234567890ABCDEFull) a.sink[0] = acc;
 }
 
-size_t zinc_coeff_smem(int L, int threads) { return ((size_t)2 * L * 2 * threads + 4 * L) * sizeof(uint64_t); }
+size_t zinc_coeff_smem(int L, int threads) { return ((size_t)2 * L * 2 * threads + 8 * L) * sizeof(uint64_t); }
 
 cudaError_t launch_zinc_coeff(const ZincCoeffArgs &a, int threads, int grid_y, size_t smem_pad, cudaStream_t s) {
   dim3 grid(a.n / (2 * threads), grid_y);

@@ -37,7 +37,12 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   const int L = LC > 0 ? LC : a.L;
   const int j0 = tile_x * T;
   uint64_t *sq = tile + (size_t)2 * L * T, *smu = sq + L, *sdel = smu + L, *sdelsh = sdel + L;
+  uint64_t *sr64 = sdelsh + L, *sr64sh = sr64 + L, *sfmask = sr64sh + L, *sfcb = sfmask + L;  // wide path
   for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    sr64[i] = a.limbs[i].r64;
+    sr64sh[i] = a.limbs[i].r64_sh;
+    sfmask[i] = a.limbs[i].fold_mask;
+    sfcb[i] = (uint64_t)a.limbs[i].fold_c | ((uint64_t)a.limbs[i].b << 32) | ((uint64_t)a.limbs[i].fold_n << 40);
     sq[i] = a.limbs[i].q;
     smu[i] = a.limbs[i].mu64;
     sdel[i] = a.limbs[i].delta;
@@ -95,12 +100,13 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   }
   const uint64_t qmin = a.qmin;
   if (a.m128) {
-    // 128-bit plaintexts (f3, the paper's Delta = 2^55): per limb, [z + hi 2^64 + lo + e1']_q
-    // with hi 2^64 = hi r64 (a Shoup product by the constant r64 = 2^64 mod q) and lo folded
-    // (reduce_fold without its final subtraction); one fold of the sum finishes.  |hi| < qmin
-    // (every 128-bit plaintext the encoder produces at these scales) takes a branch-free
-    // residue; the general case reduces hi with reduce_i64q.
+    // 128-bit plaintexts (f3, the paper's Delta = 2^55): per limb, [z + hi 2^64 + lo + e1']_q.
+    // Fast path (the whole warp has |hi| < qmin and every limb folds once): hi 2^64 = hi r64 as
+    // a Shoup product by the constant r64 = 2^64 mod q, lo folded once (below 2q), one fold of
+    // the sum finishes -- per-limb constants from shared memory.  Otherwise reduce_i128.
     pdl_wait();
+    bool fold1 = true;
+    for (int i = 0; i < L; ++i) fold1 &= ((sfcb[i] >> 40) & 0xff) == 1;
     for (size_t b = b_begin; b < b_end; ++b) {
       const uint64_t msg = a.msg_base + b;
       const int64_t *mp = a.m128 + (b * a.n + j) * 2;
@@ -111,30 +117,34 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
       const int64_t h0 = (int64_t)p0.y, h1 = (int64_t)p1.y;
       const bool hsmall = (uint64_t)(h0 < 0 ? -h0 : h0) < qmin && (uint64_t)(h1 < 0 ? -h1 : h1) < qmin;
       uint64_t *out = a.ct + b * 2 * lnn + j;
-      auto limb = [&](int i) {
-        const LimbConst &c = a.limbs[i];
-        const uint64_t q = sq[i];
-        uint64_t z10, z11, z20, z21;
-        ld2(tile + (size_t)i * T + jl, z10, z11);
-        ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-        const uint64_t r0 = hsmall ? reduce_small(h0, q) : reduce_i64q(h0, q, c.mu64);
-        const uint64_t r1 = hsmall ? reduce_small(h1, q) : reduce_i64q(h1, q, c.mu64);
-        // each term below 2q (lo folded once: < 2^b + 2^(64-b) c < 2q when fold_n == 1)
-        const uint64_t l0 = c.fold_n == 1 ? (p0.x & c.fold_mask) + (uint64_t)(uint32_t)(p0.x >> c.b) * c.fold_c
-                                          : reduce_fold(p0.x, c);
-        const uint64_t l1 = c.fold_n == 1 ? (p1.x & c.fold_mask) + (uint64_t)(uint32_t)(p1.x >> c.b) * c.fold_c
-                                          : reduce_fold(p1.x, c);
-        const uint64_t s0 = mul_shoup_lazy(r0, c.r64, c.r64_sh, q) + l0 + z10 + reduce_small(e0, q);
-        const uint64_t s1 = mul_shoup_lazy(r1, c.r64, c.r64_sh, q) + l1 + z11 + reduce_small(e1, q);
-        st2_cs(out + (size_t)i * a.n, reduce_fold(s0, c), reduce_fold(s1, c));
-        st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
-      };
-      if constexpr (LC > 0) {
-#pragma unroll
-        for (int i = 0; i < LC; ++i) limb(i);
+      if (fold1 && __all_sync(0xffffffffu, hsmall)) {
+#pragma unroll 2
+        for (int i = 0; i < L; ++i) {
+          const uint64_t q = sq[i], r64 = sr64[i], r64s = sr64sh[i], fm = sfmask[i], fcb = sfcb[i];
+          const uint32_t fc = (uint32_t)fcb, fb = (uint32_t)(fcb >> 32) & 0xff;
+          uint64_t z10, z11, z20, z21;
+          ld2(tile + (size_t)i * T + jl, z10, z11);
+          ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+          auto fold = [&](uint64_t x) { return (x & fm) + (uint64_t)(uint32_t)(x >> fb) * fc; };
+          // each term below 2q, the sum below 6q < 2^64
+          const uint64_t s0 = mul_shoup_lazy(reduce_small(h0, q), r64, r64s, q) + fold(p0.x) + z10 + reduce_small(e0, q);
+          const uint64_t s1 = mul_shoup_lazy(reduce_small(h1, q), r64, r64s, q) + fold(p1.x) + z11 + reduce_small(e1, q);
+          st2_cs(out + (size_t)i * a.n, csub(fold(s0), q), csub(fold(s1), q));
+          st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+        }
       } else {
 #pragma unroll 1
-        for (int i = 0; i < L; ++i) limb(i);
+        for (int i = 0; i < L; ++i) {
+          const LimbConst &c = a.limbs[i];
+          const uint64_t q = sq[i];
+          uint64_t z10, z11, z20, z21;
+          ld2(tile + (size_t)i * T + jl, z10, z11);
+          ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+          const uint64_t r0 = reduce_i128(h0, p0.x, c), r1 = reduce_i128(h1, p1.x, c);
+          st2_cs(out + (size_t)i * a.n, mod_add_signed(add_mod(z10, r0, q), e0, q),
+                 mod_add_signed(add_mod(z11, r1, q), e1, q));
+          st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+        }
       }
     }
     return;
