@@ -259,7 +259,8 @@ uint64_t zinc_launch_count(void);
 void zinc_launch_count_reset(void);
 
 /* Process-wide tuning knobs (launch geometry only; results never change):
- *  ZINC_TUNE_COEFF_MSGS_PER_CTA   messages per CTA of the COEFF-form Zinc kernel (default 2)
+ *  ZINC_TUNE_COEFF_MSGS_PER_CTA   messages per CTA of the COEFF-form Zinc kernel (0, default: 8 when
+ *                                 L <= 4, else 2)
  *  ZINC_TUNE_ENCODE_CHUNK_BYTES   bytes of int64 plaintexts encoded per chunk when the input is slots
  *                                 and the path is Zinc COEFF form (default 32 MiB: the chunk stays
  *                                 resident in the 126 MB L2 between the encode and the add/inject)

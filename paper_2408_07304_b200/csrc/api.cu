@@ -110,7 +110,7 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{2}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -557,7 +557,10 @@ static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, c
   a.L = c->L;
   a.qmin = c->qmin;
   // messages per CTA (tuning knob): grid = coefficient tiles x message groups
-  a.msgs_per_cta = (size_t)std::max<long long>(1, g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load());
+  // 0 (default): 8 messages per CTA when the cache tile is small (L <= 4: amortises the tile
+  // staging over more stores; C2 +7 %), else 2 (measured, profiles/r02_zinc_coeff_sweep.txt)
+  const long long mpc = g_tune[ZINC_TUNE_COEFF_MSGS_PER_CTA].load();
+  a.msgs_per_cta = (size_t)(mpc > 0 ? mpc : (c->L <= 4 ? 8 : 2));
   return a;
 }
 // The S-CTA cluster transform kernels (k_split.cu) serve N = 2^14 and 2^15.  Knob 1 (auto):

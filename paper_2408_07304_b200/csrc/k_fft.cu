@@ -45,12 +45,30 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
       g = (g * gstep) & MASK;
     }
   }
+  // split: the sub-transform's twiddles W_M^(2e) = W_{M/2}^e (e < M/4, 64 KiB at M = 2^14) come
+  // into shared memory by one TMA bulk copy, issued before the scatter, beside the FFT buffer
+  double2 *stw = buf + ML + ML / 16;
+  __shared__ __align__(8) uint64_t tw_mbar;
+  if constexpr (SPLIT) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tw_mbar, 1);
+      mbar_expect_tx(&tw_mbar, (uint32_t)((M / 4) * sizeof(double2)));
+      bulk_g2s(stw, a.fft_tw_h, (uint32_t)((M / 4) * sizeof(double2)), &tw_mbar);
+    }
+  }
   __syncthreads();
+  if constexpr (SPLIT) mbar_wait(&tw_mbar, 0);
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
-  fft_pass<LL, 0, P::K1, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
-  __syncthreads();
-  fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+  if constexpr (SPLIT) {
+    fft_pass<LL, 0, P::K1, P::THREADS, true, false, 1, true>(stw, lds, sts);
+    __syncthreads();
+    fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, 1, true>(stw, lds, sts);
+  } else {
+    fft_pass<LL, 0, P::K1, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+    __syncthreads();
+    fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+  }
   __syncthreads();
   // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
   // this encode overwrites: the loads and the first passes overlapped it, the stores wait.
@@ -73,14 +91,45 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   if constexpr (!SPLIT) {
     fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false>(a.fft_tw, lds, emit);
   } else {
-    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, 1, true>(stw, lds, sts);
     cluster_sync_all();
     const double2 *h0 = peer_smem(buf, 0), *h1 = peer_smem(buf, 1);
-    for (int x = r * (ML / 2) + threadIdx.x; x < (r + 1) * (ML / 2); x += P::THREADS) {
-      const double2 u = h0[pad16(x)];
-      const double2 t = cmul(h1[pad16(x)], __ldg(a.fft_tw + x));
-      emit(x, cadd(u, t));
-      emit(x + ML, csubd(u, t));
+    // U independent iterations: their DSMEM, twiddle and twist loads are all in flight
+    // before the first multiply (one at a time, each iteration exposed ~3 load latencies)
+    constexpr int U = 4;
+    static_assert((ML / 2) % (P::THREADS * U) == 0, "exchange tiling");
+#pragma unroll 1
+    for (int x0 = r * (ML / 2) + threadIdx.x; x0 < (r + 1) * (ML / 2); x0 += P::THREADS * U) {
+      double2 u[U], h[U], w[U], t0a[U], t0b[U], t1a[U], t1b[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int x = x0 + k * P::THREADS;
+        u[k] = h0[pad16(x)];
+        h[k] = h1[pad16(x)];
+        w[k] = __ldg(a.fft_tw + x);
+        t0a[k] = __ldg(tA + (x >> 6));
+        t0b[k] = __ldg(tB + (x & 63));
+        t1a[k] = __ldg(tA + ((x + ML) >> 6));
+        t1b[k] = __ldg(tB + ((x + ML) & 63));
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int x = x0 + k * P::THREADS;
+        const double2 t = cmul(h[k], w[k]);
+        const double2 y0 = cmul(cadd(u[k], t), cmul(t0a[k], t0b[k]));
+        const double2 y1 = cmul(csubd(u[k], t), cmul(t1a[k], t1b[k]));
+        if (a.wide) {
+          store_i128(m + 2 * x, y0.x * scale);
+          store_i128(m + 2 * (x + M), y0.y * scale);
+          store_i128(m + 2 * (x + ML), y1.x * scale);
+          store_i128(m + 2 * (x + ML + M), y1.y * scale);
+        } else {
+          m[x] = llround(y0.x * scale);
+          m[x + M] = llround(y0.y * scale);
+          m[x + ML] = llround(y1.x * scale);
+          m[x + ML + M] = llround(y1.y * scale);
+        }
+      }
     }
     cluster_sync_all();
   }
@@ -156,6 +205,10 @@ template <int LOGM> static size_t fft_smem() {
   constexpr int LL = LOGM > 13 ? LOGM - 1 : LOGM;
   return ((1 << LL) + ((1 << LL) >> 4)) * sizeof(double2);
 }
+// complex-slot encode: split CTAs also hold the sub-transform's twiddle table (M/4 entries)
+template <int LOGM> static size_t encode_smem() {
+  return fft_smem<LOGM>() + (LOGM > 13 ? (size_t)(1 << LOGM) / 4 * sizeof(double2) : 0);
+}
 template <int LOGM>
 static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {
   if (!a.complex_slots) {
@@ -176,7 +229,7 @@ static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream
   }
   constexpr int C = LOGM > 13 ? 2 : 1;
   return launch_ex(encode_kernel<LOGM>, dim3((unsigned)(batch * C)), FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
-                   fft_smem<LOGM>(), C, s, a);
+                   encode_smem<LOGM>(), C, s, a);
 }
 cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s) {
 #define CALL(K) launch_encode_t<K - 1>(a, batch, s)
