@@ -7,7 +7,7 @@
 #   bash scripts/gpu_round.sh <tag> [kernel ...]
 # env: SKIP_TESTS=1, SKIP_NCU=1, SKIP_LAUNCHES=1, BENCH_ARGS="...", NCU_ARGS="..."
 TAG=${1:-r01}; shift
-KERNELS=${@:-zinc_coeff_kernel encode_real_kernel vanilla_kernel zinc_ntt_kernel}
+KERNELS=${@:-zinc_coeff_kernel encode_real_kernel zinc_ntt_split vanilla_ntt_dit vanilla_coeff_split decrypt_split encode_kernel}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
@@ -17,7 +17,7 @@ if [ -z "$SKIP_TESTS" ]; then
 fi
 timeout 900 python bench.py $BENCH_ARGS > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err
 if [ -z "$SKIP_NCU" ]; then
-  SMALL="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-c5 $BENCH_ARGS"
+  SMALL="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-c5 --no-oracle-suite $BENCH_ARGS"
   timeout 600 $SMALL > $OUT/plain.log 2>&1; RC=$?; echo "plain exit $RC" >> $OUT/plain.log
   if [ $RC -eq 0 ]; then
     if [ -z "$SKIP_LAUNCHES" ]; then
