@@ -364,6 +364,8 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
         if (b1 < two_q) lc.fold_n = 1;
         else if ((b1 >> lc.b) < (1ull << 32) && b2 < two_q) lc.fold_n = 2;
       }
+      lc.fold_sh = lc.b > 32 ? lc.b - 32 : 0;
+      lc.fold_mhi = lc.b > 32 ? (uint32_t)((1ull << (lc.b - 32)) - 1) : 0;
       const u128 qinv = ~(u128)0 / q;  // floor((2^128 - 1) / q) = floor(2^128 / q) for q not a power of 2
       lc.qinv_hi = (uint64_t)(qinv >> 64);
       lc.qinv_lo = (uint64_t)qinv;

@@ -41,6 +41,8 @@ struct LimbConst {
   uint32_t fold_n;     // folds that bring any 64-bit value below 2q (1 or 2); 0: use reduce64
   uint64_t qinv_hi, qinv_lo;  // floor(2^128 / q): Shoup companions on the device (shoup_prep_kernel)
   uint64_t r64_sh;   // Shoup companion of r64 = 2^64 mod q
+  uint32_t fold_sh;  // b - 32 (reduce_fold works on the high word: b > 32 whenever fold_n > 0)
+  uint32_t fold_mhi; // 2^(b-32) - 1
 };
 enum : uint32_t { SCHEME_CKKS = 0, SCHEME_BFV = 1, SCHEME_BGV = 2 };
 
@@ -176,6 +178,12 @@ struct ZincTLoad {
     return t == 0 ? pt_plus_e<INTS>(raw, se[x >> SHIFT], c) : err_term<INTS>(se[x >> SHIFT], c);
   }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
+  // CKKS: |m| < q/2 makes |m + e| < q, and the residue is branch-free
+  ZINC_DEV bool small(int64_t raw) const { return !INTS && (uint64_t)raw + (c.q >> 1) < c.q; }
+  ZINC_DEV uint64_t lift_small(int64_t raw, int x) const {
+    const int64_t v = raw + se[x >> SHIFT];
+    return (uint64_t)v + (c.q & (uint64_t)(v >> 63));
+  }
 };
 
 // Forward Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> [0, 4q).
@@ -232,11 +240,16 @@ ZINC_DEV uint64_t reduce64(uint64_t x, uint64_t q, uint64_t mu) { return csub(x 
 // One fold is one IMAD.WIDE.U32 (xh c with the masked x as its addend) plus a shift and a
 // mask; fold_n folds leave a value below 2q (checked on the host), one csub finishes.
 // About half the instructions of reduce64's 64 x 64 high product, mostly off the fma pipe.
+// With b > 32 a fold touches only the high word: (hi >> (b-32)) c with {lo, hi & (2^(b-32)-1)}
+// as the addend -- a shift, a mask and one IMAD.WIDE.U32.
+ZINC_DEV uint64_t fold_once(uint64_t x, uint32_t sh, uint32_t mhi, uint32_t c) {
+  const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  return (((uint64_t)(hi & mhi) << 32) | lo) + (uint64_t)(hi >> sh) * c;
+}
 ZINC_DEV uint64_t reduce_fold(uint64_t x, const LimbConst &c) {
-  if (c.fold_n == 0) return reduce64(x, c.q, c.mu64);
-  x = (x & c.fold_mask) + (uint64_t)(uint32_t)(x >> c.b) * c.fold_c;
-  if (c.fold_n == 2) x = (x & c.fold_mask) + (uint64_t)(uint32_t)(x >> c.b) * c.fold_c;
-  return csub(x, c.q);
+  if (c.fold_n == 1) return csub(fold_once(x, c.fold_sh, c.fold_mhi, c.fold_c), c.q);
+  if (c.fold_n == 2) return csub(fold_once(fold_once(x, c.fold_sh, c.fold_mhi, c.fold_c), c.fold_sh, c.fold_mhi, c.fold_c), c.q);
+  return reduce64(x, c.q, c.mu64);
 }
 
 // ------------------------------------------------------------------ Philox4x32-10

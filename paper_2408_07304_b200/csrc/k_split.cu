@@ -134,6 +134,13 @@ struct VanTLoad {
                                                              : reduce_small(tern_at(su, i), c.q);
   }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
+  // CKKS: |m| < q/2 makes |m + e| < q, and the residue is branch-free (t = 1, 2: raw = 0)
+  ZINC_DEV bool small(int64_t raw) const { return !INTS && (uint64_t)raw + (c.q >> 1) < c.q; }
+  ZINC_DEV uint64_t lift_small(int64_t raw, int x) const {
+    const int i = x >> SHIFT;
+    const int64_t v = raw + (t == 0 ? se1[i] : t == 1 ? se2[i] : tern_at(su, i));
+    return (uint64_t)v + (c.q & (uint64_t)(v >> 63));
+  }
 };
 
 template <int LOGN, int MODE>

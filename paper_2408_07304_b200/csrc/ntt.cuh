@@ -38,6 +38,11 @@ struct SmemWords { static constexpr int value = (1 << LOGN) + ((1 << LOGN) >> 4)
 // their latencies overlap instead of each one stalling the lift that consumes it.
 template <class L, class = void> struct TwoPhase { static constexpr bool value = false; };
 template <class L> struct TwoPhase<L, decltype((void)&L::fetch)> { static constexpr bool value = true; };
+// A two-phase load may also offer `small(raw)` and `lift_small(raw, idx)`: a cheaper lift valid
+// when small() holds for the raw value (e.g. |m| < q/2 for a CKKS plaintext word).  A pass
+// takes it when it holds for every word of the whole warp's groups (one vote per group).
+template <class L, class = void> struct HasSmallLift { static constexpr bool value = false; };
+template <class L> struct HasSmallLift<L, decltype((void)&L::lift_small)> { static constexpr bool value = true; };
 
 // ---------------------------------------------------------------- forward pass
 // Load(idx) -> uint64 in [0, 4q); Store(idx, v) with v in [0, 8q) (ct_bfly_a), or below 2^64 with NR.  With
@@ -62,8 +67,21 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
       int64_t raw[G];
 #pragma unroll
       for (int r = 0; r < G; ++r) raw[r] = load.fetch(base + r * T);
+      bool small = HasSmallLift<Load>::value;
+      if constexpr (HasSmallLift<Load>::value) {
 #pragma unroll
-      for (int r = 0; r < G; ++r) v[r] = load.lift(raw[r], base + r * T);
+        for (int r = 0; r < G; ++r) small &= load.small(raw[r]);
+        small = __all_sync(0xffffffffu, small);
+      }
+      if (small) {
+        if constexpr (HasSmallLift<Load>::value) {
+#pragma unroll
+          for (int r = 0; r < G; ++r) v[r] = load.lift_small(raw[r], base + r * T);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < G; ++r) v[r] = load.lift(raw[r], base + r * T);
+      }
     } else {
 #pragma unroll
       for (int r = 0; r < G; ++r) v[r] = load(base + r * T);
@@ -280,13 +298,25 @@ ZINC_DEV void ntt_forward_dit2(uint64_t *sm, const Tw *tw, uint64_t q, Load load
   const int r = (int)cluster_rank();
   __syncthreads();
   if constexpr (TwoPhase<Load>::value) {
-    struct Parity {  // local index i -> coefficient 2 i + r
-      const Load &l;
-      int r;
-      ZINC_DEV int64_t fetch(int i) const { return l.fetch(2 * i + r); }
-      ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, 2 * i + r); }
-    };
-    ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, Parity{load, r}, sst);
+    if constexpr (HasSmallLift<Load>::value) {
+      struct Parity {  // local index i -> coefficient 2 i + r
+        const Load &l;
+        int r;
+        ZINC_DEV int64_t fetch(int i) const { return l.fetch(2 * i + r); }
+        ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, 2 * i + r); }
+        ZINC_DEV bool small(int64_t raw) const { return l.small(raw); }
+        ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, 2 * i + r); }
+      };
+      ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, Parity{load, r}, sst);
+    } else {
+      struct Parity {  // local index i -> coefficient 2 i + r
+        const Load &l;
+        int r;
+        ZINC_DEV int64_t fetch(int i) const { return l.fetch(2 * i + r); }
+        ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, 2 * i + r); }
+      };
+      ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, Parity{load, r}, sst);
+    }
   } else {
     ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, [&](int i) { return load(2 * i + r); },
                                                        sst);
@@ -528,13 +558,25 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
   const int r = (int)cluster_rank();
   __syncthreads();  // the previous transform may still read sm
   if constexpr (TwoPhase<Load>::value) {
-    struct Sub {  // local index i -> coefficient S i + r
-      const Load &l;
-      int r;
-      ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
-      ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
-    };
-    ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst);
+    if constexpr (HasSmallLift<Load>::value) {
+      struct Sub {  // local index i -> coefficient S i + r
+        const Load &l;
+        int r;
+        ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
+        ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
+        ZINC_DEV bool small(int64_t raw) const { return l.small(raw); }
+        ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, S * i + r); }
+      };
+      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst);
+    } else {
+      struct Sub {  // local index i -> coefficient S i + r
+        const Load &l;
+        int r;
+        ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
+        ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
+      };
+      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst);
+    }
   } else {
     ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, [&](int i) { return load(S * i + r); }, sst);
   }

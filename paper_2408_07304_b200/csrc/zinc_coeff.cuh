@@ -125,7 +125,7 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
           uint64_t z10, z11, z20, z21;
           ld2(tile + (size_t)i * T + jl, z10, z11);
           ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
-          auto fold = [&](uint64_t x) { return (x & fm) + (uint64_t)(uint32_t)(x >> fb) * fc; };
+          auto fold = [&](uint64_t x) { return fold_once(x, fb - 32, (uint32_t)(fm >> 32), fc); };
           // each term below 2q, the sum below 6q < 2^64
           const uint64_t s0 = mul_shoup_lazy(reduce_small(h0, q), r64, r64s, q) + fold(p0.x) + z10 + reduce_small(e0, q);
           const uint64_t s1 = mul_shoup_lazy(reduce_small(h1, q), r64, r64s, q) + fold(p1.x) + z11 + reduce_small(e1, q);
