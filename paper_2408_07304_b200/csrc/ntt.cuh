@@ -503,6 +503,17 @@ ZINC_DEV uint64_t ld_dsmem(uint32_t addr) {
   return v;
 }
 
+// Makes every DSMEM load whose value feeds `acc` complete before the next rendezvous: a
+// shared store of acc (a memory operation, so neither the compiler nor the hardware issues
+// the rendezvous before it) that reads every loaded register.  Without it, register-only
+// consumers of the loads may be scheduled after the barrier while the loads are in flight,
+// and a peer that passed the rendezvous overwrites the words being read (measured:
+// scripts/race_check.py, 3 CRT failures in 20480 COEFF-form decryptions).
+ZINC_DEV void loads_done(uint64_t acc) {
+  __shared__ uint64_t sink;
+  asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sink)), "l"(acc) : "memory");
+}
+
 template <int LOGN> struct SplitGeo {
   static constexpr int LL = 12, NL = 1 << LL, S = 1 << (LOGN - LL), LOGS = LOGN - LL;
   static constexpr int THREADS = Plan<LL>::THREADS;   // 256
@@ -599,6 +610,12 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
     for (int u = 0; u < G::KPT; ++u)
 #pragma unroll
       for (int c = 0; c < S; ++c) v[u][c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k0 + u * THREADS));
+    uint64_t acc = 0;
+#pragma unroll
+    for (int u = 0; u < G::KPT; ++u)
+#pragma unroll
+      for (int c = 0; c < S; ++c) acc ^= v[u][c];
+    loads_done(acc);
     cb.sync_war<S>();  // every CTA has read its inputs: shared memory is free
 #pragma unroll
     for (int u = 0; u < G::KPT; ++u) {
@@ -608,6 +625,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
     }
   } else {
     constexpr int U = G::KPT >= 2 ? 2 : 1;
+    uint64_t acc = 0;
 #pragma unroll 1
     for (int u0 = 0; u0 < G::KPT; u0 += U) {
       uint64_t v[U][S];
@@ -616,12 +634,17 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
 #pragma unroll
         for (int c = 0; c < S; ++c) v[u][c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k0 + (u0 + u) * THREADS));
 #pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int c = 0; c < S; ++c) acc ^= v[u][c];
+#pragma unroll
       for (int u = 0; u < U; ++u) {
         const int k = k0 + (u0 + u) * THREADS;
         split_fwd_combine<LOGN, NR>(v[u], k, tw, q);
         out(S * k, v[u]);
       }
     }
+    loads_done(acc);
     cb.sync_war<S>();  // the peers finished reading this CTA's buffer
   }
 }
@@ -662,11 +685,14 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
   Tw w[S];
 #pragma unroll
   for (int i = 1; i < S; ++i) w[i] = ldtw(itw + i);
+  uint64_t acc = 0;
 #pragma unroll 1
   for (int j = r * (NL / S) + threadIdx.x; j < (r + 1) * (NL / S); j += THREADS) {
     uint64_t x[S];
 #pragma unroll
     for (int cc = 0; cc < S; ++cc) x[cc] = ld_dsmem(peer[cc] + 8u * (uint32_t)pad16(j));
+#pragma unroll
+    for (int cc = 0; cc < S; ++cc) acc ^= x[cc];
 #pragma unroll
     for (int t = G::LOGS - 1; t >= 1; --t) {
       const int d = 1 << (G::LOGS - t - 1);
@@ -686,6 +712,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
 #pragma unroll
     for (int cc = 0; cc < S; ++cc) store(j + cc * NL, x[cc]);
   }
+  loads_done(acc);
   cb.sync_war<S>();  // the peers finished reading this CTA's buffer
 }
 

@@ -200,6 +200,23 @@ def test_small_batch_latency_paths_bit_exact(Z, orc, name, B):
         assert np.max(np.abs(zdec.cpu().numpy() - z)) < cfg.tolerance()
 
 
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_split_rendezvous_repeatability(Z, orc, name):
+    """The S-CTA kernels' DSMEM exchanges under load: thousands of cluster rendezvous per call.
+    COEFF-form decryption (forward exchange that reads every input before overwriting its own
+    share) and the encryptions are repeated and must be identical and CRT-consistent every time
+    (a missing load-completion before the buffer-free rendezvous failed ~1 in 7000 here)."""
+    s = setup_for(Z, orc, name)
+    B = 2048 if name == "C3" else 512
+    z = torch.from_numpy(np.ascontiguousarray(slots_batch(s.cfg, 0, B) if not s.cfg.complex_slots else np.stack(
+        [slots_batch(s.cfg, 0, B).real, slots_batch(s.cfg, 0, B).imag], axis=-1))).cuda()
+    ct = Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, z, 8, 0)
+    for _ in range(4):
+        assert torch.equal(Z.ckks_encrypt_batch(s.ctx, s.pk, COEFF, z, 8, 0), ct)
+        _, st, _ = Z.ckks_decrypt_batch(s.ctx, s.sk, COEFF, ct, slots=False)
+        assert int(st.sum()) == 0
+
+
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_encode_within_one(Z, orc, name):
     s = setup_for(Z, orc, name)
