@@ -277,7 +277,9 @@ def c5_sweep(Z, torch, dev, rank, world, batches=(1, 16, 256, 4096, 65536), reps
     """BASELINE C5: N=2^14, 8 x 54-bit, Delta=2^40, uniform slots; latency and ct/s of
     Zinc (COEFF form) and vanilla (NTT form) per batch size over all ranks (batch b split
     as [r b / P, (r+1) b / P); ranks with no message are idle and report 0 ms), device time
-    with CUDA events (1 warm-up + `reps` timed, median; job time = max over ranks), and
+    with CUDA events around the Python call (1 warm-up + `reps` timed, median; job time = max
+    over ranks; at tiny batches it includes the host's argument marshalling before the first
+    launch), the call's kernels' summed device time (`*_kernels_ms`, traced per launch), and
     zinc_precompute_cache timed alone."""
     from paper_2408_07304_b200.dist import max_over_ranks, shard_range
     cfg = CONFIGS["C5"]
@@ -318,13 +320,27 @@ def c5_sweep(Z, torch, dev, rank, world, batches=(1, 16, 256, 4096, 65536), reps
             if nb > z.shape[0]:
                 z = z.repeat((nb + z.shape[0] - 1) // z.shape[0], 1)[:nb].contiguous()
             ct = ctx.empty_ct(nb)
-            zc = timed(lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, z, cfg.enc_seed, b0, out=ct), reps)
-            vn = timed(lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, z, cfg.enc_seed, b0, out=ct), reps)
+            fz = lambda: Z.zinc_encrypt_batch(ctx, cache[Z.COEFF], Z.COEFF, z, cfg.enc_seed, b0, out=ct)
+            fv = lambda: Z.ckks_encrypt_batch(ctx, pk, Z.NTT, z, cfg.enc_seed, b0, out=ct)
+            zc = timed(fz, reps)
+            vn = timed(fv, reps)
+            # device busy time: the library's per-kernel CUDA events, summed (no host gaps)
+            busy = []
+            for fn in (fz, fv):
+                Z.profile_enable(True)
+                fn()
+                torch.cuda.synchronize()
+                busy.append(sum(v[0] for v in Z.profile_read().values()))
+                Z.profile_enable(False)
+            zk, vk = busy
             del ct, z
             torch.cuda.empty_cache()
-        zc, vn = max_over_ranks([zc, vn], device=dev)
+        else:
+            zk = vk = 0.0
+        zc, vn, zk, vk = max_over_ranks([zc, vn, zk, vk], device=dev)
         out["batches"][str(B)] = {"zinc_coeff_ms": zc, "zinc_coeff_ct_per_s": B / (zc / 1e3),
                                   "vanilla_ntt_ms": vn, "vanilla_ntt_ct_per_s": B / (vn / 1e3),
+                                  "zinc_coeff_kernels_ms": zk, "vanilla_ntt_kernels_ms": vk,
                                   "ranks_active": min(world, B), "ranks_idle": max(0, world - B)}
     ctx.close()
     return out
