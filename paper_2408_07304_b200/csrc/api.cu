@@ -892,6 +892,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
   a.coeff_out = x;
   a.status_out = status_out;
   a.L = c->L;
+  a.plain_ckks = c->scheme == ZINC_SCHEME_CKKS && !wide;
   if (wide) {
     a.x128_out = xw;
     a.q0inv_q1 = powm(c->q[0] % c->q[1], c->q[1] - 2, c->q[1]);

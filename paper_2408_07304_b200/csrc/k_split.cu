@@ -61,6 +61,29 @@ template <int LOGN> struct SplitSmem {
 };
 
 // ============================================================ Zinc, NTT form
+// Exchange output of the Zinc NTT form: ct = [cache + v] (v the lazy transform output); the
+// cache words of an output group are loaded by pre() one k ahead (ntt_forward_split).
+template <int S>
+struct ZincNttOut {
+  struct Pre {
+    ulonglong2 z[S / 2];
+  };
+  const uint64_t *z;
+  uint64_t *ctt;
+  const LimbConst &c;
+  ZINC_DEV Pre pre(int x0) const {
+    Pre p;
+#pragma unroll
+    for (int u = 0; u < S / 2; ++u) p.z[u] = ld2_nc(z + x0 + 2 * u);
+    return p;
+  }
+  ZINC_DEV void operator()(int x0, uint64_t (&v)[S], const Pre &p) const {
+#pragma unroll
+    for (int u = 0; u < S / 2; ++u)  // lazy output + canonical cache word < 2^64
+      st2_cs(ctt + x0 + 2 * u, reduce_fold(p.z[u].x + v[2 * u], c), reduce_fold(p.z[u].y + v[2 * u + 1], c));
+  }
+};
+
 // c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2'): both transforms through one copy of
 // the transform code (t at run time); the exchange streams cache-added words to HBM.
 template <int LOGN, int MODE>
@@ -102,18 +125,12 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
       ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoad<INTS, G::LOGS>{m, t ? se2 : se1, c, t},
-          [&](int x0, uint64_t (&v)[S]) {
-#pragma unroll
-            for (int u = 0; u < S; u += 2) {
-              const ulonglong2 zz = ld2_nc(z + x0 + u);  // lazy output + canonical cache word < 2^64
-              st2_cs(ctt + x0 + u, reduce_fold(zz.x + v[u], c), reduce_fold(zz.y + v[u + 1], c));
-            }
-          },
-          stw, [&]() {
+          ZincNttOut<S>{z, ctt, c}, stw, [&]() {
             if (t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
           });
     }
   }
+  cb.settle();  // the peers finished reading this CTA's share
 }
 
 // ============================================================ vanilla, NTT form
@@ -210,6 +227,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
           });
     }
   }
+  cb.settle();  // the peers finished reading this CTA's share
 }
 
 // ============================================================ vanilla, COEFF form
@@ -271,10 +289,12 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
           if (i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
         });
     ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {},
-        [&](int x, uint64_t v) {
-          const uint64_t e = pt_plus_e<INTS>(m ? __ldg(m + x) : 0, se1[inv_sample_idx<LOGN>(x, r)], c);
-          __stcs(ct0 + x, add_mod(csub(v, q), e, q));
-        });
+        with_pre1(
+            [&](int x, uint64_t v, uint64_t mx) {
+              const uint64_t e = pt_plus_e<INTS>((int64_t)mx, se1[inv_sample_idx<LOGN>(x, r)], c);
+              __stcs(ct0 + x, add_mod(csub(v, q), e, q));
+            },
+            [&](int x) { return m ? (uint64_t)__ldg(m + x) : (uint64_t)0; }));
     ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
           __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[inv_sample_idx<LOGN>(x, r)], c), q));
         });
   }
+  cb.settle();  // the peers finished reading this CTA's share
 }
 
 // ============================================================ decrypt (Eq. 10)
@@ -293,7 +314,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
 // c2^ s straight into this CTA's share), inverse split, + c1.  NTT form: inverse split of
 // c1 + c2 s read from global memory.  Each output position is handled by the same thread
 // in every limb, so the CRT check re-reads only words the thread wrote itself.
-template <int LOGN, int FORM, bool NR>
+template <int LOGN, int FORM, bool NR, bool PLAIN = false>
 __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
   using G = SplitGeo<LOGN>;
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL;
@@ -315,14 +336,15 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
     const uint64_t *c2 = c1 + (size_t)L * N;
     const uint64_t *s = a.sk_ntt + (size_t)i * N, *ssh = a.sk_sh + (size_t)i * N;
     const Tw *itw = a.itw + (size_t)i * N;
-    auto epilogue = [&](int x, uint64_t v) {
+    // w = {c1[x] (COEFF form), x0[x] (limbs > 0)}: loaded one exchange index ahead (pre1)
+    auto epilogue = [&](int x, uint64_t v, ulonglong2 w) {
       uint64_t xi = csub(v, q);
-      if (FORM == 1) xi = add_mod(xi, __ldg(c1 + x), q);
-      if (c.scheme == SCHEME_BFV) {
+      if (FORM == 1) xi = add_mod(xi, w.x, q);
+      if (!PLAIN && c.scheme == SCHEME_BFV) {
         a.xl_out[(b * L + i) * N + x] = xi;
         return;
       }
-      if (a.x128_out) {  // wide CKKS: x from limbs 0 and 1, checked on the others
+      if (!PLAIN && a.x128_out) {  // wide CKKS: x from limbs 0 and 1, checked on the others
         int64_t *xw = a.x128_out + (b * N + x) * 2;
         if (i == 0) {
           xw[0] = (int64_t)xi;
@@ -341,11 +363,16 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
         return;
       }
       if (i == 0) {
-        x0[x] = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
+        const int64_t v = xi > q0 / 2 ? -(int64_t)(q0 - xi) : (int64_t)xi;
+        x0[x] = (!PLAIN && c.scheme == SCHEME_BGV && L == 1) ? (int64_t)mod_t(v, c.t, c.t_mu) : v;
       } else {
-        if (reduce_i64(x0[x], c) != xi) bad = 1;
+        if (reduce_i64((int64_t)w.y, c) != xi) bad = 1;
+        if (!PLAIN && c.scheme == SCHEME_BGV && i == L - 1) x0[x] = (int64_t)mod_t((int64_t)w.y, c.t, c.t_mu);
       }
-      if (c.scheme == SCHEME_BGV && i == L - 1) x0[x] = (int64_t)mod_t(x0[x], c.t, c.t_mu);
+    };
+    // x0 is re-read only by the thread that wrote it (the same output positions every limb)
+    auto pre = [&](int x) {
+      return make_ulonglong2(FORM == 1 ? __ldg(c1 + x) : 0, i > 0 ? (uint64_t)x0[x] : 0);
     };
     if (FORM == 0) {
       ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
@@ -354,7 +381,7 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
             for (int u = 0; u < 16; ++u)
               v[u] = __ldg(c1 + base + u) + mul_shoup_lazy(__ldg(c2 + base + u), __ldg(s + base + u), __ldg(ssh + base + u), q);
           },
-          epilogue);
+          with_pre1(epilogue, pre));
     } else {
       const Tw *tw = a.tw + (size_t)i * N;
       // the forward split reads its early-pass twiddles from global memory here (stw = tw)
@@ -365,9 +392,11 @@ __global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
               sm[pad16(x0g + u - r * NL)] = mul_shoup_lazy(v[u], __ldg(s + x0g + u), __ldg(ssh + x0g + u), q);
           },
           tw);
-      ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {}, epilogue);
+      ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {},
+                                     with_pre1(epilogue, pre));
     }
   }
+  cb.settle();
   bad = __syncthreads_or(bad);
   // the cluster's verdict: every CTA publishes its flag, rank 0 reads them over DSMEM
   if (threadIdx.x == 0) bad_flag = bad;
@@ -411,9 +440,10 @@ static cudaError_t launch_decrypt_split_t(const DecryptArgs &a, int form, bool n
   using G = SplitGeo<LOGN>;
   const dim3 grid((unsigned)(batch * G::S));
   const size_t smem = SplitSmem<LOGN>::DATA;
-  if (form == 0) return launch_ex(decrypt_split_kernel<LOGN, 0, false>, grid, G::THREADS, smem, G::S, s, a);
-  if (nr) return launch_ex(decrypt_split_kernel<LOGN, 1, true>, grid, G::THREADS, smem, G::S, s, a);
-  return launch_ex(decrypt_split_kernel<LOGN, 1, false>, grid, G::THREADS, smem, G::S, s, a);
+#define DS(F, R, P) launch_ex(decrypt_split_kernel<LOGN, F, R, P>, grid, G::THREADS, smem, G::S, s, a)
+  if (a.plain_ckks) return form == 0 ? DS(0, false, true) : nr ? DS(1, true, true) : DS(1, false, true);
+  return form == 0 ? DS(0, false, false) : nr ? DS(1, true, false) : DS(1, false, false);
+#undef DS
 }
 
 cudaError_t launch_zinc_ntt_split(int log_n, const ZincNttArgs &a, int mode, size_t batch, int groups, cudaStream_t s) {

@@ -83,6 +83,7 @@ struct DecryptArgs {
   int64_t *x128_out;      // wide CKKS: x from limbs 0 and 1 (two-limb CRT), int64 pairs [B][N][2]
   uint64_t q0inv_q1;      // q_0^-1 mod q_1
   int L;
+  int plain_ckks;         // CKKS, 64-bit coefficients: the kernels compile out BFV / BGV / wide
 };
 struct LiftArgs {           // 128-bit plaintexts -> RNS residues (f3)
   const LimbConst *limbs;

@@ -44,15 +44,21 @@ template <class L> struct TwoPhase<L, decltype((void)&L::fetch)> { static conste
 template <class L, class = void> struct HasSmallLift { static constexpr bool value = false; };
 template <class L> struct HasSmallLift<L, decltype((void)&L::lift_small)> { static constexpr bool value = true; };
 
+struct NoHook {
+  ZINC_DEV void operator()() const {}
+};
+
 // ---------------------------------------------------------------- forward pass
 // Load(idx) -> uint64 in [0, 4q); Store(idx, v) with v in [0, 8q) (ct_bfly_a), or below 2^64 with NR.  With
 // GROUPED, Store is called once per group as store(base, v) with the 2^K words
 // of the group (T == 1: contiguous words base .. base + 2^K - 1).
 // SMEM_TW: `tw` points to a shared-memory copy of the table (the early passes'
-// indices are all < kSmemTw).
+// indices are all < kSmemTw).  pre_store() runs before each group's first store (the
+// split transforms, one group per thread, settle a deferred cluster rendezvous there).
 template <int LOGN, int S0, int K, int THREADS, bool GROUPED = false, bool SMEM_TW = false, bool NR = false,
-          class Load, class Store>
-ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, Store store) {
+          class Load, class Store, class PreStore = NoHook>
+ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, Store store,
+                      PreStore pre_store = PreStore()) {
   constexpr int N = 1 << LOGN;
   constexpr int G = 1 << K;
   constexpr int T = N >> (S0 + K);
@@ -109,6 +115,7 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
         }
       }
     }
+    pre_store();
     if constexpr (GROUPED) {
       store(base, v);
     } else {
@@ -281,9 +288,6 @@ ZINC_DEV void ntt_forward(uint64_t *sm, const Tw *tw, uint64_t q, Load load, GSt
 // pair (2k', 2k'+1) -- global positions, values as the one-CTA transform's -- to
 // `pair(x, v0, v1)`.  The pair function must not write shared memory (the partner may
 // still be reading it); callers stream to global memory.
-struct NoHook {
-  ZINC_DEV void operator()() const {}
-};
 // after_b(): called by every thread once all threads are past pass B (the last use of stw).
 template <int LOGN, bool STW = false, bool NR = false, class Load, class Pair, class AfterB = NoHook>
 ZINC_DEV void ntt_forward_dit2(uint64_t *sm, const Tw *tw, uint64_t q, Load load, Pair pair,
@@ -438,12 +442,20 @@ ZINC_DEV void ntt_inverse(uint64_t *sm, const Tw *itw, const LimbConst &c, GLoad
 // every variant over 10^5 exchanges, scripts/split_check.py):
 //  - sync_raw (peers read this CTA's freshly stored share): the stores must be visible
 //    to remote DSMEM readers, which a CTA-scope fence does not guarantee (observed stale
-//    reads); a cluster-scope release fence (MEMBAR.GPU) per thread does.
+//    reads); a cluster-scope release fence (MEMBAR.GPU) per thread does.  Release only:
+//    fence.acq_rel.cluster adds an acquire, i.e. CCTL.IVALL, which invalidated the SM's L1
+//    (the cached pass-C and exchange twiddles of all three resident CTAs) at every exchange,
+//    while the peers' reads are explicit DSMEM loads that never touch L1.
 //  - sync_war (this CTA will overwrite what the peers read): every DSMEM load of the
 //    exchange must have completed, which the CTA-scope fence (MEMBAR.CTA) ensures.
+//    war_arrive() arrives without waiting and marks the rendezvous pending; settle() waits
+//    for it and must run before the next write to the share (the split forward transform
+//    calls it in pass A just before the first shared-memory store, so the wait overlaps
+//    pass A's loads and butterflies) and before the CTA exits.
 struct ClusterBar {
   uint64_t *mbar;  // [2], this CTA's shared memory
   uint32_t k;
+  bool pending = false;
   template <int S>
   ZINC_DEV void init() {
     if (threadIdx.x == 0) {
@@ -454,6 +466,7 @@ struct ClusterBar {
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     k = 0;
+    pending = false;
     // every CTA's barriers are initialised before anyone arrives remotely (once per kernel)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -477,16 +490,33 @@ struct ClusterBar {
     ++k;
   }
   template <int S>
-  ZINC_DEV void sync_raw() {
-    asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  ZINC_DEV void raw_arrive() {
+    settle();
+    asm volatile("fence.release.cluster;" ::: "memory");
     arrive<S>();
+  }
+  template <int S>
+  ZINC_DEV void sync_raw() {
+    raw_arrive<S>();
     wait();
   }
   template <int S>
-  ZINC_DEV void sync_war() {
+  ZINC_DEV void war_arrive() {
     asm volatile("fence.acq_rel.cta;" ::: "memory");
     arrive<S>();
-    wait();
+    pending = true;
+  }
+  ZINC_DEV void settle() {
+    if (pending) {
+      wait();
+      pending = false;
+    }
+  }
+  template <int S>
+  ZINC_DEV void sync_war() {
+    settle();
+    war_arrive<S>();
+    settle();
   }
 };
 
@@ -524,30 +554,61 @@ template <int LOGN> struct SplitGeo {
 
 // Radix-S combine of the forward transform (register-resident, see above): v[c] = F_{c,s}[k]
 // in, v[m] = a^[S k + m] out.  Level t maps the pair (v[p], v[p + S/2]) to (v'[2p], v'[2p+1])
-// with twiddle W[N / 2^(t+1) + 2^(s-t-1) k + (p mod 2^(s-t-1))].
-template <int LOGN, bool NR>
-ZINC_DEV void split_fwd_combine(uint64_t (&v)[SplitGeo<LOGN>::S], int k, const Tw *tw, uint64_t q) {
+// with twiddle W[N / 2^(t+1) + 2^(s-t-1) k + (p mod 2^(s-t-1))]: 2^(s-t-1) distinct twiddles per
+// level, S - 1 per k, held at w[2^(s-t-1) - 1 + j] (split_fwd_tw loads them, so an exchange can
+// issue them ahead of the rendezvous or of the previous k's stores).
+template <int LOGN>
+ZINC_DEV void split_fwd_tw(Tw (&w)[SplitGeo<LOGN>::S - 1], int k, const Tw *tw) {
   using G = SplitGeo<LOGN>;
-  constexpr int S = G::S, N = 1 << LOGN;
-  const uint64_t two_q = 2 * q;
+  constexpr int N = 1 << LOGN;
 #pragma unroll
   for (int t = G::LOGS - 1; t >= 0; --t) {
     const int span = 1 << (G::LOGS - t - 1);  // 2^(s-t-1)
-    uint64_t o[S];
-    Tw w[S / 2];
 #pragma unroll
-    for (int p = 0; p < S / 2; ++p) w[p] = ldtw(tw + (N >> (t + 1)) + span * k + (p & (span - 1)));
+    for (int j = 0; j < span; ++j) w[span - 1 + j] = ldtw(tw + (N >> (t + 1)) + span * k + j);
+  }
+}
+template <int LOGN, bool NR>
+ZINC_DEV void split_fwd_combine_w(uint64_t (&v)[SplitGeo<LOGN>::S], const Tw (&w)[SplitGeo<LOGN>::S - 1], uint64_t q) {
+  using G = SplitGeo<LOGN>;
+  constexpr int S = G::S;
+  const uint64_t two_q = 2 * q;
+#pragma unroll
+  for (int t = G::LOGS - 1; t >= 0; --t) {
+    const int span = 1 << (G::LOGS - t - 1);
+    uint64_t o[S];
 #pragma unroll
     for (int p = 0; p < S / 2; ++p) {
+      const Tw ww = w[span - 1 + (p & (span - 1))];
       uint64_t X = v[p], Y = v[p + S / 2];
-      if constexpr (NR) ct_bfly_nr(X, Y, w[p].x, w[p].y, q, two_q);
-      else ct_bfly_a(X, Y, w[p].x, w[p].y, q, 2 * two_q);
+      if constexpr (NR) ct_bfly_nr(X, Y, ww.x, ww.y, q, two_q);
+      else ct_bfly_a(X, Y, ww.x, ww.y, q, 2 * two_q);
       o[2 * p] = X;
       o[2 * p + 1] = Y;
     }
 #pragma unroll
     for (int p = 0; p < S; ++p) v[p] = o[p];
   }
+}
+template <int LOGN, bool NR>
+ZINC_DEV void split_fwd_combine(uint64_t (&v)[SplitGeo<LOGN>::S], int k, const Tw *tw, uint64_t q) {
+  Tw w[SplitGeo<LOGN>::S - 1];
+  split_fwd_tw<LOGN>(w, k, tw);
+  split_fwd_combine_w<LOGN, NR>(v, w, q);
+}
+
+// An exchange output functor may offer `pre(x0)`: the global loads its store of outputs
+// x0 .. x0 + S - 1 needs (e.g. the cache words), issued one k ahead like the twiddles.
+template <class O, class = void> struct HasPre { static constexpr bool value = false; };
+template <class O> struct HasPre<O, decltype((void)&O::pre)> { static constexpr bool value = true; };
+struct NoPre {};
+template <class O> ZINC_DEV auto out_pre(const O &o, int x0) {
+  if constexpr (HasPre<O>::value) return o.pre(x0);
+  else return NoPre{};
+}
+template <class O, class V, class P> ZINC_DEV void out_call(O &o, int x0, V &v, const P &p) {
+  if constexpr (HasPre<O>::value) o(x0, v, p);
+  else o(x0, v);
 }
 
 // Forward NTT of one limb by the S-CTA cluster.  `load` as ntt_forward (global coefficient
@@ -567,6 +628,10 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
   auto sst = [&](int i, uint64_t v) { sm[pad16(i)] = v; };
   auto sld = [&](int i) { return sm[pad16(i)]; };
   const int r = (int)cluster_rank();
+  // a deferred buffer-free rendezvous (the previous exchange) settles just before pass A's
+  // first shared-memory store: one group per thread, so once per thread
+  static_assert(P::THREADS == THREADS && (G::NL >> P::KA) == THREADS, "one pass-A group per thread");
+  auto settle = [&]() { cb.settle(); };
   __syncthreads();  // the previous transform may still read sm
   if constexpr (TwoPhase<Load>::value) {
     if constexpr (HasSmallLift<Load>::value) {
@@ -578,7 +643,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
         ZINC_DEV bool small(int64_t raw) const { return l.small(raw); }
         ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, S * i + r); }
       };
-      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst);
+      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst, settle);
     } else {
       struct Sub {  // local index i -> coefficient S i + r
         const Load &l;
@@ -586,10 +651,10 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
         ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
         ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
       };
-      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst);
+      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst, settle);
     }
   } else {
-    ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, [&](int i) { return load(S * i + r); }, sst);
+    ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, [&](int i) { return load(S * i + r); }, sst, settle);
   }
   __syncthreads();
   ct_pass<LL, SB, P::KB, THREADS, false, true, NR>(stw, q, 1, sld, sst);
@@ -599,12 +664,12 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
 #pragma unroll
     for (int j = 0; j < 16; ++j) sm[pad16(base + j)] = v[j];
   });
-  cb.sync_raw<S>();  // every CTA's sub-transform complete
   uint32_t peer[S];
 #pragma unroll
   for (int c = 0; c < S; ++c) peer[c] = dsmem_addr(sm, (uint32_t)c);
   const int k0 = r * (G::NL / S) + threadIdx.x;
   if constexpr (LOAD_ALL) {
+    cb.sync_raw<S>();  // every CTA's sub-transform complete
     uint64_t v[G::KPT][S];
 #pragma unroll
     for (int u = 0; u < G::KPT; ++u)
@@ -624,30 +689,94 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
       out(S * k, v[u]);
     }
   } else {
-    constexpr int U = G::KPT >= 2 ? 2 : 1;
+    // Software-pipelined exchange, one k per step: the twiddles and the output functor's
+    // global loads of k are issued before the rendezvous (k = the first) or before the
+    // previous k's stores, and so is k's DSMEM gather, so no global-load latency sits
+    // between a store and the next k.  The buffer-free rendezvous is deferred (settle()).
+    constexpr int S1 = S - 1;
+    constexpr bool DB = S <= 4;  // double-buffered registers (k and k + 1) fit at S = 4
+    using PreT = decltype(out_pre(out, 0));
+    cb.raw_arrive<S>();  // every CTA's sub-transform complete (wait below)
+    Tw wc[S1];
+    PreT pc;
+    split_fwd_tw<LOGN>(wc, k0, tw);
+    pc = out_pre(out, S * k0);
+    cb.wait();
+    uint64_t vc[S];
+#pragma unroll
+    for (int c = 0; c < S; ++c) vc[c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k0));
     uint64_t acc = 0;
-#pragma unroll 1
-    for (int u0 = 0; u0 < G::KPT; u0 += U) {
-      uint64_t v[U][S];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+    for (int u = 0; u < G::KPT; ++u) {
+      const int k = k0 + u * THREADS;
+      if constexpr (DB) {
+        Tw wn[S1];
+        PreT pn;
+        uint64_t vn[S];
+        if (u + 1 < G::KPT) {
+          split_fwd_tw<LOGN>(wn, k + THREADS, tw);
+          pn = out_pre(out, S * (k + THREADS));
 #pragma unroll
-        for (int c = 0; c < S; ++c) v[u][c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k0 + (u0 + u) * THREADS));
+          for (int c = 0; c < S; ++c) vn[c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k + THREADS));
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+        for (int c = 0; c < S; ++c) acc ^= vc[c];
+        split_fwd_combine_w<LOGN, NR>(vc, wc, q);
+        out_call(out, S * k, vc, pc);
+        if (u + 1 < G::KPT) {
 #pragma unroll
-        for (int c = 0; c < S; ++c) acc ^= v[u][c];
+          for (int c = 0; c < S; ++c) vc[c] = vn[c];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = k0 + (u0 + u) * THREADS;
-        split_fwd_combine<LOGN, NR>(v[u], k, tw, q);
-        out(S * k, v[u]);
+          for (int j = 0; j < S1; ++j) wc[j] = wn[j];
+          pc = pn;
+        }
+      } else {  // S = 8: registers for one k only
+        if (u > 0) {
+          split_fwd_tw<LOGN>(wc, k, tw);
+          pc = out_pre(out, S * k);
+#pragma unroll
+          for (int c = 0; c < S; ++c) vc[c] = ld_dsmem(peer[c] + 8u * (uint32_t)pad16(k));
+        }
+#pragma unroll
+        for (int c = 0; c < S; ++c) acc ^= vc[c];
+        split_fwd_combine_w<LOGN, NR>(vc, wc, q);
+        out_call(out, S * k, vc, pc);
       }
     }
     loads_done(acc);
-    cb.sync_war<S>();  // the peers finished reading this CTA's buffer
+    cb.war_arrive<S>();  // the peers may overwrite their shares once every CTA arrived
   }
 }
+
+// An inverse-exchange store functor may offer `pre1(x)`: the global words its store of output
+// x needs (a ciphertext or plaintext word), then called as store(x, v, words).  WithPre1 adds
+// it to a plain functor pair.
+template <class O, class = void> struct HasPre1 { static constexpr bool value = false; };
+template <class O> struct HasPre1<O, decltype((void)&O::pre1)> { static constexpr bool value = true; };
+template <int S, class T> struct PreW {
+  T w[S];
+};
+template <int S, int NL, class O> ZINC_DEV auto inv_pre(const O &o, int j) {
+  if constexpr (HasPre1<O>::value) {
+    PreW<S, decltype(o.pre1(0))> p;
+#pragma unroll
+    for (int cc = 0; cc < S; ++cc) p.w[cc] = o.pre1(j + cc * NL);
+    return p;
+  } else {
+    return NoPre{};
+  }
+}
+template <class O, class P> ZINC_DEV void inv_store(O &o, int x, uint64_t v, const P &p, int cc) {
+  if constexpr (HasPre1<O>::value) o(x, v, p.w[cc]);
+  else o(x, v);
+}
+template <class F, class G> struct WithPre1 {
+  F f;
+  G g;
+  ZINC_DEV auto pre1(int x) const { return g(x); }
+  template <class W> ZINC_DEV void operator()(int x, uint64_t v, const W &w) const { f(x, v, w); }
+};
+template <class F, class G> ZINC_DEV WithPre1<F, G> with_pre1(F f, G g) { return WithPre1<F, G>{f, g}; }
 
 // Inverse NTT of one limb by the S-CTA cluster.  With GLOBAL_IN, `gload(base, v[16])`
 // supplies the 16 contiguous inputs at global position base (in [r NL, (r+1) NL)) in
@@ -665,6 +794,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
   auto sld = [&](int i) { return sm[pad16(i)]; };
   const int r = (int)cluster_rank();
   const int tb = S + r;
+  cb.settle();  // a deferred buffer-free rendezvous completes before this share is rewritten
   __syncthreads();
   if constexpr (GLOBAL_IN) {
     gs_pass<LL, SC, P::KC, THREADS, true>(itw, c, tb, [&](int base, uint64_t (&v)[16]) { gload(base + r * NL, v); },
@@ -676,23 +806,49 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
   gs_pass<LL, SB, P::KB, THREADS>(itw, c, tb, sld, sst);
   __syncthreads();
   gs_pass<LL, 0, P::KA, THREADS, false, false>(itw, c, tb, sld, sst);
-  cb.sync_raw<S>();  // every share transformed, every input consumed
-  uint32_t peer[S];
-#pragma unroll
-  for (int cc = 0; cc < S; ++cc) peer[cc] = dsmem_addr(sm, (uint32_t)cc);
   const uint64_t q = c.q, four_q = 2 * c.two_q;
   // the S - 1 cross-share twiddles: stage t uses W^-1[2^t + beta], beta < 2^t
   Tw w[S];
 #pragma unroll
   for (int i = 1; i < S; ++i) w[i] = ldtw(itw + i);
+  // Software-pipelined exchange as the forward's: the store functor's global words (pre1) of
+  // index j are loaded before the rendezvous (the first j) or before the previous j's stores,
+  // with j's DSMEM gather.
+  cb.raw_arrive<S>();  // every share transformed, every input consumed (wait below)
+  uint32_t peer[S];
+#pragma unroll
+  for (int cc = 0; cc < S; ++cc) peer[cc] = dsmem_addr(sm, (uint32_t)cc);
+  const int j0 = r * (NL / S) + threadIdx.x;
+  auto pc = inv_pre<S, NL>(store, j0);
+  cb.wait();
+  uint64_t xc[S];
+#pragma unroll
+  for (int cc = 0; cc < S; ++cc) xc[cc] = ld_dsmem(peer[cc] + 8u * (uint32_t)pad16(j0));
   uint64_t acc = 0;
-#pragma unroll 1
-  for (int j = r * (NL / S) + threadIdx.x; j < (r + 1) * (NL / S); j += THREADS) {
-    uint64_t x[S];
+  // one index ahead: the pre words when there is one per output, the gather too at S = 4
+  constexpr bool PRE_DB = sizeof(decltype(pc)) <= S * sizeof(uint64_t);
+  constexpr bool DB = S <= 4 && PRE_DB;
 #pragma unroll
-    for (int cc = 0; cc < S; ++cc) x[cc] = ld_dsmem(peer[cc] + 8u * (uint32_t)pad16(j));
+  for (int u = 0; u < G::KPT; ++u) {
+    const int j = j0 + u * THREADS;
+    uint64_t xn[DB ? S : 1];
+    decltype(pc) pn;
+    if (u > 0) {
+      if constexpr (!PRE_DB) pc = inv_pre<S, NL>(store, j);
+      if constexpr (!DB) {
 #pragma unroll
-    for (int cc = 0; cc < S; ++cc) acc ^= x[cc];
+        for (int cc = 0; cc < S; ++cc) xc[cc] = ld_dsmem(peer[cc] + 8u * (uint32_t)pad16(j));
+      }
+    }
+    if (u + 1 < G::KPT) {
+      if constexpr (PRE_DB) pn = inv_pre<S, NL>(store, j + THREADS);
+      if constexpr (DB) {
+#pragma unroll
+        for (int cc = 0; cc < S; ++cc) xn[cc] = ld_dsmem(peer[cc] + 8u * (uint32_t)pad16(j + THREADS));
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < S; ++cc) acc ^= xc[cc];
 #pragma unroll
     for (int t = G::LOGS - 1; t >= 1; --t) {
       const int d = 1 << (G::LOGS - t - 1);
@@ -700,20 +856,27 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
       for (int cc = 0; cc < S; ++cc)
         if ((cc & d) == 0) {
           const Tw ww = w[(1 << t) + (cc >> (G::LOGS - t))];
-          gs_bfly(x[cc], x[cc + d], ww.x, ww.y, q, four_q);
+          gs_bfly(xc[cc], xc[cc + d], ww.x, ww.y, q, four_q);
         }
     }
 #pragma unroll
     for (int cc = 0; cc < S / 2; ++cc) {  // stage 0: pairs (c, c + S/2), N^-1 folded in
-      const uint64_t X = x[cc], Y = x[cc + S / 2];
-      x[cc] = mul_shoup_lazy(X + Y, c.ninv, c.ninv_sh, q);
-      x[cc + S / 2] = mul_shoup_lazy(X - Y + four_q, c.ninv_w, c.ninv_w_sh, q);
+      const uint64_t X = xc[cc], Y = xc[cc + S / 2];
+      xc[cc] = mul_shoup_lazy(X + Y, c.ninv, c.ninv_sh, q);
+      xc[cc + S / 2] = mul_shoup_lazy(X - Y + four_q, c.ninv_w, c.ninv_w_sh, q);
     }
 #pragma unroll
-    for (int cc = 0; cc < S; ++cc) store(j + cc * NL, x[cc]);
+    for (int cc = 0; cc < S; ++cc) inv_store(store, j + cc * NL, xc[cc], pc, cc);
+    if (u + 1 < G::KPT) {
+      if constexpr (DB) {
+#pragma unroll
+        for (int cc = 0; cc < S; ++cc) xc[cc] = xn[cc];
+      }
+      if constexpr (PRE_DB) pc = pn;
+    }
   }
   loads_done(acc);
-  cb.sync_war<S>();  // the peers finished reading this CTA's buffer
+  cb.war_arrive<S>();  // the peers finished reading this CTA's buffer once every CTA arrived
 }
 
 }  // namespace zinc
