@@ -186,6 +186,14 @@ struct ZincTLoad {
   }
 };
 
+// ZincTLoad with the smallness of m decided once per message (plaintext_small, k_split.cu):
+// t = 1 (e2', no plaintext) is always small.
+template <bool INTS, int SHIFT = 1>
+struct ZincTLoadU : ZincTLoad<INTS, SHIFT> {
+  bool all_small;
+  ZINC_DEV bool uniform_small() const { return !INTS && (all_small || this->t != 0); }
+};
+
 // Forward Cooley-Tukey butterfly, lazy (Harvey): X, Y in [0, 4q) -> [0, 4q).
 ZINC_DEV void ct_bfly(uint64_t &X, uint64_t &Y, uint64_t w, uint64_t wp, uint64_t q, uint64_t two_q) {
   uint64_t x = csub(X, two_q);

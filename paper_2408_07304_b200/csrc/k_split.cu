@@ -54,6 +54,22 @@ ZINC_DEV int inv_sample_idx(int x, int r) {
   return (x >> G::LL) * span + (x & (G::NL - 1)) - r * span;
 }
 
+// CKKS plaintext words of this CTA's subsequence (x = S i + r) all below q_min / 2 in absolute
+// value (q_min over the CTA's limbs): then every lift of m + e is branch-free (lift_small), for
+// every limb, decided once per message instead of per word, limb and transform.
+template <int LOGN, int THREADS>
+ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, int lo, int hi) {
+  using G = SplitGeo<LOGN>;
+  if (!m) return true;
+  uint64_t qmin = ~0ull;
+  for (int i = lo; i < hi; ++i) qmin = min(qmin, limbs[i].q);
+  const uint64_t half = qmin >> 1;
+  int big = 0;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < G::NL; i += THREADS) big |= (uint64_t)__ldg(m + G::S * i + r) + half >= qmin;
+  return !__syncthreads_or(big);
+}
+
 template <int LOGN> struct SplitSmem {
   using G = SplitGeo<LOGN>;
   static constexpr size_t DATA = SmemWords<G::LL>::value * sizeof(uint64_t);  // 34816
@@ -114,6 +130,7 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -124,7 +141,7 @@ __global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
     for (int t = t_lo; t < t_hi; ++t) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
-      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoad<INTS, G::LOGS>{m, t ? se2 : se1, c, t},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoadU<INTS, G::LOGS>{{m, t ? se2 : se1, c, t}, all_small},
           ZincNttOut<S>{z, ctt, c}, stw, [&]() {
             if (t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
           });
@@ -150,9 +167,10 @@ struct VanTLoad {
     return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
                                                              : reduce_small(tern_at(su, i), c.q);
   }
+  bool all_small;  // CTA-uniform (plaintext_small, or t > 0: no plaintext term)
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
   // CKKS: |m| < q/2 makes |m + e| < q, and the residue is branch-free (t = 1, 2: raw = 0)
-  ZINC_DEV bool small(int64_t raw) const { return !INTS && (uint64_t)raw + (c.q >> 1) < c.q; }
+  ZINC_DEV bool uniform_small() const { return !INTS && all_small; }
   ZINC_DEV uint64_t lift_small(int64_t raw, int x) const {
     const int i = x >> SHIFT;
     const int64_t v = raw + (t == 0 ? se1[i] : t == 1 ? se2[i] : tern_at(su, i));
@@ -191,6 +209,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
   pdl_trigger();
   pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -203,7 +222,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
     tws.wait();
 #pragma unroll 1
     for (int t = t_lo; t < t_hi; ++t) {
-      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t, all_small || t > 0},
           [&](int x0, uint64_t (&v)[S]) {
             if (t < 2 || gridDim.z > 1) {
               uint64_t *dst = (t == 0 ? ct0 : t == 1 ? ct1 : a.u_hat + (b * L + i) * N) + x0;

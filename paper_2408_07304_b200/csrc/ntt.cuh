@@ -43,6 +43,10 @@ template <class L> struct TwoPhase<L, decltype((void)&L::fetch)> { static conste
 // takes it when it holds for every word of the whole warp's groups (one vote per group).
 template <class L, class = void> struct HasSmallLift { static constexpr bool value = false; };
 template <class L> struct HasSmallLift<L, decltype((void)&L::lift_small)> { static constexpr bool value = true; };
+// ... or decide it once for every word it will ever load: uniform_small() (a CTA-uniform flag
+// the kernel computed up front), which spares the per-word test and the warp vote.
+template <class L, class = void> struct HasUniformSmall { static constexpr bool value = false; };
+template <class L> struct HasUniformSmall<L, decltype((void)&L::uniform_small)> { static constexpr bool value = true; };
 
 struct NoHook {
   ZINC_DEV void operator()() const {}
@@ -74,7 +78,9 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
 #pragma unroll
       for (int r = 0; r < G; ++r) raw[r] = load.fetch(base + r * T);
       bool small = HasSmallLift<Load>::value;
-      if constexpr (HasSmallLift<Load>::value) {
+      if constexpr (HasUniformSmall<Load>::value) {
+        small = load.uniform_small();
+      } else if constexpr (HasSmallLift<Load>::value) {
 #pragma unroll
         for (int r = 0; r < G; ++r) small &= load.small(raw[r]);
         small = __all_sync(0xffffffffu, small);
@@ -484,8 +490,10 @@ struct ClusterBar {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar + (k & 1)), par = (k >> 1) & 1u;
     uint32_t done = 0;
     while (!done) {
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done) : "r"(a), "r"(par) : "memory");
+      // with a suspend-time hint the thread sleeps in try_wait until the phase completes
+      // instead of re-polling (spin iterations took ~1 instruction per butterfly)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(a), "r"(par), "r"(0x989680u) : "memory");
     }
     ++k;
   }
@@ -634,7 +642,17 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
   auto settle = [&]() { cb.settle(); };
   __syncthreads();  // the previous transform may still read sm
   if constexpr (TwoPhase<Load>::value) {
-    if constexpr (HasSmallLift<Load>::value) {
+    if constexpr (HasUniformSmall<Load>::value) {
+      struct Sub {  // local index i -> coefficient S i + r
+        const Load &l;
+        int r;
+        ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
+        ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
+        ZINC_DEV bool uniform_small() const { return l.uniform_small(); }
+        ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, S * i + r); }
+      };
+      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst, settle);
+    } else if constexpr (HasSmallLift<Load>::value) {
       struct Sub {  // local index i -> coefficient S i + r
         const Load &l;
         int r;
