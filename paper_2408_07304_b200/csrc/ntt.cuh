@@ -490,10 +490,8 @@ struct ClusterBar {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar + (k & 1)), par = (k >> 1) & 1u;
     uint32_t done = 0;
     while (!done) {
-      // with a suspend-time hint the thread sleeps in try_wait until the phase completes
-      // instead of re-polling (spin iterations took ~1 instruction per butterfly)
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done) : "r"(a), "r"(par), "r"(0x989680u) : "memory");
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(a), "r"(par) : "memory");
     }
     ++k;
   }

@@ -31,7 +31,11 @@ for f in re.split(r"\n\s*Function : ", sass)[1:]:
     body = {k: v for k, v in ops.items() if not k.startswith(LOOP_OVERHEAD)}
     n = sum(body.values())
     fma = sum(v for k, v in body.items() if k.startswith(("IMAD", "HFMA2", "FFMA", "FMUL")))
-    res[int(m.group(1))] = (n / 8, fma / 8, body)
+    # butterflies per loop trip: 8 per source iteration times ptxas's unroll factor; the
+    # 3-partial-product Shoup quotient (variants 1-3) has exactly two IMAD.HI.U32 per butterfly
+    v = int(m.group(1))
+    nb = 8 if v == 0 else max(8, 8 * round(body.get("IMAD.HI.U32", 16) / 16))
+    res[v] = (n / nb, fma / nb, body)
 for v in sorted(res):
     n, fma, body = res[v]
     print(f"{v} {NAMES[v]:11s} instr/bfly {n:6.3f}  fma-pipe/bfly {fma:6.3f}  other/bfly {n - fma:6.3f}  "
