@@ -116,6 +116,7 @@ static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1},
 struct zinc_ctx {
   int device, log_n, n, L, log_scale;
   int num_sms = 0;
+  size_t encode_wave_msgs[2] = {0, 0};  // messages per full encode wave: real, complex slots
   int scheme = ZINC_SCHEME_CKKS;
   uint64_t t = 0;  // plaintext modulus (BFV, BGV)
   bool wide = false;  // CKKS with log_scale >= 48: slot plaintexts take the 128-bit path
@@ -456,6 +457,8 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     zinc_ctx_destroy(c);
     return fail(ZINC_ECUDA, "device attribute query failed");
   }
+  for (int cx = 0; cx < 2; ++cx) c->encode_wave_msgs[cx] = encode_wave_msgs(log_n, cx == 1, c->num_sms);
+  cudaGetLastError();  // an occupancy query failure only disables the wave rounding
   // stream-ordered scratch (slot encodes) comes from the default pool: keep it
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -739,6 +742,13 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
   if (coeff_zinc) {
     const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());
     chunk = chunk_bytes / per_msg;
+    // whole waves of the encode: its last wave would otherwise run part-empty once per chunk
+    // (C4: 128 messages = 1.73 waves of 74 -> 148; C3: 256 of 296 -> 296), within 1.25x the bytes
+    const size_t w = c->encode_wave_msgs[kind == ZINC_PT_SLOTS_C128];
+    if (w > 0) {
+      const size_t r = std::max<size_t>(1, (chunk + w / 2) / w) * w;
+      if (r * 4 <= chunk * 5) chunk = r;
+    }
   } else {
     const long long knob = g_tune[ZINC_TUNE_NTT_CHUNK_MSGS].load();
     // 16 waves of two message-CTA groups per SM (the transform kernels' residency)

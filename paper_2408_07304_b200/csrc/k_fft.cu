@@ -231,6 +231,36 @@ static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream
   return launch_ex(encode_kernel<LOGM>, dim3((unsigned)(batch * C)), FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
                    encode_smem<LOGM>(), C, s, a);
 }
+// Messages one full wave of the (throughput) encode kernel covers: resident CTAs per SM (the
+// occupancy calculator, with the kernel's dynamic shared memory) x SMs / CTAs per message.
+template <int LOGM>
+static size_t encode_wave_msgs_t(bool complex_slots, int num_sms) {
+  int per_sm = 0;
+  if (!complex_slots) {
+    if (set_smem(encode_real_kernel<LOGM, false>, encode_real_smem<LOGM>()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_real_kernel<LOGM, false>, 256,
+                                                      encode_real_smem<LOGM>()) != cudaSuccess)
+      return 0;
+    return (size_t)per_sm * num_sms;
+  }
+  constexpr int C = LOGM > 13 ? 2 : 1;
+  if (set_smem(encode_kernel<LOGM>, encode_smem<LOGM>()) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_kernel<LOGM>,
+                                                    FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
+                                                    encode_smem<LOGM>()) != cudaSuccess)
+    return 0;
+  return (size_t)per_sm * num_sms / C;
+}
+size_t encode_wave_msgs(int log_n, bool complex_slots, int num_sms) {
+  switch (log_n) {
+    case 12: return encode_wave_msgs_t<11>(complex_slots, num_sms);
+    case 13: return encode_wave_msgs_t<12>(complex_slots, num_sms);
+    case 14: return encode_wave_msgs_t<13>(complex_slots, num_sms);
+    case 15: return encode_wave_msgs_t<14>(complex_slots, num_sms);
+  }
+  return 0;
+}
+
 cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s) {
 #define CALL(K) launch_encode_t<K - 1>(a, batch, s)
   ZINC_LOGN_SWITCH(log_n, CALL)

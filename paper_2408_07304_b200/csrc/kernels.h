@@ -175,6 +175,8 @@ cudaError_t launch_bfv_scale(const BfvScaleArgs &a, cudaStream_t s);
 cudaError_t launch_lift(const LiftArgs &a, cudaStream_t s);
 cudaError_t launch_pt_add(const PtAddArgs &a, cudaStream_t s);
 cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s);
+// messages per full wave of the encode kernel (0 if unknown)
+size_t encode_wave_msgs(int log_n, bool complex_slots, int num_sms);
 cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s);
 cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s);
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
