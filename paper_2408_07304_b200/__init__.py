@@ -118,19 +118,29 @@ def _check(rc: int, what: str):
 
 
 def _ptr(t):
+    """Device address of a contiguous tensor (or an int address) as a plain int: the
+    argtypes (c_void_p) convert it, so no ctypes object is built per argument."""
     if t is None:
         return None
     if isinstance(t, torch.Tensor):
         if not t.is_contiguous():
             raise ZincError("tensor must be contiguous")
-        return ctypes.c_void_p(t.data_ptr())
-    return ctypes.c_void_p(int(t))
+        return t.data_ptr()
+    return int(t)
+
+
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 
 
 def _stream(stream=None):
+    """cudaStream_t of `stream`, else of torch's current stream on the current device (read
+    through torch's raw-stream accessor: about a microsecond less per call than building a
+    torch.cuda.Stream object on the small-batch latency path)."""
     if stream is None:
+        if _raw_stream is not None:
+            return _raw_stream(torch.cuda.current_device())
         stream = torch.cuda.current_stream()
-    return ctypes.c_void_p(stream.cuda_stream)
+    return stream.cuda_stream
 
 
 class Context:

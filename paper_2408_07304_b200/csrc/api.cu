@@ -209,6 +209,14 @@ static zinc_status upload(T **dst, const std::vector<T> &src) {
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
 // Stream-ordered scratch, released (cudaFreeAsync on its stream) on every exit path.
+// cudaSetDevice only when the device is not already current (it is on every call of a
+// one-GPU process; the runtime call itself costs host time on the small-batch path).
+static cudaError_t use_device(int d) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur == d) return cudaSuccess;
+  return cudaSetDevice(d);
+}
+
 struct ScratchBuf {
   void *p = nullptr;
   cudaStream_t s;
@@ -792,7 +800,7 @@ static zinc_status check_encrypt(const zinc_ctx *c, const uint64_t *key, int for
   if ((st = check_form(form)) || (st = check_kind(kind)) || (st = check_ptrs({key, pt, ct}))) return st;
   if (c->scheme != ZINC_SCHEME_CKKS && kind != ZINC_PT_COEFF_I64)
     return fail(ZINC_EINVAL, "BFV / BGV contexts take integer plaintext coefficients (ZINC_PT_COEFF_I64)");
-  if (cudaSetDevice(c->device) != cudaSuccess) return fail(ZINC_ECUDA, "cudaSetDevice failed");
+  if (use_device(c->device) != cudaSuccess) return fail(ZINC_ECUDA, "cudaSetDevice failed");
   return ZINC_OK;
 }
 
@@ -803,7 +811,7 @@ zinc_status zinc_keygen(const zinc_ctx *c, uint64_t seed, uint64_t *sk_ntt, int8
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_ptrs({sk_ntt, pk_ntt}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   KeygenArgs a{};
   a.limbs = c->d_limbs;
   a.tw = c->d_tw;
@@ -822,7 +830,7 @@ zinc_status zinc_precompute_cache(const zinc_ctx *c, const uint64_t *pk_ntt, uin
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_form(form)) || (st = check_ptrs({pk_ntt, cache}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   // C-8: vanilla Enc(0), message index 2^64 - 1
   return run_path(c, PATH_VANILLA, pk_ntt, form, nullptr, 1, seed, UINT64_MAX, cache, (cudaStream_t)stream);
 }
@@ -884,7 +892,7 @@ static zinc_status decrypt_impl(const zinc_ctx *c, const uint64_t *sk_ntt, int f
   if (coeff128_out && ((uintptr_t)coeff128_out & 15u)) return fail(ZINC_EINVAL, "output pointer misaligned");
   if (c->scheme != ZINC_SCHEME_CKKS && slots_out)
     return fail(ZINC_EINVAL, "BFV / BGV decryption has no slot decoding (slots_out must be NULL)");
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   ScratchBuf xb(s), xwb(s), xlb(s), skb(s);
   CUDA_TRY(skb.alloc((size_t)c->L * c->n * 8));
   LAUNCH(ZINC_K_SHOUP_PREP, s, launch_shoup_prep(c->d_limbs, sk_ntt, skb.as<uint64_t>(), (size_t)c->L * c->n, c->log_n, c->L, s));
@@ -961,7 +969,7 @@ zinc_status zinc_ct_add_batch(const zinc_ctx *c, const uint64_t *x, const uint64
   if (batch == 0) return ZINC_OK;
   zinc_status st;
   if ((st = check_ptrs({x, y, out}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   CtAddArgs a{};
   a.limbs = c->d_limbs;
   a.a = x;
@@ -980,7 +988,7 @@ zinc_status zinc_ct_sum_batch(const zinc_ctx *c, const uint64_t *ct, size_t batc
   if (!c) return fail(ZINC_EINVAL, "null ctx");
   zinc_status st;
   if ((st = check_ptrs({out})) || (batch && (st = check_ptrs({ct})))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   CtSumArgs a{};
   a.limbs = c->d_limbs;
   a.ct = ct;
@@ -1000,7 +1008,7 @@ zinc_status ckks_encode_batch_wide(const zinc_ctx *c, zinc_pt_kind kind, const v
   if (kind != ZINC_PT_SLOTS_F64 && kind != ZINC_PT_SLOTS_C128) return fail(ZINC_EINVAL, "encode needs a slot kind");
   zinc_status st;
   if ((st = check_ptrs({slots, m_out}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   return encode_into(c, kind, slots, batch, m_out, (cudaStream_t)stream, true);
 }
 
@@ -1012,7 +1020,7 @@ zinc_status ckks_encode_batch(const zinc_ctx *c, zinc_pt_kind kind, const void *
   if (kind != ZINC_PT_SLOTS_F64 && kind != ZINC_PT_SLOTS_C128) return fail(ZINC_EINVAL, "encode needs a slot kind");
   zinc_status st;
   if ((st = check_ptrs({slots, m_out}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   return encode_into(c, kind, slots, batch, m_out, (cudaStream_t)stream);
 }
 
@@ -1021,7 +1029,7 @@ static zinc_status ntt_dir(const zinc_ctx *c, uint64_t *data, size_t count, int 
   if (count == 0) return ZINC_OK;
   zinc_status st;
   if ((st = check_ptrs({data}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   NttArgs a{};
   a.limbs = c->d_limbs;
   a.tw = c->d_tw;
@@ -1049,7 +1057,7 @@ zinc_status zinc_debug_sample(const zinc_ctx *c, int tag, uint64_t seed, uint64_
   if (n == 0) return ZINC_OK;
   zinc_status st;
   if ((st = check_ptrs({out}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   SampleArgs a{};
   a.tag = (uint32_t)tag;
   a.limb = (uint32_t)limb;
@@ -1071,7 +1079,7 @@ zinc_status zinc_int_peak(const zinc_ctx *c, int variant, int blocks, int iters,
   if (variant == 1 && c->q[0] >= (1ull << 58)) return fail(ZINC_EINVAL, "lazy-free butterflies need q < 2^58");
   zinc_status st;
   if ((st = check_ptrs({sink}))) return st;
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   IntPeakArgs a{};
   a.q = c->q[0];
   a.w = c->psi[0];
@@ -1096,7 +1104,7 @@ zinc_status zinc_encrypt_batch_host(const zinc_ctx *c, int path, const uint64_t 
     return fail(ZINC_EINVAL, "BFV / BGV contexts take integer plaintext coefficients (ZINC_PT_COEFF_I64)");
   if (chunk == 0) chunk = 256;
   chunk = std::min(chunk, batch);
-  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(use_device(c->device));
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_words = (size_t)2 * c->L * c->n;
   // Per-call resources (the context stays immutable): two streams, an event ordering them

@@ -5,6 +5,9 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -185,9 +188,27 @@ struct TwStager {
 };
 
 // ============================================================ launchers
+// The dynamic shared-memory opt-in of a kernel, set once per (kernel, device, size): a
+// cudaFuncSetAttribute per launch cost ~1 us of host time on every small-batch call.
 template <class K>
 inline cudaError_t set_smem(K kernel, size_t bytes) {
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (bytes <= 48 * 1024) return cudaSuccess;  // below the default limit: no opt-in needed
+  static std::mutex mu;
+  static std::vector<std::tuple<const void *, int, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void *k = reinterpret_cast<const void *>(kernel);
+  {
+    std::lock_guard<std::mutex> l(mu);
+    for (const auto &d : done)
+      if (std::get<0>(d) == k && std::get<1>(d) == dev && std::get<2>(d) >= bytes) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> l(mu);
+    done.emplace_back(k, dev, bytes);
+  }
+  return e;
 }
 
 // Programmatic dependent launch (PdlScope in kernels.h): kernels trigger their dependents
