@@ -7,6 +7,12 @@
 
 namespace zinc {
 
+// resident CTAs per SM the cluster kernels are compiled for: 4 (64 registers, 47 KiB each;
+// measured +4-14% over 3 at C3 / C4 despite ~60 B of spills)
+#ifndef ZINC_SPLIT_MINB
+#define ZINC_SPLIT_MINB 4
+#endif
+
 // ============================================================ samplers (C-4) on a share
 // CBD samples of the coefficients x = S i + r (the forward split's subsequence), at i.
 template <int THREADS>
@@ -103,7 +109,7 @@ struct ZincNttOut {
 // c1' = zero1 + NTT(m + e1'), c2' = zero2 + NTT(e2'): both transforms through one copy of
 // the transform code (t at run time); the exchange streams cache-added words to HBM.
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(256, 3) zinc_ntt_split_kernel(ZincNttArgs a) {
+__global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(ZincNttArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
   using G = SplitGeo<LOGN>;
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
@@ -179,7 +185,7 @@ struct VanTLoad {
 };
 
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a) {
+__global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel(VanillaArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
   using G = SplitGeo<LOGN>;
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_ntt_split_kernel(VanillaArgs a
 // temporary); INTT(pk1 u^) + e1 + m -> ct0; INTT(ct1) + e2 -> ct1.  The forward output
 // range of a CTA is its inverse input range: no data moves between CTAs in between.
 template <int LOGN, int MODE>
-__global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs a) {
+__global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kernel(VanillaArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
   using G = SplitGeo<LOGN>;
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
@@ -334,7 +340,7 @@ __global__ void __launch_bounds__(256, 3) vanilla_coeff_split_kernel(VanillaArgs
 // c1 + c2 s read from global memory.  Each output position is handled by the same thread
 // in every limb, so the CRT check re-reads only words the thread wrote itself.
 template <int LOGN, int FORM, bool NR, bool PLAIN = false>
-__global__ void __launch_bounds__(256, 3) decrypt_split_kernel(DecryptArgs a) {
+__global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) decrypt_split_kernel(DecryptArgs a) {
   using G = SplitGeo<LOGN>;
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL;
   extern __shared__ __align__(16) uint64_t sm[];
