@@ -79,7 +79,7 @@ ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, i
 template <int LOGN> struct SplitSmem {
   using G = SplitGeo<LOGN>;
   static constexpr size_t DATA = SmemWords<G::LL>::value * sizeof(uint64_t);  // 34816
-  static constexpr size_t TW = G::STW * sizeof(Tw);                          // 4096
+  static constexpr size_t TW = SPLIT_STW ? G::STW * sizeof(Tw) : 0;          // 4096
 };
 
 // ============================================================ Zinc, NTT form
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
   extern __shared__ __align__(16) uint64_t sm[];
   Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
-  int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
+  int8_t *se1 = reinterpret_cast<int8_t *>(stw + (SPLIT_STW ? G::STW : 0)), *se2 = se1 + NL;
   __shared__ __align__(8) uint64_t tw_mbar, cl_mbar[2];
   TwStager tws{&tw_mbar, 0};
   ClusterBar cb{cl_mbar, 0};
@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
   const int L = a.L;
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
-  tws.init();
+  if constexpr (SPLIT_STW) tws.init();
   cb.init<S>();
-  tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
+  if constexpr (SPLIT_STW) tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   // small batches spread the two transforms over gridDim.z = 2 (t = blockIdx.z)
   const int t_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, t_hi = gridDim.z > 1 ? t_lo + 1 : 2;
   if (t_lo == 0) sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
@@ -142,14 +142,14 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
     const uint64_t q = c.q;
     const Tw *tw = a.tw + (size_t)i * N;
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
-    tws.wait();
+    if constexpr (SPLIT_STW) tws.wait();
 #pragma unroll 1
     for (int t = t_lo; t < t_hi; ++t) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
       ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoadU<INTS, G::LOGS>{{m, t ? se2 : se1, c, t}, all_small},
           ZincNttOut<S>{z, ctt, c}, stw, [&]() {
-            if (t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
+            if (SPLIT_STW && t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
           });
     }
   }
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
   extern __shared__ __align__(16) uint64_t sm[];
   Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
-  int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
+  int8_t *se1 = reinterpret_cast<int8_t *>(stw + (SPLIT_STW ? G::STW : 0)), *se2 = se1 + NL;
   uint8_t *su = reinterpret_cast<uint8_t *>(se2 + NL);
   __shared__ __align__(8) uint64_t tw_mbar, cl_mbar[2];
   TwStager tws{&tw_mbar, 0};
@@ -202,9 +202,9 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
   const int L = a.L;
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
-  tws.init();
+  if constexpr (SPLIT_STW) tws.init();
   cb.init<S>();
-  tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
+  if constexpr (SPLIT_STW) tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   // small batches spread the three transforms over gridDim.z = 3 (t = blockIdx.z; the u
   // transform then writes u^ to a.u_hat and vanilla_combine_kernel forms pk u^)
   const int t_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, t_hi = gridDim.z > 1 ? t_lo + 1 : 3;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
-    tws.wait();
+    if constexpr (SPLIT_STW) tws.wait();
 #pragma unroll 1
     for (int t = t_lo; t < t_hi; ++t) {
       ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t, all_small || t > 0},
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
             }
           },
           stw, [&]() {
-            if (t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
+            if (SPLIT_STW && t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
           });
     }
   }
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
   constexpr int N = 1 << LOGN, S = G::S, NL = G::NL, THREADS = G::THREADS;
   extern __shared__ __align__(16) uint64_t sm[];
   Tw *stw = reinterpret_cast<Tw *>(sm + SmemWords<G::LL>::value);
-  int8_t *se1 = reinterpret_cast<int8_t *>(stw + G::STW), *se2 = se1 + NL;
+  int8_t *se1 = reinterpret_cast<int8_t *>(stw + (SPLIT_STW ? G::STW : 0)), *se2 = se1 + NL;
   uint8_t *su = reinterpret_cast<uint8_t *>(se2 + NL);
   __shared__ __align__(8) uint64_t tw_mbar, cl_mbar[2];
   TwStager tws{&tw_mbar, 0};
@@ -278,9 +278,9 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
   const int L = a.L;
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
-  tws.init();
+  if constexpr (SPLIT_STW) tws.init();
   cb.init<S>();
-  tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
+  if constexpr (SPLIT_STW) tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
   sample_cbd_inv<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
   sample_cbd_inv<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
     uint64_t *ct0 = a.ct + b * 2 * L * N + (size_t)i * N;
     uint64_t *ct1 = ct0 + (size_t)L * N;
     auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
-    tws.wait();
+    if constexpr (SPLIT_STW) tws.wait();
     ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> G::LOGS), q); },
         [&](int x0, uint64_t (&v)[S]) {
 #pragma unroll
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
           }
         },
         stw, [&]() {
-          if (i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
+          if (SPLIT_STW && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);
         });
     ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {},
         with_pre1(

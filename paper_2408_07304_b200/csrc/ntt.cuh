@@ -550,6 +550,13 @@ ZINC_DEV void loads_done(uint64_t acc) {
   asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sink)), "l"(acc) : "memory");
 }
 
+// Passes A, B of the split forward read W[0, 256) from a TMA-staged shared copy (1) or through
+// L1 (0; measured 2.6 % slower for the Zinc NTT form at C3, 1 % faster for decryption).
+#ifndef ZINC_SPLIT_STW
+#define ZINC_SPLIT_STW 1
+#endif
+constexpr bool SPLIT_STW = ZINC_SPLIT_STW;
+
 template <int LOGN> struct SplitGeo {
   static constexpr int LL = 12, NL = 1 << LL, S = 1 << (LOGN - LL), LOGS = LOGN - LL;
   static constexpr int THREADS = Plan<LL>::THREADS;   // 256
@@ -623,7 +630,8 @@ template <class O, class V, class P> ZINC_DEV void out_call(O &o, int x0, V &v, 
 // otherwise).  With LOAD_ALL the exchange first reads all of the CTA's inputs into
 // registers and passes a cluster barrier before any `out` call, so `out` may write this
 // CTA's shared memory (the inverse input of a following ntt_inverse_split).
-// stw: shared copy of W[0, SplitGeo::STW); after_b() runs once pass B no longer reads it.
+// stw: shared copy of W[0, SplitGeo::STW); after_b() runs once every thread of the CTA is past
+// pass C (at the data-ready rendezvous, a CTA barrier), so it may restage stw.
 template <int LOGN, bool NR, bool LOAD_ALL = false, class Load, class Out, class AfterB = NoHook>
 ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint64_t q, Load load, Out out,
                                 const Tw *stw, AfterB after_b = AfterB()) {
@@ -649,7 +657,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
         ZINC_DEV bool uniform_small() const { return l.uniform_small(); }
         ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, S * i + r); }
       };
-      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst, settle);
+      ct_pass<LL, 0, P::KA, THREADS, false, SPLIT_STW, NR>(SPLIT_STW ? stw : tw, q, 1, Sub{load, r}, sst, settle);
     } else if constexpr (HasSmallLift<Load>::value) {
       struct Sub {  // local index i -> coefficient S i + r
         const Load &l;
@@ -659,7 +667,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
         ZINC_DEV bool small(int64_t raw) const { return l.small(raw); }
         ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, S * i + r); }
       };
-      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst, settle);
+      ct_pass<LL, 0, P::KA, THREADS, false, SPLIT_STW, NR>(SPLIT_STW ? stw : tw, q, 1, Sub{load, r}, sst, settle);
     } else {
       struct Sub {  // local index i -> coefficient S i + r
         const Load &l;
@@ -667,15 +675,19 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
         ZINC_DEV int64_t fetch(int i) const { return l.fetch(S * i + r); }
         ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, S * i + r); }
       };
-      ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, Sub{load, r}, sst, settle);
+      ct_pass<LL, 0, P::KA, THREADS, false, SPLIT_STW, NR>(SPLIT_STW ? stw : tw, q, 1, Sub{load, r}, sst, settle);
     }
   } else {
-    ct_pass<LL, 0, P::KA, THREADS, false, true, NR>(stw, q, 1, [&](int i) { return load(S * i + r); }, sst, settle);
+    ct_pass<LL, 0, P::KA, THREADS, false, SPLIT_STW, NR>(SPLIT_STW ? stw : tw, q, 1, [&](int i) { return load(S * i + r); }, sst, settle);
   }
   __syncthreads();
-  ct_pass<LL, SB, P::KB, THREADS, false, true, NR>(stw, q, 1, sld, sst);
-  __syncthreads();
-  after_b();
+  ct_pass<LL, SB, P::KB, THREADS, false, SPLIT_STW, NR>(SPLIT_STW ? stw : tw, q, 1, sld, sst);
+  // Pass B's groups of thread g lie in the 256-word block g / 16 and pass C's in [16 g, 16 g + 16):
+  // both passes of warp w touch exactly the words [512 w, 512 w + 512), so a warp hands pass B's
+  // output to its own pass C with a warp barrier instead of a CTA barrier, and the warps of a CTA
+  // run passes B, C and the exchange prologue out of step with one another.
+  static_assert(THREADS == 256 && P::KB == 4 && P::KC == 4 && SB == 4, "warp-local passes B, C");
+  __syncwarp();
   ct_pass<LL, SC, P::KC, THREADS, true, false, NR>(tw, q, 1, sld, [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) sm[pad16(base + j)] = v[j];
@@ -685,7 +697,9 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
   for (int c = 0; c < S; ++c) peer[c] = dsmem_addr(sm, (uint32_t)c);
   const int k0 = r * (G::NL / S) + threadIdx.x;
   if constexpr (LOAD_ALL) {
-    cb.sync_raw<S>();  // every CTA's sub-transform complete
+    cb.raw_arrive<S>();  // every CTA's sub-transform complete
+    after_b();
+    cb.wait();
     uint64_t v[G::KPT][S];
 #pragma unroll
     for (int u = 0; u < G::KPT; ++u)
@@ -713,6 +727,7 @@ ZINC_DEV void ntt_forward_split(uint64_t *sm, ClusterBar &cb, const Tw *tw, uint
     constexpr bool DB = S <= 4;  // double-buffered registers (k and k + 1) fit at S = 4
     using PreT = decltype(out_pre(out, 0));
     cb.raw_arrive<S>();  // every CTA's sub-transform complete (wait below)
+    after_b();
     Tw wc[S1];
     PreT pc;
     split_fwd_tw<LOGN>(wc, k0, tw);
@@ -818,7 +833,7 @@ ZINC_DEV void ntt_inverse_split(uint64_t *sm, ClusterBar &cb, const Tw *itw, con
   } else {
     gs_pass<LL, SC, P::KC, THREADS>(itw, c, tb, sld, sst);
   }
-  __syncthreads();
+  __syncwarp();  // the first two passes of warp w touch only words [512 w, 512 w + 512) (forward)
   gs_pass<LL, SB, P::KB, THREADS>(itw, c, tb, sld, sst);
   __syncthreads();
   gs_pass<LL, 0, P::KA, THREADS, false, false>(itw, c, tb, sld, sst);
