@@ -277,10 +277,14 @@ void zinc_launch_count_reset(void);
  *  ZINC_TUNE_SMALL_ENCODE         real-slot encode of fewer messages than SMs: 0 (default) the throughput
  *                                 kernel (256 threads, radix-16: 15 us per message at N = 2^14, measured
  *                                 fastest), 1 512 threads radix-8 (18 us), 2 1024 threads radix-4 (21 us)
+ *  ZINC_TUNE_PT_IN_CT             Zinc COEFF form from slots: stage each encoded plaintext in its own
+ *                                 ciphertext's last c2 limb (no scratch; encodes need not wait for the
+ *                                 previous add/inject) instead of double-buffered scratch: 2 always,
+ *                                 1 (default) for a single chunk and for L <= 4, 0 never
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_PDL = 2,
        ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_SPLIT = 5, ZINC_TUNE_SMALL_ENCODE = 6,
-       ZINC_TUNE_COUNT = 7 };
+       ZINC_TUNE_PT_IN_CT = 7, ZINC_TUNE_COUNT = 8 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

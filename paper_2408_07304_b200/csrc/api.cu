@@ -110,7 +110,7 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -536,9 +536,11 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
 }
 
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
-                               cudaStream_t s, bool wide = false) {
+                               cudaStream_t s, bool wide = false, size_t m_stride = 0, int wait_mode = 0) {
   EncodeArgs a = encode_args(c, kind, slots, m);
   a.wide = wide ? 1 : 0;
+  a.m_stride = m_stride ? m_stride : (size_t)c->n * (wide ? 2 : 1);
+  a.wait_mode = wait_mode;
   // few messages: a latency variant with more threads per message (knob ZINC_TUNE_SMALL_ENCODE)
   a.fast = batch < (size_t)c->num_sms ? (int)g_tune[ZINC_TUNE_SMALL_ENCODE].load() : 0;
   LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
@@ -569,6 +571,7 @@ static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, c
   a.n = c->n;
   a.L = c->L;
   a.qmin = c->qmin;
+  a.m_stride = (size_t)c->n;
   // messages per CTA (tuning knob): grid = coefficient tiles x message groups
   // 0 (default): 8 messages per CTA when the cache tile is small (L <= 4: amortises the tile
   // staging over more stores; C2 +7 %), else 2 (measured, profiles/r02_zinc_coeff_sweep.txt)
@@ -594,10 +597,11 @@ static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
 }
 static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, int form, const int64_t *m,
                             size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s,
-                            bool m_is_scratch = false) {
+                            bool m_is_scratch = false, size_t m_stride = 0) {
   if (path == PATH_ZINC && form == ZINC_FORM_COEFF) {
     ZincCoeffArgs a = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
     a.discard_m = m_is_scratch ? 1 : 0;
+    if (m_stride) a.m_stride = m_stride;
     a.prefetch = (const char *)g_l2_prefetch.p;
     a.prefetch_bytes = g_l2_prefetch.bytes & ~(size_t)15;
     int threads = 256;
@@ -765,21 +769,33 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
   chunk = std::max<size_t>(1, std::min(batch, chunk));
   const bool pdl = g_tune[ZINC_TUNE_PDL].load() != 0;
   const int nb = batch > chunk ? 2 : 1;
-  ScratchBuf mbuf(s);
-  CUDA_TRY(mbuf.alloc(nb * chunk * per_msg));
-  int64_t *m = mbuf.as<int64_t>();
   const size_t in_stride = pt_stride_bytes(c, kind);
   const size_t ct_stride = (size_t)2 * c->L * c->n;
+  // Zinc COEFF form: each message's encoded plaintext goes into its own ciphertext's last c2
+  // limb (N words of the 2 L N it will write).  The add/inject thread that owns coefficients
+  // j, j + 1 reads m[j], m[j + 1] there before it overwrites those words, and no other kernel
+  // touches the slab in between: no scratch allocation, no buffer reuse between chunks, so an
+  // encode's plaintext stores need not wait for the previous add/inject (wait_mode 1), and the
+  // overwritten lines are written back once, as ciphertext.
+  // Knob 1 (auto) takes it for a single chunk (the small-batch latency path: no scratch
+  // allocation, 2.3 us of host time) and at L <= 4 (C2: +1.8 %); measured even at C4 and 0.5 %
+  // behind the scratch chain at C3 (profiles/r02b_pt_in_ct_ab.txt).
+  const long long pic = g_tune[ZINC_TUNE_PT_IN_CT].load();
+  const bool in_ct = coeff_zinc && (pic == 2 || (pic == 1 && (batch <= chunk || c->L <= 4)));
+  ScratchBuf mbuf(s);
+  if (!in_ct) CUDA_TRY(mbuf.alloc(nb * chunk * per_msg));
+  int64_t *m = mbuf.as<int64_t>();
   zinc_status st = ZINC_OK;
   size_t k = 0;
   for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
     const size_t cnt = std::min(chunk, batch - off);
-    int64_t *mb = m + (size_t)(k % nb) * chunk * c->n;
+    int64_t *mb = in_ct ? (int64_t *)(ct + off * ct_stride + (ct_stride - c->n)) : m + (size_t)(k % nb) * chunk * c->n;
+    const size_t mstride = in_ct ? ct_stride : (size_t)c->n;
     {
       // the first launch keeps a full dependency on whatever produced the inputs (its
       // loads precede its griddepcontrol.wait); later ones chain on this pipeline's kernels
       PdlScope pdl_scope(pdl && k > 0);
-      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s);
+      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s, false, mstride, in_ct ? 1 : 0);
     }
     PdlScope pdl_scope(pdl);
     // the Zinc COEFF kernel of this chunk warms the next chunk's slots into L2 for its encode
@@ -787,7 +803,8 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
     const bool pf = coeff_zinc && g_tune[ZINC_TUNE_L2_PREFETCH].load() != 0 && nxt > 0 && aligned16(pt) &&
                     in_stride % 16 == 0;
     g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + chunk) * in_stride, nxt * in_stride} : L2Prefetch{};
-    if (st == ZINC_OK) st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, true);
+    if (st == ZINC_OK)
+      st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, !in_ct, mstride);
     g_l2_prefetch = L2Prefetch{};
   }
   return st;

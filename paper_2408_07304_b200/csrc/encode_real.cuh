@@ -163,8 +163,9 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
   // this encode overwrites: the loads and the FFT above overlapped it, the stores wait.
   pdl_trigger();
-  pdl_wait();
-  encode_real_post<LOGM, WIDE, THREADS>(a, a.m_out + b * (2 * M) * (WIDE ? 2 : 1), buf, sptw);
+  if (a.wait_mode == 0) pdl_wait();
+  encode_real_post<LOGM, WIDE, THREADS>(a, a.m_out + b * a.m_stride, buf, sptw);
+  if (a.wait_mode == 1) pdl_wait();  // completion still implies the previous kernel's (stream order)
 }
 
 }  // namespace zinc

@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
   // this encode overwrites: the loads and the first passes overlapped it, the stores wait.
   pdl_trigger();
-  pdl_wait();
-  int64_t *m = a.m_out + b * (2 * M) * (a.wide ? 2 : 1);
+  if (a.wait_mode == 0) pdl_wait();
+  int64_t *m = a.m_out + b * a.m_stride;
   const double scale = a.scale;  // Delta / M, a power of two
   // twist zeta^-j from two small L1-resident tables instead of 16 B of L2 table per output
   const double2 *tA = a.twist_split, *tB = a.twist_split + M / 64;
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
     }
     cluster_sync_all();
   }
+  if (a.wait_mode == 1) pdl_wait();  // completion still implies the previous kernel's (stream order)
 }
 
 // ============================================================ encode, real slots

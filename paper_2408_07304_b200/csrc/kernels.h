@@ -42,6 +42,8 @@ struct ZincCoeffArgs {
   const int64_t *m128;    // CKKS 128-bit plaintexts (int64 pairs [batch][N][2]); overrides m
   const char *prefetch;   // the next chunk's slots: warmed into L2 while this chunk streams
   size_t prefetch_bytes;  // (16-byte multiple; 0: none)
+  size_t m_stride;        // int64 words between messages' plaintexts in m (N, or 2 L N when the
+                          // plaintexts sit in the ciphertexts' last c2 limb, see encrypt_any)
 };
 struct VanillaArgs {
   const LimbConst *limbs;
@@ -118,6 +120,9 @@ struct EncodeArgs {
   int fast;                 // real slots, batch below the SM count: the latency variant (more threads)
   double scale;
   int64_t *m_out;
+  size_t m_stride;          // int64 words between messages' plaintexts in m_out (N; 2N when wide)
+  int wait_mode;            // PDL: 0 wait for the previous kernel before the plaintext stores,
+                            // 1 after them (the stores go to a region no earlier kernel touches)
 };
 struct DecodeArgs {
   const int64_t *coeff;     // int64 [B][N], or int64 pairs [B][N][2] when wide

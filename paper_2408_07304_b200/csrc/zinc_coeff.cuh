@@ -89,7 +89,7 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   pdl_wait();
   // first message's plaintext words, fetched while the tile is in flight
   ulonglong2 mv = make_ulonglong2(0, 0);
-  if (a.m && b_begin < b_end) mv = ld2_nc(a.m + b_begin * a.n + j);
+  if (a.m && b_begin < b_end) mv = ld2_nc(a.m + b_begin * a.m_stride + j);
   {
     uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
     uint32_t done = 0;
@@ -152,7 +152,7 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
   for (size_t b = b_begin; b < b_end; ++b) {
     const uint64_t msg = a.msg_base + b;
     const int64_t m0 = (int64_t)mv.x, m1 = (int64_t)mv.y;
-    if (a.m && b + 1 < b_end) mv = ld2_nc(a.m + (b + 1) * a.n + j);  // prefetch
+    if (a.m && b + 1 < b_end) mv = ld2_nc(a.m + (b + 1) * a.m_stride + j);  // prefetch
     const uint4 w1 = stream_block(a.seed, msg, TAG_ZINC_E1, 0, (uint32_t)(j >> 1));
     const uint4 w2 = stream_block(a.seed, msg, TAG_ZINC_E2, 0, (uint32_t)(j >> 1));
     const int e0 = cbd_lo(w1), e1 = cbd_hi(w1);
@@ -176,7 +176,7 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
       // the library's own encode scratch is dead once read (the stores above consumed it):
       // drop its L2 lines without a write-back.  Lanes 8r..8r+7 share a 128-byte line.
       if (a.discard_m && (threadIdx.x & 7) == 0)
-        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.n + j) : "memory");
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.m_stride + j) : "memory");
       continue;
     }
     // CKKS: v = m + e1' (|m| < 2^62 rules out int64 overflow); BGV (Eq. 13): v = (m mod t) +
@@ -222,7 +222,7 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
     // the library's own encode scratch is dead once read (the stores above consumed it):
     // drop its L2 lines without a write-back.  Lanes 8r..8r+7 share a 128-byte line.
     if (a.discard_m && (threadIdx.x & 7) == 0)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.n + j) : "memory");
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a.m + b * a.m_stride + j) : "memory");
   }
 }
 

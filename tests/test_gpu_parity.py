@@ -397,6 +397,8 @@ def test_int_peak_kernel_runs(Z, orc, variant):
     {4: 7},                                   # transform paths: 7-message chunks, PDL chain
     {4: 5, 2: 0},                             # transform paths: 5-message chunks, stream order
     {4: 1},                                   # one message per chunk
+    {7: 0},                                   # Zinc COEFF plaintexts in double-buffered scratch
+    {7: 2, 1: 1 << 20},                       # ... in the ciphertext slab, over 9 chunks
 ])
 def test_tuning_knobs_never_change_results(Z, orc, knobs):
     """Launch geometry (messages per CTA, encode chunk sizes, programmatic dependent launch,
