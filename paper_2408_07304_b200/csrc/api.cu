@@ -595,9 +595,20 @@ static int limbs_per_cta(const zinc_ctx *c, size_t batch) {
   int groups = (int)std::min<size_t>((size_t)c->L, (want + batch - 1) / batch);
   return (c->L + groups - 1) / groups;
 }
+// The vanilla NTT form's transform-split small-batch launch (its three transforms on separate
+// CTAs, u^ through scratch, then vanilla_combine_kernel): when a handful of messages would leave
+// SMs idle.
+static bool vanilla_t_split(const zinc_ctx *c, int form, size_t batch) {
+  const int lpc = limbs_per_cta(c, batch);
+  const int groups = (c->L + lpc - 1) / lpc;
+  return c->log_n >= 14 && g_tune[ZINC_TUNE_SPLIT].load() != 0 && form == ZINC_FORM_NTT &&
+         batch * (size_t)groups * 3 * ((size_t)c->n >> 12) <= 2 * (size_t)c->num_sms;
+}
+// uhat_scratch: room for batch x L x N words the caller allocated with its own scratch (one pool
+// allocation per call on the small-batch path instead of two); null: allocate here.
 static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, int form, const int64_t *m,
                             size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s,
-                            bool m_is_scratch = false, size_t m_stride = 0) {
+                            bool m_is_scratch = false, size_t m_stride = 0, uint64_t *uhat_scratch = nullptr) {
   if (path == PATH_ZINC && form == ZINC_FORM_COEFF) {
     ZincCoeffArgs a = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
     a.discard_m = m_is_scratch ? 1 : 0;
@@ -645,12 +656,11 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.L = c->L;
   a.limbs_per_cta = lpc;
   // a handful of messages (NTT form): the three transforms on separate CTAs, then a combine
-  const bool t_split = c->log_n >= 14 && g_tune[ZINC_TUNE_SPLIT].load() != 0 && form == ZINC_FORM_NTT &&
-                       batch * (size_t)groups * 3 * ((size_t)c->n >> 12) <= 2 * (size_t)c->num_sms;
+  const bool t_split = vanilla_t_split(c, form, batch);
   ScratchBuf uhat(s), pk_sh(s);
   if (t_split) {
-    CUDA_TRY(uhat.alloc(batch * (size_t)c->L * c->n * 8));
-    a.u_hat = uhat.as<uint64_t>();
+    if (!uhat_scratch) CUDA_TRY(uhat.alloc(batch * (size_t)c->L * c->n * 8));
+    a.u_hat = uhat_scratch ? uhat_scratch : uhat.as<uint64_t>();
   } else {
     // Shoup companions of pk: the per-message pointwise products pk u^ become Shoup products
     // (the transform-split launch's combine kernel uses Barrett products instead)
@@ -783,8 +793,12 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
   const long long pic = g_tune[ZINC_TUNE_PT_IN_CT].load();
   const bool in_ct = coeff_zinc && (pic == 2 || (pic == 1 && (batch <= chunk || c->L <= 4)));
   ScratchBuf mbuf(s);
-  if (!in_ct) CUDA_TRY(mbuf.alloc(nb * chunk * per_msg));
+  // a single-chunk vanilla NTT call on the transform-split path gets its u^ scratch here too
+  const bool uh = !coeff_zinc && path == PATH_VANILLA && batch <= chunk && vanilla_t_split(c, form, batch);
+  const size_t uh_words = uh ? batch * (size_t)c->L * c->n : 0;
+  if (!in_ct) CUDA_TRY(mbuf.alloc(nb * chunk * per_msg + uh_words * 8));
   int64_t *m = mbuf.as<int64_t>();
+  uint64_t *uhat_scratch = uh ? reinterpret_cast<uint64_t *>(m + nb * chunk * c->n) : nullptr;
   zinc_status st = ZINC_OK;
   size_t k = 0;
   for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
@@ -804,7 +818,8 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
                     in_stride % 16 == 0;
     g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + chunk) * in_stride, nxt * in_stride} : L2Prefetch{};
     if (st == ZINC_OK)
-      st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, !in_ct, mstride);
+      st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, !in_ct, mstride,
+                    uhat_scratch);
     g_l2_prefetch = L2Prefetch{};
   }
   return st;
