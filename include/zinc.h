@@ -281,10 +281,14 @@ void zinc_launch_count_reset(void);
  *                                 ciphertext's last c2 limb (no scratch; encodes need not wait for the
  *                                 previous add/inject) instead of double-buffered scratch: 2 always,
  *                                 1 (default) for a single chunk and for L <= 4, 0 never
+ *  ZINC_TUNE_SMALL_CLUSTER        real slots, at most (SMs / 8) messages: 1 (default) each message's
+ *                                 encode runs on an 8-CTA cluster, and Zinc COEFF form fuses the
+ *                                 add/inject into the same launch (k_small.cu); 0: the throughput
+ *                                 kernels (one CTA per message's encode, then the path kernel)
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_PDL = 2,
        ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_SPLIT = 5, ZINC_TUNE_SMALL_ENCODE = 6,
-       ZINC_TUNE_PT_IN_CT = 7, ZINC_TUNE_COUNT = 8 };
+       ZINC_TUNE_PT_IN_CT = 7, ZINC_TUNE_SMALL_CLUSTER = 8, ZINC_TUNE_COUNT = 9 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

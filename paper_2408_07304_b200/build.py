@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.environ.get("ZINC_BUILD_OUT", os.path.join(HERE, "libzinc.so"))
 OBJDIR = os.environ.get("ZINC_BUILD_DIR", os.path.join(HERE, "build"))
-SOURCES = ["api.cu", "k_stream.cu", "k_vanilla.cu", "k_ntt.cu", "k_fft.cu", "k_split.cu"]
+SOURCES = ["api.cu", "k_stream.cu", "k_vanilla.cu", "k_ntt.cu", "k_fft.cu", "k_split.cu", "k_small.cu"]
 HEADERS = ["common.cuh", "ntt.cuh", "fft.cuh", "kernels.h", "kcommon.cuh", "zinc_coeff.cuh", "encode_real.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -110,7 +110,7 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}, {1}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}, {1}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -535,6 +535,13 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
   return a;
 }
 
+// The small-batch latency path (k_small.cu): real slots, few enough messages that one 8-CTA
+// cluster per message still leaves SMs over (knob ZINC_TUNE_SMALL_CLUSTER).
+static bool small_cluster(const zinc_ctx *c, int kind, size_t batch) {
+  return kind == ZINC_PT_SLOTS_F64 && g_tune[ZINC_TUNE_SMALL_CLUSTER].load() != 0 &&
+         batch * (size_t)small_cluster_ctas() <= (size_t)c->num_sms;
+}
+
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
                                cudaStream_t s, bool wide = false, size_t m_stride = 0, int wait_mode = 0) {
   EncodeArgs a = encode_args(c, kind, slots, m);
@@ -543,7 +550,10 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
   a.wait_mode = wait_mode;
   // few messages: a latency variant with more threads per message (knob ZINC_TUNE_SMALL_ENCODE)
   a.fast = batch < (size_t)c->num_sms ? (int)g_tune[ZINC_TUNE_SMALL_ENCODE].load() : 0;
-  LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
+  if (small_cluster(c, kind, batch) && !wide)
+    LAUNCH(ZINC_K_ENCODE, s, launch_encode_cluster(c->log_n, a, batch, s));
+  else
+    LAUNCH(ZINC_K_ENCODE, s, launch_encode(c->log_n, a, batch, s));
   return ZINC_OK;
 }
 
@@ -760,6 +770,19 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
   if (kind == ZINC_PT_COEFF_I128 || c->wide) return encrypt_wide(c, path, key, form, kind, pt, batch, seed, msg_base, ct, s);
   const size_t per_msg = (size_t)c->n * 8;
   const bool coeff_zinc = path == PATH_ZINC && form == ZINC_FORM_COEFF;
+  if (coeff_zinc && c->scheme == ZINC_SCHEME_CKKS && small_cluster(c, kind, batch)) {
+    // a handful of messages: encode and add/inject in one launch; R cluster replicas per
+    // message (each encodes, then streams PP of the 2L ciphertext polynomials) fill the SMs
+    const int polys = 2 * c->L;
+    int R = (int)std::max<size_t>(1, 2 * (size_t)c->num_sms / (batch * (size_t)small_cluster_ctas()));
+    R = std::min(R, polys);
+    const int PP = (polys + R - 1) / R;
+    R = (polys + PP - 1) / PP;
+    const EncodeArgs e = encode_args(c, kind, pt, nullptr);
+    const ZincCoeffArgs z = zinc_coeff_args(c, key, nullptr, batch, seed, msg_base, ct);
+    LAUNCH(ZINC_K_ZINC_COEFF, s, launch_zinc_coeff_small(c->log_n, e, z, batch, R, PP, s));
+    return ZINC_OK;
+  }
   size_t chunk;
   if (coeff_zinc) {
     const size_t chunk_bytes = (size_t)std::max<long long>(per_msg, g_tune[ZINC_TUNE_ENCODE_CHUNK_BYTES].load());

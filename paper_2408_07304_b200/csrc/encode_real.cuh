@@ -34,10 +34,27 @@ ZINC_DEV uint32_t pow5_mod_pow2(uint32_t e, uint32_t mask) {
 // c = zeta^-H = e^{-i pi / 4} (H = N/4).  t_j and p_j come from two split tables each
 // (j = 64 a + b: t_j = A[a] B[b], p_j = A5[a] B5[b]; `ptw` = [A | B | A5 | B5], H/64 + 64
 // entries per pair, 4 KiB at N = 2^14) instead of 48 bytes of L2-resident tables per j.
+// One output index j of the split step: y0, y1 from X_j, X_{H-j} (unconjugated) and the four
+// table entries A[j/64], B[j%64], A5[j/64], B5[j%64].  Shared by encode_real_post and the
+// cluster encode (k_small.cu), so both round the same doubles.
+ZINC_DEV void encode_post_y(double2 xj, double2 xh, double2 ta, double2 tb, double2 t5a, double2 t5b, double2 &y0,
+                            double2 &y1) {
+  constexpr double R = 0.70710678118654752440;  // c = R (1 - i)
+  const double2 t = cmul(ta, tb);
+  const double2 pj = cmul(t5a, t5b);
+  const double2 xr = conj2(xh);
+  const double2 e = make_double2(0.5 * (xj.x + xr.x), 0.5 * (xj.y + xr.y));
+  const double2 d = make_double2(0.5 * (xj.x - xr.x), 0.5 * (xj.y - xr.y));
+  const double2 o = make_double2(d.y, -d.x);  // -i d
+  const double2 U = cmul(e, t), W = cmul(o, pj);
+  y0 = cadd(U, W);
+  const double2 df = csubd(U, W);
+  y1 = make_double2(R * (df.x + df.y), R * (df.y - df.x));
+}
+
 template <int LOGM, bool WIDE, int THREADS = 256, bool PT_SMEM = true>
 ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *buf, const double2 *ptw) {
   constexpr int M = 1 << LOGM, H = M / 2, NA = H / 64;
-  constexpr double R = 0.70710678118654752440;  // c = R (1 - i)
   const double2 *tA = ptw, *tB = ptw + NA, *tA5 = tB + 64, *tB5 = tA5 + NA;
   auto ld = [](const double2 *p) { return PT_SMEM ? *p : __ldg(p); };
   const int tid = threadIdx.x;
@@ -49,15 +66,9 @@ ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *b
 #pragma unroll
     for (int u = 0; u < V; ++u) {
       const int j = j0 + u * THREADS;
-      const double2 t = cmul(ld(tA + (j >> 6)), ld(tB + (j & 63)));
-      const double2 pj = cmul(ld(tA5 + (j >> 6)), ld(tB5 + (j & 63)));
-      const double2 xj = buf[pad16(j)], xr = conj2(buf[pad16((H - j) & (H - 1))]);
-      const double2 e = make_double2(0.5 * (xj.x + xr.x), 0.5 * (xj.y + xr.y));
-      const double2 d = make_double2(0.5 * (xj.x - xr.x), 0.5 * (xj.y - xr.y));
-      const double2 o = make_double2(d.y, -d.x);  // -i d
-      const double2 U = cmul(e, t), W = cmul(o, pj);
-      const double2 y0 = cadd(U, W), df = csubd(U, W);
-      const double2 y1 = make_double2(R * (df.x + df.y), R * (df.y - df.x));
+      double2 y0, y1;
+      encode_post_y(buf[pad16(j)], buf[pad16((H - j) & (H - 1))], ld(tA + (j >> 6)), ld(tB + (j & 63)),
+                    ld(tA5 + (j >> 6)), ld(tB5 + (j & 63)), y0, y1);
       if constexpr (WIDE) {  // 128-bit coefficients (f3: Delta = 2^55 and large slots)
         store_i128(m + 2 * j, y0.x * scale);
         store_i128(m + 2 * (j + M), y0.y * scale);

@@ -183,6 +183,13 @@ cudaError_t launch_encode(int log_n, const EncodeArgs &a, size_t batch, cudaStre
 // messages per full wave of the encode kernel (0 if unknown)
 size_t encode_wave_msgs(int log_n, bool complex_slots, int num_sms);
 cudaError_t launch_decode(int log_n, const DecodeArgs &a, size_t batch, cudaStream_t s);
+// small-batch latency path (k_small.cu): real-slot encode of one message per C-CTA cluster
+// (C = small_cluster_ctas()), alone (plaintexts to a.m_out) or fused with the COEFF-form Zinc
+// add/inject (R cluster replicas per message, PP ciphertext polynomials per replica)
+int small_cluster_ctas();
+cudaError_t launch_encode_cluster(int log_n, const EncodeArgs &a, size_t batch, cudaStream_t s);
+cudaError_t launch_zinc_coeff_small(int log_n, const EncodeArgs &e, const ZincCoeffArgs &z, size_t batch, int R,
+                                    int PP, cudaStream_t s);
 cudaError_t launch_ntt(int log_n, const NttArgs &a, int inv, size_t polys, cudaStream_t s);
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t s);
 cudaError_t launch_ct_add(const CtAddArgs &a, cudaStream_t s);

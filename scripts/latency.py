@@ -20,6 +20,8 @@ cache = {f: Z.zinc_precompute_cache(ctx, pk, cfg.cache_seed, f) for f in (Z.COEF
 out = {}
 if os.environ.get("ZINC_SMALL_ENCODE") is not None:
     Z.tune(Z.TUNE_SMALL_ENCODE, int(os.environ["ZINC_SMALL_ENCODE"]))
+if os.environ.get("ZINC_SMALL_CLUSTER") is not None:
+    Z.tune(Z.TUNE_SMALL_CLUSTER, int(os.environ["ZINC_SMALL_CLUSTER"]))
 for B in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,16").split(",")]:
     z = torch.from_numpy(np.ascontiguousarray(slots_batch(cfg, 0, B))).cuda()
     ct = ctx.empty_ct(B)

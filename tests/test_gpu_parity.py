@@ -505,3 +505,45 @@ def test_ct_add_and_sum_bit_exact_and_decrypt(Z, orc, name):
     _, st, zz = Z.ckks_decrypt_batch(s.ctx, s.sk, COEFF, tot[None].contiguous())
     assert int(st.sum()) == 0
     assert np.max(np.abs(zz[0].cpu().numpy() - z.sum(axis=0))) < k * cfg.tolerance()
+
+
+def _setup_real15(Z, orc):
+    """N = 2^15 with C4's primes but real slots (C4 itself has complex slots): the cluster
+    encode's N = 2^15 instantiation."""
+    from workloads import _cfg
+    if "C4r" not in _setups:
+        _setups["C4r"] = Setup(Z, orc, _cfg("C4r", 14, 15, [55] * 16, 40, 64, "uniform"))
+    return _setups["C4r"]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4r"])
+def test_small_cluster_path_bit_identical(Z, orc, name):
+    """The small-batch latency path (k_small.cu): one message's encode over an 8-CTA cluster,
+    and the Zinc COEFF form fused into the same launch with R cluster replicas per message.
+    Plaintexts and ciphertexts are bit-identical to the throughput kernels (knob off) at every
+    batch the path takes (1 .. SMs / 8) and at the first batch it does not, and the Zinc
+    ciphertexts equal the oracle's encryption of those plaintexts."""
+    s = _setup_real15(Z, orc) if name == "C4r" else setup_for(Z, orc, name)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    seed, base = 17, 900
+    for B in sorted({1, 2, 3, 7, sms // 8, sms // 8 + 1}):
+        z = torch.from_numpy(np.ascontiguousarray(slots_batch(s.cfg, 5, B))).cuda()
+        calls = [lambda: Z.ckks_encode_batch(s.ctx, z),
+                 lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[COEFF], COEFF, z, seed, base),
+                 lambda: Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, z, seed, base),
+                 lambda: Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, z, seed, base)]
+        got = [f() for f in calls]
+        old = Z.tune(Z.TUNE_SMALL_CLUSTER, 0)
+        try:
+            ref = [f() for f in calls]
+            torch.cuda.synchronize()
+        finally:
+            Z.tune(Z.TUNE_SMALL_CLUSTER, old)
+        for k, (a, b) in enumerate(zip(got, ref)):
+            assert torch.equal(a, b), (name, B, k)
+        m = np64(got[0])
+        idx = sorted({0, B // 2, B - 1})
+        _check_msgs(orc, s, "zinc", COEFF, m, np64(got[1]), seed, base, idx)
+        if name != "C4r":
+            for b in idx:
+                assert np.max(np.abs(m[b] - orc.encode(np64(z)[b], s.cfg.log_n, s.cfg.log_scale))) <= 1
