@@ -110,6 +110,10 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
+// 1: the Zinc COEFF slot chain starts with a one-wave chunk (see encrypt_any)
+#ifndef ZINC_FIRST_WAVE
+#define ZINC_FIRST_WAVE 0
+#endif
 static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}, {1}, {1}};
 
 // ------------------------------------------------------------------ context
@@ -824,8 +828,17 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
   uint64_t *uhat_scratch = uh ? reinterpret_cast<uint64_t *>(m + nb * chunk * c->n) : nullptr;
   zinc_status st = ZINC_OK;
   size_t k = 0;
-  for (size_t off = 0; off < batch && st == ZINC_OK; off += chunk, ++k) {
-    const size_t cnt = std::min(chunk, batch - off);
+  // Zinc COEFF form: the first chunk is one encode wave (nothing overlaps its encode, so the
+  // pipeline's fill time is that chunk's), the rest are full chunks
+  size_t first = chunk;
+#if ZINC_FIRST_WAVE
+  if (coeff_zinc && batch > chunk) {
+    const size_t w = c->encode_wave_msgs[kind == ZINC_PT_SLOTS_C128];
+    if (w > 0 && 2 * w <= chunk) first = w;
+  }
+#endif
+  for (size_t off = 0, cnt = 0; off < batch && st == ZINC_OK; off += cnt, ++k) {
+    cnt = std::min(k == 0 ? first : chunk, batch - off);
     int64_t *mb = in_ct ? (int64_t *)(ct + off * ct_stride + (ct_stride - c->n)) : m + (size_t)(k % nb) * chunk * c->n;
     const size_t mstride = in_ct ? ct_stride : (size_t)c->n;
     {
@@ -836,10 +849,10 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
     }
     PdlScope pdl_scope(pdl);
     // the Zinc COEFF kernel of this chunk warms the next chunk's slots into L2 for its encode
-    const size_t nxt = std::min(chunk, batch - std::min(batch, off + chunk));
+    const size_t nxt = std::min(chunk, batch - (off + cnt));
     const bool pf = coeff_zinc && g_tune[ZINC_TUNE_L2_PREFETCH].load() != 0 && nxt > 0 && aligned16(pt) &&
                     in_stride % 16 == 0;
-    g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + chunk) * in_stride, nxt * in_stride} : L2Prefetch{};
+    g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + cnt) * in_stride, nxt * in_stride} : L2Prefetch{};
     if (st == ZINC_OK)
       st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, !in_ct, mstride,
                     uhat_scratch);

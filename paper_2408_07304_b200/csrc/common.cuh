@@ -145,6 +145,21 @@ ZINC_DEV uint64_t pt_plus_e(int64_t m, int e, const LimbConst &c) {
     return add_mod(csub(mul_shoup_lazy(mt, c.delta, c.delta_sh, c.q), c.q), reduce_small(e, c.q), c.q);
   return reduce_i64q((int64_t)mt + (int64_t)c.t * e, c.q, c.mu64);
 }
+// A plaintext word read by a transform's first pass.  Each is used once per limb by one thread
+// and the cluster kernels read them with stride S (8 of every 32 bytes): with ZINC_M_NOALLOC
+// the load bypasses L1 allocation, which leaves L1 to the twiddles.
+#ifndef ZINC_M_NOALLOC
+#define ZINC_M_NOALLOC 1
+#endif
+ZINC_DEV int64_t ldm(const int64_t *p) {
+#if ZINC_M_NOALLOC
+  int64_t v;
+  asm("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
 // Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).
 // The plaintext-plus-error input of the first forward transform as a two-phase load
 // (ntt.cuh TwoPhase): fetch(x) reads m[x] from global memory, lift(raw, x) adds the sample
@@ -154,7 +169,7 @@ struct PtLoad {
   const int64_t *m;
   const int8_t *se1;
   const LimbConst &c;
-  ZINC_DEV int64_t fetch(int x) const { return m ? __ldg(m + x) : 0; }
+  ZINC_DEV int64_t fetch(int x) const { return m ? ldm(m + x) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const { return pt_plus_e<INTS>(raw, se1[x >> SHIFT], c); }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
 };
@@ -173,7 +188,7 @@ struct ZincTLoad {
   const int8_t *se;
   const LimbConst &c;
   int t;
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? __ldg(m + x) : 0; }
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + x) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     return t == 0 ? pt_plus_e<INTS>(raw, se[x >> SHIFT], c) : err_term<INTS>(se[x >> SHIFT], c);
   }

@@ -72,7 +72,7 @@ ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, i
   const uint64_t half = qmin >> 1;
   int big = 0;
 #pragma unroll 4
-  for (int i = threadIdx.x; i < G::NL; i += THREADS) big |= (uint64_t)__ldg(m + G::S * i + r) + half >= qmin;
+  for (int i = threadIdx.x; i < G::NL; i += THREADS) big |= (uint64_t)ldm(m + G::S * i + r) + half >= qmin;
   return !__syncthreads_or(big);
 }
 
@@ -167,7 +167,7 @@ struct VanTLoad {
   const uint8_t *su;
   const LimbConst &c;
   int t;
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? __ldg(m + x) : 0; }
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + x) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     const int i = x >> SHIFT;
     return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
               const uint64_t e = pt_plus_e<INTS>((int64_t)mx, se1[inv_sample_idx<LOGN>(x, r)], c);
               __stcs(ct0 + x, add_mod(csub(v, q), e, q));
             },
-            [&](int x) { return m ? (uint64_t)__ldg(m + x) : (uint64_t)0; }));
+            [&](int x) { return m ? (uint64_t)ldm(m + x) : (uint64_t)0; }));
     ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
