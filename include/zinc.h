@@ -285,10 +285,15 @@ void zinc_launch_count_reset(void);
  *                                 encode runs on an 8-CTA cluster, and Zinc COEFF form fuses the
  *                                 add/inject into the same launch (k_small.cu); 0: the throughput
  *                                 kernels (one CTA per message's encode, then the path kernel)
+ *  ZINC_TUNE_M_DEINT             slots feeding an NTT-form transform path at N >= 2^14: 1 (default) the
+ *                                 encode writes its scratch plaintexts de-interleaved by the cluster
+ *                                 size of the path kernel, so every CTA reads its subsequence
+ *                                 x = S i + r contiguously; 0: natural order (strided reads)
  * Sets knob to value (>= 0); *old_value (host, may be NULL) receives the previous value. */
 enum { ZINC_TUNE_COEFF_MSGS_PER_CTA = 0, ZINC_TUNE_ENCODE_CHUNK_BYTES = 1, ZINC_TUNE_PDL = 2,
        ZINC_TUNE_L2_PREFETCH = 3, ZINC_TUNE_NTT_CHUNK_MSGS = 4, ZINC_TUNE_SPLIT = 5, ZINC_TUNE_SMALL_ENCODE = 6,
-       ZINC_TUNE_PT_IN_CT = 7, ZINC_TUNE_SMALL_CLUSTER = 8, ZINC_TUNE_COUNT = 9 };
+       ZINC_TUNE_PT_IN_CT = 7, ZINC_TUNE_SMALL_CLUSTER = 8, ZINC_TUNE_M_DEINT = 9,
+       ZINC_TUNE_COUNT = 10 };
 zinc_status zinc_tune(int knob, long long value, long long *old_value);
 
 /* Thread-local message for the last non-OK status of this thread. */

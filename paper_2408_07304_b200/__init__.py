@@ -25,7 +25,7 @@ __all__ = [
     "ckks_decrypt_batch", "ckks_encode_batch", "zinc_ntt_forward", "zinc_ntt_inverse",
     "zinc_debug_sample", "zinc_int_peak", "zinc_ct_add_batch", "zinc_ct_sum_batch", "zinc_encrypt_batch_host", "launch_count",
     "launch_count_reset", "tune", "TUNE_COEFF_MSGS_PER_CTA", "TUNE_ENCODE_CHUNK_BYTES", "TUNE_PDL", "TUNE_L2_PREFETCH",
-    "TUNE_NTT_CHUNK_MSGS", "TUNE_SPLIT", "TUNE_SMALL_ENCODE", "TUNE_PT_IN_CT", "TUNE_SMALL_CLUSTER", "BFLY_CT", "BFLY_CT_NR", "BFLY_CT_A", "BFLY_GS", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
+    "TUNE_NTT_CHUNK_MSGS", "TUNE_SPLIT", "TUNE_SMALL_ENCODE", "TUNE_PT_IN_CT", "TUNE_SMALL_CLUSTER", "TUNE_M_DEINT", "BFLY_CT", "BFLY_CT_NR", "BFLY_CT_A", "BFLY_GS", "LIB_PATH", "EXPORTED_SYMBOLS", "profile_enable", "profile_read", "KERNEL_NAMES",
 ]
 
 NTT, COEFF = 0, 1
@@ -366,7 +366,7 @@ def profile_read() -> dict:
 
 
 TUNE_COEFF_MSGS_PER_CTA, TUNE_ENCODE_CHUNK_BYTES, TUNE_PDL, TUNE_L2_PREFETCH, TUNE_NTT_CHUNK_MSGS = 0, 1, 2, 3, 4
-TUNE_SPLIT, TUNE_SMALL_ENCODE, TUNE_PT_IN_CT, TUNE_SMALL_CLUSTER = 5, 6, 7, 8
+TUNE_SPLIT, TUNE_SMALL_ENCODE, TUNE_PT_IN_CT, TUNE_SMALL_CLUSTER, TUNE_M_DEINT = 5, 6, 7, 8, 9
 
 
 def tune(knob: int, value: int) -> int:

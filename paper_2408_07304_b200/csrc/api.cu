@@ -110,11 +110,7 @@ struct NvtxRange {
 static const int kWideLogScale = 48;
 
 // ------------------------------------------------------------------ tuning
-// 1: the Zinc COEFF slot chain starts with a one-wave chunk (see encrypt_any)
-#ifndef ZINC_FIRST_WAVE
-#define ZINC_FIRST_WAVE 0
-#endif
-static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}, {1}, {1}};
+static std::atomic<long long> g_tune[ZINC_TUNE_COUNT] = {{0}, {32ll << 20}, {1}, {1}, {0}, {1}, {0}, {1}, {1}, {1}};
 
 // ------------------------------------------------------------------ context
 struct zinc_ctx {
@@ -547,8 +543,10 @@ static bool small_cluster(const zinc_ctx *c, int kind, size_t batch) {
 }
 
 static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, size_t batch, int64_t *m,
-                               cudaStream_t s, bool wide = false, size_t m_stride = 0, int wait_mode = 0) {
+                               cudaStream_t s, bool wide = false, size_t m_stride = 0, int wait_mode = 0,
+                               int deint_log = 0) {
   EncodeArgs a = encode_args(c, kind, slots, m);
+  a.deint_log = deint_log;
   a.wide = wide ? 1 : 0;
   a.m_stride = m_stride ? m_stride : (size_t)c->n * (wide ? 2 : 1);
   a.wait_mode = wait_mode;
@@ -622,7 +620,8 @@ static bool vanilla_t_split(const zinc_ctx *c, int form, size_t batch) {
 // allocation per call on the small-batch path instead of two); null: allocate here.
 static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, int form, const int64_t *m,
                             size_t batch, uint64_t seed, uint64_t msg_base, uint64_t *ct, cudaStream_t s,
-                            bool m_is_scratch = false, size_t m_stride = 0, uint64_t *uhat_scratch = nullptr) {
+                            bool m_is_scratch = false, size_t m_stride = 0, uint64_t *uhat_scratch = nullptr,
+                            int m_deint = 0) {
   if (path == PATH_ZINC && form == ZINC_FORM_COEFF) {
     ZincCoeffArgs a = zinc_coeff_args(c, key, m, batch, seed, msg_base, ct);
     a.discard_m = m_is_scratch ? 1 : 0;
@@ -650,6 +649,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
     a.msg_base = msg_base;
     a.L = c->L;
     a.limbs_per_cta = lpc;
+    a.m_deint = m_deint;
     // a handful of messages: the two transforms on separate CTAs as well
     a.t_split = batch * (size_t)groups * 2 * ((size_t)c->n >> 12) <= 2 * (size_t)c->num_sms ? 1 : 0;
     if (use_split(c, SPLIT_ZINC_NTT))
@@ -669,6 +669,7 @@ static zinc_status run_path(const zinc_ctx *c, int path, const uint64_t *key, in
   a.msg_base = msg_base;
   a.L = c->L;
   a.limbs_per_cta = lpc;
+  a.m_deint = m_deint;
   // a handful of messages (NTT form): the three transforms on separate CTAs, then a combine
   const bool t_split = vanilla_t_split(c, form, batch);
   ScratchBuf uhat(s), pk_sh(s);
@@ -828,24 +829,25 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
   uint64_t *uhat_scratch = uh ? reinterpret_cast<uint64_t *>(m + nb * chunk * c->n) : nullptr;
   zinc_status st = ZINC_OK;
   size_t k = 0;
-  // Zinc COEFF form: the first chunk is one encode wave (nothing overlaps its encode, so the
-  // pipeline's fill time is that chunk's), the rest are full chunks
-  size_t first = chunk;
-#if ZINC_FIRST_WAVE
-  if (coeff_zinc && batch > chunk) {
-    const size_t w = c->encode_wave_msgs[kind == ZINC_PT_SLOTS_C128];
-    if (w > 0 && 2 * w <= chunk) first = w;
-  }
-#endif
   for (size_t off = 0, cnt = 0; off < batch && st == ZINC_OK; off += cnt, ++k) {
-    cnt = std::min(k == 0 ? first : chunk, batch - off);
+    cnt = std::min(chunk, batch - off);
     int64_t *mb = in_ct ? (int64_t *)(ct + off * ct_stride + (ct_stride - c->n)) : m + (size_t)(k % nb) * chunk * c->n;
     const size_t mstride = in_ct ? ct_stride : (size_t)c->n;
+    // NTT-form transform paths at N >= 2^14: the CTAs of a cluster read the subsequences
+    // x = S i + r of m (S = 2 for the parity-split vanilla kernel, N / 2^12 for the S-CTA
+    // kernels), so the encode writes the scratch de-interleaved by S and every CTA's read is
+    // contiguous (whole 32-byte sectors instead of 8 bytes of each)
+    int deint = 0;
+    if (!coeff_zinc && form == ZINC_FORM_NTT && c->log_n >= 14 && g_tune[ZINC_TUNE_M_DEINT].load() != 0 &&
+        !small_cluster(c, kind, cnt)) {
+      if (path == PATH_ZINC) deint = use_split(c, SPLIT_ZINC_NTT) ? c->log_n - 12 : 0;
+      else deint = (vanilla_t_split(c, form, cnt) || use_split(c, SPLIT_VANILLA_NTT)) ? c->log_n - 12 : 1;
+    }
     {
       // the first launch keeps a full dependency on whatever produced the inputs (its
       // loads precede its griddepcontrol.wait); later ones chain on this pipeline's kernels
       PdlScope pdl_scope(pdl && k > 0);
-      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s, false, mstride, in_ct ? 1 : 0);
+      st = encode_into(c, kind, (const char *)pt + off * in_stride, cnt, mb, s, false, mstride, in_ct ? 1 : 0, deint);
     }
     PdlScope pdl_scope(pdl);
     // the Zinc COEFF kernel of this chunk warms the next chunk's slots into L2 for its encode
@@ -855,7 +857,7 @@ static zinc_status encrypt_any(const zinc_ctx *c, int path, const uint64_t *key,
     g_l2_prefetch = pf ? L2Prefetch{(const char *)pt + (off + cnt) * in_stride, nxt * in_stride} : L2Prefetch{};
     if (st == ZINC_OK)
       st = run_path(c, path, key, form, mb, cnt, seed, msg_base + off, ct + off * ct_stride, s, !in_ct, mstride,
-                    uhat_scratch);
+                    uhat_scratch, deint);
     g_l2_prefetch = L2Prefetch{};
   }
   return st;

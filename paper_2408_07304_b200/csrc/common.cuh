@@ -160,6 +160,8 @@ ZINC_DEV int64_t ldm(const int64_t *p) {
   return __ldg(p);
 #endif
 }
+// Index of coefficient x in a plaintext de-interleaved by 2^d (EncodeArgs::deint_log), d = 0: x.
+ZINC_DEV int deint_idx(int x, int d, int log_n) { return ((x & ((1 << d) - 1)) << (log_n - d)) + (x >> d); }
 // Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).
 // The plaintext-plus-error input of the first forward transform as a two-phase load
 // (ntt.cuh TwoPhase): fetch(x) reads m[x] from global memory, lift(raw, x) adds the sample
@@ -169,7 +171,8 @@ struct PtLoad {
   const int64_t *m;
   const int8_t *se1;
   const LimbConst &c;
-  ZINC_DEV int64_t fetch(int x) const { return m ? ldm(m + x) : 0; }
+  int d = 0, log_n = 0;  // m de-interleaved by 2^d (deint_idx)
+  ZINC_DEV int64_t fetch(int x) const { return m ? ldm(m + deint_idx(x, d, log_n)) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const { return pt_plus_e<INTS>(raw, se1[x >> SHIFT], c); }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
 };
@@ -188,7 +191,8 @@ struct ZincTLoad {
   const int8_t *se;
   const LimbConst &c;
   int t;
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + x) : 0; }
+  int d = 0, log_n = 0;  // m de-interleaved by 2^d (deint_idx)
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + deint_idx(x, d, log_n)) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     return t == 0 ? pt_plus_e<INTS>(raw, se[x >> SHIFT], c) : err_term<INTS>(se[x >> SHIFT], c);
   }

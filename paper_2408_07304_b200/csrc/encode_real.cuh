@@ -74,11 +74,12 @@ ZINC_DEV void encode_real_post(const EncodeArgs &a, int64_t *m, const double2 *b
         store_i128(m + 2 * (j + M), y0.y * scale);
         store_i128(m + 2 * (j + H), y1.x * scale);
         store_i128(m + 2 * (j + H + M), y1.y * scale);
-      } else {
-        m[j] = llround(y0.x * scale);  // plain stores: the path kernel re-reads m from L2
-        m[j + M] = llround(y0.y * scale);
-        m[j + H] = llround(y1.x * scale);
-        m[j + H + M] = llround(y1.y * scale);
+      } else {  // plain stores: the path kernel re-reads m from L2 (de-interleaved by 2^d for it)
+        const int d = a.deint_log;
+        m[deint_idx(j, d, LOGM + 1)] = llround(y0.x * scale);
+        m[deint_idx(j + M, d, LOGM + 1)] = llround(y0.y * scale);
+        m[deint_idx(j + H, d, LOGM + 1)] = llround(y1.x * scale);
+        m[deint_idx(j + H + M, d, LOGM + 1)] = llround(y1.y * scale);
       }
     }
   }

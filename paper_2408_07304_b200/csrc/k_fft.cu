@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
       store_i128(m + 2 * j, w.x * scale);
       store_i128(m + 2 * (j + M), w.y * scale);
     } else {
-      m[j] = llround(w.x * scale);
-      m[j + M] = llround(w.y * scale);
+      m[deint_idx(j, a.deint_log, LOGM + 1)] = llround(w.x * scale);
+      m[deint_idx(j + M, a.deint_log, LOGM + 1)] = llround(w.y * scale);
     }
   };
   if constexpr (!SPLIT) {
@@ -124,10 +124,11 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
           store_i128(m + 2 * (x + ML), y1.x * scale);
           store_i128(m + 2 * (x + ML + M), y1.y * scale);
         } else {
-          m[x] = llround(y0.x * scale);
-          m[x + M] = llround(y0.y * scale);
-          m[x + ML] = llround(y1.x * scale);
-          m[x + ML + M] = llround(y1.y * scale);
+          const int d = a.deint_log;
+          m[deint_idx(x, d, LOGM + 1)] = llround(y0.x * scale);
+          m[deint_idx(x + M, d, LOGM + 1)] = llround(y0.y * scale);
+          m[deint_idx(x + ML, d, LOGM + 1)] = llround(y1.x * scale);
+          m[deint_idx(x + ML + M, d, LOGM + 1)] = llround(y1.y * scale);
         }
       }
     }

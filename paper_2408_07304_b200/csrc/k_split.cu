@@ -64,7 +64,7 @@ ZINC_DEV int inv_sample_idx(int x, int r) {
 // value (q_min over the CTA's limbs): then every lift of m + e is branch-free (lift_small), for
 // every limb, decided once per message instead of per word, limb and transform.
 template <int LOGN, int THREADS>
-ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, int lo, int hi) {
+ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, int lo, int hi, int d = 0) {
   using G = SplitGeo<LOGN>;
   if (!m) return true;
   uint64_t qmin = ~0ull;
@@ -72,7 +72,7 @@ ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, i
   const uint64_t half = qmin >> 1;
   int big = 0;
 #pragma unroll 4
-  for (int i = threadIdx.x; i < G::NL; i += THREADS) big |= (uint64_t)ldm(m + G::S * i + r) + half >= qmin;
+  for (int i = threadIdx.x; i < G::NL; i += THREADS) big |= (uint64_t)ldm(m + deint_idx(G::S * i + r, d, LOGN)) + half >= qmin;
   return !__syncthreads_or(big);
 }
 
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi);
+  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi, a.m_deint);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
     for (int t = t_lo; t < t_hi; ++t) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
-      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoadU<INTS, G::LOGS>{{m, t ? se2 : se1, c, t}, all_small},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoadU<INTS, G::LOGS>{{m, t ? se2 : se1, c, t, a.m_deint, LOGN}, all_small},
           ZincNttOut<S>{z, ctt, c}, stw, [&]() {
             if (SPLIT_STW && t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
           });
@@ -167,7 +167,8 @@ struct VanTLoad {
   const uint8_t *su;
   const LimbConst &c;
   int t;
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + x) : 0; }
+  int d, log_n;  // m de-interleaved by 2^d (deint_idx)
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + deint_idx(x, d, log_n)) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     const int i = x >> SHIFT;
     return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
   pdl_trigger();
   pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi);
+  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi, a.m_deint);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
     if constexpr (SPLIT_STW) tws.wait();
 #pragma unroll 1
     for (int t = t_lo; t < t_hi; ++t) {
-      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t, all_small || t > 0},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t, a.m_deint, LOGN, all_small || t > 0},
           [&](int x0, uint64_t (&v)[S]) {
             if (t < 2 || gridDim.z > 1) {
               uint64_t *dst = (t == 0 ? ct0 : t == 1 ? ct1 : a.u_hat + (b * L + i) * N) + x0;

@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
     auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     tws.wait();
     // sample of coefficient x = 2 i' + r sits at i' = x >> 1
-    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c},
+    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c, a.m_deint, LOGN},
                                      [&](int x, uint64_t v0, uint64_t v1) { st2(ct0 + x, canon(v0), canon(v1)); }, stw);
     ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); },
                                      [&](int x, uint64_t v0, uint64_t v1) { st2(ct1 + x, canon(v0), canon(v1)); }, stw);

@@ -55,6 +55,7 @@ struct VanillaArgs {
   uint64_t *u_hat;        // small batches, NTT form: the u transform's output [batch][L][N] (else null)
   uint64_t seed, msg_base;
   int L, limbs_per_cta;
+  int m_deint;            // log2 of the de-interleave of m (EncodeArgs::deint_log); 0: natural order
 };
 struct ZincNttArgs {
   const LimbConst *limbs;
@@ -65,6 +66,7 @@ struct ZincNttArgs {
   uint64_t seed, msg_base;
   int L, limbs_per_cta;
   int t_split;            // small batches: the two transforms on separate CTAs (gridDim.z = 2)
+  int m_deint;            // log2 of the de-interleave of m (EncodeArgs::deint_log); 0: natural order
 };
 struct KeygenArgs {
   const LimbConst *limbs;
@@ -123,6 +125,9 @@ struct EncodeArgs {
   size_t m_stride;          // int64 words between messages' plaintexts in m_out (N; 2N when wide)
   int wait_mode;            // PDL: 0 wait for the previous kernel before the plaintext stores,
                             // 1 after them (the stores go to a region no earlier kernel touches)
+  int deint_log;            // d > 0: coefficient x is stored at (x mod 2^d) N / 2^d + (x >> d), the order
+                            // in which the CTAs of a 2^d-CTA cluster transform read their subsequences
+                            // x = 2^d i + r (contiguous instead of stride 2^d); 64-bit plaintexts only
 };
 struct DecodeArgs {
   const int64_t *coeff;     // int64 [B][N], or int64 pairs [B][N][2] when wide

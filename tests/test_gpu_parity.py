@@ -399,6 +399,8 @@ def test_int_peak_kernel_runs(Z, orc, variant):
     {4: 1},                                   # one message per chunk
     {7: 0},                                   # Zinc COEFF plaintexts in double-buffered scratch
     {7: 2, 1: 1 << 20},                       # ... in the ciphertext slab, over 9 chunks
+    {9: 0},                                   # transform paths: scratch plaintexts in natural order
+    {9: 0, 4: 7},
 ])
 def test_tuning_knobs_never_change_results(Z, orc, knobs):
     """Launch geometry (messages per CTA, encode chunk sizes, programmatic dependent launch,
@@ -547,3 +549,33 @@ def test_small_cluster_path_bit_identical(Z, orc, name):
         if name != "C4r":
             for b in idx:
                 assert np.max(np.abs(m[b] - orc.encode(np64(z)[b], s.cfg.log_n, s.cfg.log_scale))) <= 1
+
+
+@pytest.mark.parametrize("name,B", [("C3", 40), ("C4", 6)])
+@pytest.mark.parametrize("split", [0, 1, 2])
+def test_deinterleaved_scratch_plaintexts_bit_identical(Z, orc, name, B, split):
+    """Slots feeding the NTT-form transform paths at N >= 2^14: the encode writes its scratch
+    plaintexts de-interleaved by the path kernel's cluster size (TUNE_M_DEINT, default) or in
+    natural order; same ciphertexts for every kernel family (TUNE_SPLIT), real and complex slots,
+    over a multi-chunk chain, and equal to the oracle's encryption of the GPU-encoded plaintexts."""
+    s = setup_for(Z, orc, name)
+    z = slots_batch(s.cfg, 0, B)
+    if s.cfg.complex_slots:
+        z = np.stack([z.real, z.imag], axis=-1)
+    zd = torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    m = np64(Z.ckks_encode_batch(s.ctx, zd))
+    outs = {}
+    for deint in (1, 0):
+        old = {k: Z.tune(k, v) for k, v in {Z.TUNE_M_DEINT: deint, Z.TUNE_SPLIT: split, Z.TUNE_NTT_CHUNK_MSGS: 25}.items()}
+        try:
+            outs[deint] = (Z.zinc_encrypt_batch(s.ctx, s.cache[NTT], NTT, zd, 5, 77),
+                           Z.ckks_encrypt_batch(s.ctx, s.pk, NTT, zd, 5, 77))
+            torch.cuda.synchronize()
+        finally:
+            for k, v in old.items():
+                Z.tune(k, v)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    idx = [0, B // 2, B - 1]
+    _check_msgs(orc, s, "zinc", NTT, m, np64(outs[1][0]), 5, 77, idx)
+    _check_msgs(orc, s, "vanilla", NTT, m, np64(outs[1][1]), 5, 77, idx)
