@@ -27,6 +27,20 @@ namespace zinc {
 using Tw = ulonglong2;
 
 ZINC_DEV Tw ldtw(const Tw *p) { return __ldg(p); }
+// Two consecutive twiddle pairs (one 32-byte sector, p 32-byte aligned) in one 256-bit load
+// (sm_100's LDG.256): the late stages' groups use 2, 4, 8 consecutive table entries, and two
+// 128-bit loads of one sector cost the L1 data pipe two sector accesses.
+#ifndef ZINC_TW_LD256
+#define ZINC_TW_LD256 1
+#endif
+ZINC_DEV void ldtw2(const Tw *p, Tw &a, Tw &b) {
+#if ZINC_TW_LD256
+  asm("ld.global.nc.v4.u64 {%0, %1, %2, %3}, [%4];" : "=l"(a.x), "=l"(a.y), "=l"(b.x), "=l"(b.y) : "l"(p));
+#else
+  a = __ldg(p);
+  b = __ldg(p + 1);
+#endif
+}
 
 // Padded shared-memory index (1 pad word per 16).
 ZINC_DEV int pad16(int i) { return i + (i >> 4); }
@@ -103,9 +117,15 @@ ZINC_DEV void ct_pass(const Tw *__restrict__ tw, uint64_t q, int tb, Load load, 
     Tw wpre[PRE ? G - 1 : 1];
     if constexpr (PRE) {
 #pragma unroll
-      for (int l = 0; l < K; ++l)
+      for (int l = 0; l < K; ++l) {
+        const Tw *p = tw + (tb << (S0 + l)) + (beta << l);  // an even index for l >= 1
+        if (l == 0) {
+          wpre[0] = ldtw(p);
+        } else {
 #pragma unroll
-        for (int blk = 0; blk < (1 << l); ++blk) wpre[(1 << l) - 1 + blk] = ldtw(tw + (tb << (S0 + l)) + (beta << l) + blk);
+          for (int blk = 0; blk < (1 << l); blk += 2) ldtw2(p + blk, wpre[(1 << l) - 1 + blk], wpre[(1 << l) + blk]);
+        }
+      }
     }
 #pragma unroll
     for (int l = 0; l < K; ++l) {
@@ -168,11 +188,24 @@ ZINC_DEV void gs_pass(const Tw *__restrict__ itw, const LimbConst &c, int tb, Lo
           v[j + D] = mul_shoup_lazy(d, c.ninv_w, c.ninv_w_sh, q);
         }
       } else {
+        const Tw *p = itw + (tb << (S0 + l)) + (beta << l);  // an even index for l >= 1
+        if (SMEM_TW || l == 0) {
 #pragma unroll
-        for (int blk = 0; blk < (1 << l); ++blk) {
-          const Tw w = SMEM_TW ? itw[(tb << (S0 + l)) + (beta << l) + blk] : ldtw(itw + (tb << (S0 + l)) + (beta << l) + blk);
+          for (int blk = 0; blk < (1 << l); ++blk) {
+            const Tw w = SMEM_TW ? p[blk] : ldtw(p + blk);
 #pragma unroll
-          for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, four_q);
+            for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w.x, w.y, q, four_q);
+          }
+        } else {
+#pragma unroll
+          for (int blk = 0; blk < (1 << l); blk += 2) {
+            Tw w0, w1;
+            ldtw2(p + blk, w0, w1);
+#pragma unroll
+            for (int j = 0; j < D; ++j) gs_bfly(v[blk * 2 * D + j], v[blk * 2 * D + j + D], w0.x, w0.y, q, four_q);
+#pragma unroll
+            for (int j = 0; j < D; ++j) gs_bfly(v[(blk + 1) * 2 * D + j], v[(blk + 1) * 2 * D + j + D], w1.x, w1.y, q, four_q);
+          }
         }
       }
     }
@@ -577,8 +610,13 @@ ZINC_DEV void split_fwd_tw(Tw (&w)[SplitGeo<LOGN>::S - 1], int k, const Tw *tw) 
 #pragma unroll
   for (int t = G::LOGS - 1; t >= 0; --t) {
     const int span = 1 << (G::LOGS - t - 1);  // 2^(s-t-1)
+    const Tw *p = tw + (N >> (t + 1)) + span * k;  // an even index for span >= 2
+    if (span == 1) {
+      w[0] = ldtw(p);
+    } else {
 #pragma unroll
-    for (int j = 0; j < span; ++j) w[span - 1 + j] = ldtw(tw + (N >> (t + 1)) + span * k + j);
+      for (int j = 0; j < span; j += 2) ldtw2(p + j, w[span - 1 + j], w[span + j]);
+    }
   }
 }
 template <int LOGN, bool NR>
