@@ -66,14 +66,7 @@ ZINC_DEV int inv_sample_idx(int x, int r) {
 template <int LOGN, int THREADS>
 ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, int lo, int hi, int d = 0) {
   using G = SplitGeo<LOGN>;
-  if (!m) return true;
-  uint64_t qmin = ~0ull;
-  for (int i = lo; i < hi; ++i) qmin = min(qmin, limbs[i].q);
-  const uint64_t half = qmin >> 1;
-  int big = 0;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < G::NL; i += THREADS) big |= (uint64_t)ldm(m + deint_idx(G::S * i + r, d, LOGN)) + half >= qmin;
-  return !__syncthreads_or(big);
+  return plaintext_small_sub<THREADS>(m, G::LOGS, r, G::NL, d, LOGN, limbs, lo, hi);
 }
 
 template <int LOGN> struct SplitSmem {
@@ -88,7 +81,7 @@ template <int LOGN> struct SplitSmem {
 template <int S>
 struct ZincNttOut {
   struct Pre {
-    ulonglong2 z[S / 2];
+    U64x4 z[S / 4];
   };
   const uint64_t *z;
   uint64_t *ctt;
@@ -96,13 +89,14 @@ struct ZincNttOut {
   ZINC_DEV Pre pre(int x0) const {
     Pre p;
 #pragma unroll
-    for (int u = 0; u < S / 2; ++u) p.z[u] = ld2_nc(z + x0 + 2 * u);
+    for (int u = 0; u < S / 4; ++u) p.z[u] = ld4_nc(z + x0 + 4 * u);
     return p;
   }
   ZINC_DEV void operator()(int x0, uint64_t (&v)[S], const Pre &p) const {
 #pragma unroll
-    for (int u = 0; u < S / 2; ++u)  // lazy output + canonical cache word < 2^64
-      st2_cs(ctt + x0 + 2 * u, reduce_fold(p.z[u].x + v[2 * u], c), reduce_fold(p.z[u].y + v[2 * u + 1], c));
+    for (int u = 0; u < S / 4; ++u)  // lazy output + canonical cache word < 2^64
+      st4_cs(ctt + x0 + 4 * u, reduce_fold(p.z[u].v[0] + v[4 * u], c), reduce_fold(p.z[u].v[1] + v[4 * u + 1], c),
+             reduce_fold(p.z[u].v[2] + v[4 * u + 2], c), reduce_fold(p.z[u].v[3] + v[4 * u + 3], c));
   }
 };
 
@@ -160,31 +154,6 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
 // NTT(m + e1) -> ct0, NTT(e2) -> ct1, NTT(u) -> ct0 += pk1 u^, ct1 += pk2 u^ (Eq. 8, A1).
 // The three transforms of a limb run through one copy of the transform code; every
 // exchange thread re-reads only the ciphertext words it wrote itself.
-template <bool INTS, int SHIFT>
-struct VanTLoad {
-  const int64_t *m;
-  const int8_t *se1, *se2;
-  const uint8_t *su;
-  const LimbConst &c;
-  int t;
-  int d, log_n;  // m de-interleaved by 2^d (deint_idx)
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + deint_idx(x, d, log_n)) : 0; }
-  ZINC_DEV uint64_t lift(int64_t raw, int x) const {
-    const int i = x >> SHIFT;
-    return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
-                                                             : reduce_small(tern_at(su, i), c.q);
-  }
-  bool all_small;  // CTA-uniform (plaintext_small, or t > 0: no plaintext term)
-  ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
-  // CKKS: |m| < q/2 makes |m + e| < q, and the residue is branch-free (t = 1, 2: raw = 0)
-  ZINC_DEV bool uniform_small() const { return !INTS && all_small; }
-  ZINC_DEV uint64_t lift_small(int64_t raw, int x) const {
-    const int i = x >> SHIFT;
-    const int64_t v = raw + (t == 0 ? se1[i] : t == 1 ? se2[i] : tern_at(su, i));
-    return (uint64_t)v + (c.q & (uint64_t)(v >> 63));
-  }
-};
-
 template <int LOGN, int MODE>
 __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel(VanillaArgs a) {
   constexpr bool INTS = MODE == 2, NR = MODE == 0;
@@ -234,17 +203,21 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
             if (t < 2 || gridDim.z > 1) {
               uint64_t *dst = (t == 0 ? ct0 : t == 1 ? ct1 : a.u_hat + (b * L + i) * N) + x0;
 #pragma unroll
-              for (int u = 0; u < S; u += 2) st2(dst + u, canon(v[u]), canon(v[u + 1]));
+              for (int u = 0; u < S; u += 4) st4(dst + u, canon(v[u]), canon(v[u + 1]), canon(v[u + 2]), canon(v[u + 3]));
             } else {
 #pragma unroll
-              for (int u = 0; u < S; u += 2) {
-                const ulonglong2 p1 = ld2_nc(pk1 + x0 + u), p2 = ld2_nc(pk2 + x0 + u);
-                const ulonglong2 s1 = ld2_nc(pk1s + x0 + u), s2 = ld2_nc(pk2s + x0 + u);
-                uint64_t a0, a1, b0, b1;
-                ld2(ct0 + x0 + u, a0, a1);
-                ld2(ct1 + x0 + u, b0, b1);
-                st2_cs(ct0 + x0 + u, add_shoup(a0, v[u], p1.x, s1.x, q), add_shoup(a1, v[u + 1], p1.y, s1.y, q));
-                st2_cs(ct1 + x0 + u, add_shoup(b0, v[u], p2.x, s2.x, q), add_shoup(b1, v[u + 1], p2.y, s2.y, q));
+              for (int u = 0; u < S; u += 4) {
+                const U64x4 p1 = ld4_nc(pk1 + x0 + u), p2 = ld4_nc(pk2 + x0 + u);
+                const U64x4 s1 = ld4_nc(pk1s + x0 + u), s2 = ld4_nc(pk2s + x0 + u);
+                const U64x4 ca = ld4(ct0 + x0 + u), cb2 = ld4(ct1 + x0 + u);
+                uint64_t o0[4], o1[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  o0[j] = add_shoup(ca.v[j], v[u + j], p1.v[j], s1.v[j], q);
+                  o1[j] = add_shoup(cb2.v[j], v[u + j], p2.v[j], s2.v[j], q);
+                }
+                st4_cs(ct0 + x0 + u, o0[0], o0[1], o0[2], o0[3]);
+                st4_cs(ct1 + x0 + u, o1[0], o1[1], o1[2], o1[3]);
               }
             }
           },
@@ -302,13 +275,15 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
     ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> G::LOGS), q); },
         [&](int x0, uint64_t (&v)[S]) {
 #pragma unroll
-          for (int u = 0; u < S; u += 2) {
-            const ulonglong2 p1 = ld2_nc(pk1 + x0 + u), p2 = ld2_nc(pk2 + x0 + u);
-            const ulonglong2 s1 = ld2_nc(pk1s + x0 + u), s2 = ld2_nc(pk2s + x0 + u);
+          for (int u = 0; u < S; u += 4) {
+            const U64x4 p1 = ld4_nc(pk1 + x0 + u), p2 = ld4_nc(pk2 + x0 + u);
+            const U64x4 s1 = ld4_nc(pk1s + x0 + u), s2 = ld4_nc(pk2s + x0 + u);
             // [0, 2q): the inverse transforms take inputs below 4q
-            st2(ct1 + x0 + u, mul_shoup_lazy(v[u], p2.x, s2.x, q), mul_shoup_lazy(v[u + 1], p2.y, s2.y, q));  // temporary
-            sm[pad16(x0 + u - r * NL)] = mul_shoup_lazy(v[u], p1.x, s1.x, q);  // this CTA's inverse input
-            sm[pad16(x0 + u + 1 - r * NL)] = mul_shoup_lazy(v[u + 1], p1.y, s1.y, q);
+            st4(ct1 + x0 + u, mul_shoup_lazy(v[u], p2.v[0], s2.v[0], q), mul_shoup_lazy(v[u + 1], p2.v[1], s2.v[1], q),
+                mul_shoup_lazy(v[u + 2], p2.v[2], s2.v[2], q), mul_shoup_lazy(v[u + 3], p2.v[3], s2.v[3], q));  // temporary
+#pragma unroll
+            for (int j = 0; j < 4; ++j)  // this CTA's inverse input
+              sm[pad16(x0 + u + j - r * NL)] = mul_shoup_lazy(v[u + j], p1.v[j], s1.v[j], q);
           }
         },
         stw, [&]() {
@@ -324,7 +299,11 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
     ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
         [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-          for (int u = 0; u < 16; u += 2) ld2(ct1 + base + u, v[u], v[u + 1]);
+          for (int u = 0; u < 16; u += 4) {
+            const U64x4 w = ld4(ct1 + base + u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[u + j] = w.v[j];
+          }
         },
         [&](int x, uint64_t v) {
           __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[inv_sample_idx<LOGN>(x, r)], c), q));
@@ -404,8 +383,12 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) decrypt_split_kernel(Dec
       ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
           [&](int base, uint64_t (&v)[16]) {
 #pragma unroll
-            for (int u = 0; u < 16; ++u)
-              v[u] = __ldg(c1 + base + u) + mul_shoup_lazy(__ldg(c2 + base + u), __ldg(s + base + u), __ldg(ssh + base + u), q);
+            for (int u = 0; u < 16; u += 4) {
+              const U64x4 w1 = ld4_nc(c1 + base + u), w2 = ld4_nc(c2 + base + u), ws = ld4_nc(s + base + u),
+                          wh = ld4_nc(ssh + base + u);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[u + j] = w1.v[j] + mul_shoup_lazy(w2.v[j], ws.v[j], wh.v[j], q);
+            }
           },
           with_pre1(epilogue, pre));
     } else {
@@ -414,8 +397,11 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) decrypt_split_kernel(Dec
       ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return __ldg(c2 + x); },
           [&](int x0g, uint64_t (&v)[S]) {
 #pragma unroll
-            for (int u = 0; u < S; ++u)
-              sm[pad16(x0g + u - r * NL)] = mul_shoup_lazy(v[u], __ldg(s + x0g + u), __ldg(ssh + x0g + u), q);
+            for (int u = 0; u < S; u += 4) {
+              const U64x4 ws = ld4_nc(s + x0g + u), wh = ld4_nc(ssh + x0g + u);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) sm[pad16(x0g + u + j - r * NL)] = mul_shoup_lazy(v[u + j], ws.v[j], wh.v[j], q);
+            }
           },
           tw);
       ntt_inverse_split<LOGN, false>(sm, cb, itw, c, [](int, uint64_t (&)[16]) {},

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
   const int64_t *m = a.m ? a.m + b * N : nullptr;
+  const bool all_small = !INTS && plaintext_small_sub<THREADS>(m, 1, r, G::NL, a.m_deint, LOGN, a.limbs, lo, hi);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -169,23 +170,27 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
     uint64_t *ct1 = ct0 + (size_t)L * N;
     auto canon = [&](uint64_t v) { return reduce_fold(v, c); };
     tws.wait();
-    // sample of coefficient x = 2 i' + r sits at i' = x >> 1
-    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, PtLoad<INTS, 1>{m, se1, c, a.m_deint, LOGN},
-                                     [&](int x, uint64_t v0, uint64_t v1) { st2(ct0 + x, canon(v0), canon(v1)); }, stw);
-    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return err_term<INTS>(se2[x >> 1], c); },
-                                     [&](int x, uint64_t v0, uint64_t v1) { st2(ct1 + x, canon(v0), canon(v1)); }, stw);
-    ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, [&](int x) { return reduce_small(tern_at(su, x >> 1), q); },
-        [&](int x, uint64_t v0, uint64_t v1) {
-          const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x), s1 = ld2_nc(pk1s + x), s2 = ld2_nc(pk2s + x);
-          uint64_t a0, a1, b0, b1;
-          ld2(ct0 + x, a0, a1);
-          ld2(ct1 + x, b0, b1);
-          st2_cs(ct0 + x, add_shoup(a0, v0, p1.x, s1.x, q), add_shoup(a1, v1, p1.y, s1.y, q));
-          st2_cs(ct1 + x, add_shoup(b0, v0, p2.x, s2.x, q), add_shoup(b1, v1, p2.y, s2.y, q));
-        },
-        stw, [&]() {
-          if (i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
-        });
+    // the three transforms through one copy of the transform code (t at run time: a third of
+    // the instruction footprint); the sample of coefficient x = 2 i' + r sits at i' = x >> 1
+#pragma unroll 1
+    for (int t = 0; t < 3; ++t) {
+      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, VanTLoad<INTS, 1>{m, se1, se2, su, c, t, a.m_deint, LOGN, all_small || t > 0},
+          [&](int x, uint64_t v0, uint64_t v1) {
+            if (t < 2) {
+              st2((t == 0 ? ct0 : ct1) + x, canon(v0), canon(v1));
+            } else {
+              const ulonglong2 p1 = ld2_nc(pk1 + x), p2 = ld2_nc(pk2 + x), s1 = ld2_nc(pk1s + x), s2 = ld2_nc(pk2s + x);
+              uint64_t a0, a1, b0, b1;
+              ld2(ct0 + x, a0, a1);
+              ld2(ct1 + x, b0, b1);
+              st2_cs(ct0 + x, add_shoup(a0, v0, p1.x, s1.x, q), add_shoup(a1, v1, p1.y, s1.y, q));
+              st2_cs(ct1 + x, add_shoup(b0, v0, p2.x, s2.x, q), add_shoup(b1, v1, p2.y, s2.y, q));
+            }
+          },
+          stw, [&]() {
+            if (t == 2 && i + 1 < hi) tws.issue(stw, tw + N);  // lands during pass C + exchange
+          });
+    }
   }
 }
 

@@ -78,11 +78,102 @@ ZINC_DEV void st2(uint64_t *p, uint64_t a, uint64_t b) {
 ZINC_DEV void st2_cs(uint64_t *p, uint64_t a, uint64_t b) {
   asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
+// 256-bit (four-word, 32-byte aligned) forms: sm_100's LDG / STG .256.  A thread that moves four
+// consecutive words with two 128-bit accesses touches its 32-byte sector twice; the L1 data pipe
+// counts sector accesses.  ZINC_LDST256 = 0 falls back to two 128-bit accesses.
+#ifndef ZINC_LDST256
+#define ZINC_LDST256 1
+#endif
+struct U64x4 {
+  uint64_t v[4];
+};
+ZINC_DEV U64x4 ld4_nc(const uint64_t *p) {  // read-only data, no L1 allocation
+  U64x4 r;
+#if ZINC_LDST256
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(r.v[0]), "=l"(r.v[1]), "=l"(r.v[2]), "=l"(r.v[3]) : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.v[0]), "=l"(r.v[1]) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(r.v[2]), "=l"(r.v[3]) : "l"(p + 2));
+#endif
+  return r;
+}
+ZINC_DEV U64x4 ld4(const uint64_t *p) {  // coherent: words this kernel wrote earlier
+  U64x4 r;
+#if ZINC_LDST256
+  asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(r.v[0]), "=l"(r.v[1]), "=l"(r.v[2]), "=l"(r.v[3]) : "l"(p) : "memory");
+#else
+  ld2(p, r.v[0], r.v[1]);
+  ld2(p + 2, r.v[2], r.v[3]);
+#endif
+  return r;
+}
+ZINC_DEV void st4(uint64_t *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+#if ZINC_LDST256
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+#else
+  st2(p, a, b);
+  st2(p + 2, c, d);
+#endif
+}
+ZINC_DEV void st4_cs(uint64_t *p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {  // streaming (evict-first)
+#if ZINC_LDST256
+  asm volatile("st.global.cs.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+#else
+  st2_cs(p, a, b);
+  st2_cs(p + 2, c, d);
+#endif
+}
 ZINC_DEV ulonglong2 ld2_nc(const void *p) {
   ulonglong2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
   return v;
 }
+
+// CKKS plaintext words of a CTA's subsequence x = 2^log_s i + r (i < nl) all below q_min / 2 in
+// absolute value (q_min over the CTA's limbs): then every lift of m + e is branch-free
+// (lift_small) for every limb, decided once per message instead of per word, limb and transform.
+// d: m de-interleaved by 2^d (deint_idx).
+template <int THREADS>
+ZINC_DEV bool plaintext_small_sub(const int64_t *m, int log_s, int r, int nl, int d, int log_n, const LimbConst *limbs,
+                                  int lo, int hi) {
+  if (!m) return true;
+  uint64_t qmin = ~0ull;
+  for (int i = lo; i < hi; ++i) qmin = min(qmin, limbs[i].q);
+  const uint64_t half = qmin >> 1;
+  int big = 0;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < nl; i += THREADS) big |= (uint64_t)ldm(m + deint_idx((i << log_s) + r, d, log_n)) + half >= qmin;
+  return !__syncthreads_or(big);
+}
+
+// The three inputs of a vanilla NTT-form limb as one two-phase load (t = 0: m + e1, 1: e2, 2: u),
+// so the three transforms run through one copy of the transform code.  Samples sit at x >> SHIFT.
+template <bool INTS, int SHIFT>
+struct VanTLoad {
+  const int64_t *m;
+  const int8_t *se1, *se2;
+  const uint8_t *su;
+  const LimbConst &c;
+  int t;
+  int d, log_n;  // m de-interleaved by 2^d (deint_idx)
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + deint_idx(x, d, log_n)) : 0; }
+  ZINC_DEV uint64_t lift(int64_t raw, int x) const {
+    const int i = x >> SHIFT;
+    return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
+                                                             : reduce_small(tern_at(su, i), c.q);
+  }
+  bool all_small;  // CTA-uniform (plaintext_small, or t > 0: no plaintext term)
+  ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
+  // CKKS: |m| < q/2 makes |m + e| < q, and the residue is branch-free (t = 1, 2: raw = 0)
+  ZINC_DEV bool uniform_small() const { return !INTS && all_small; }
+  ZINC_DEV uint64_t lift_small(int64_t raw, int x) const {
+    const int i = x >> SHIFT;
+    const int64_t v = raw + (t == 0 ? se1[i] : t == 1 ? se2[i] : tern_at(su, i));
+    return (uint64_t)v + (c.q & (uint64_t)(v >> 63));
+  }
+};
 
 // ============================================================ smem epilogues
 // Transform outputs go back into the CTA's own shared-memory buffer (final-pass

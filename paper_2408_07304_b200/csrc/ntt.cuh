@@ -341,7 +341,17 @@ ZINC_DEV void ntt_forward_dit2(uint64_t *sm, const Tw *tw, uint64_t q, Load load
   const int r = (int)cluster_rank();
   __syncthreads();
   if constexpr (TwoPhase<Load>::value) {
-    if constexpr (HasSmallLift<Load>::value) {
+    if constexpr (HasUniformSmall<Load>::value) {
+      struct Parity {  // local index i -> coefficient 2 i + r
+        const Load &l;
+        int r;
+        ZINC_DEV int64_t fetch(int i) const { return l.fetch(2 * i + r); }
+        ZINC_DEV uint64_t lift(int64_t raw, int i) const { return l.lift(raw, 2 * i + r); }
+        ZINC_DEV bool uniform_small() const { return l.uniform_small(); }
+        ZINC_DEV uint64_t lift_small(int64_t raw, int i) const { return l.lift_small(raw, 2 * i + r); }
+      };
+      ct_pass<LL, 0, P::KA, P::THREADS, false, STW, NR>(STW ? stw : tw, q, 1, Parity{load, r}, sst);
+    } else if constexpr (HasSmallLift<Load>::value) {
       struct Parity {  // local index i -> coefficient 2 i + r
         const Load &l;
         int r;
