@@ -124,7 +124,7 @@ struct zinc_ctx {
   std::vector<LimbConst> h_limbs;
   LimbConst *d_limbs = nullptr;
   Tw *d_tw = nullptr, *d_itw = nullptr;
-  double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr, *d_post_tw = nullptr;
+  double2 *d_fft_tw = nullptr, *d_twist = nullptr, *d_fft_tw_h = nullptr, *d_fft_tw_hp = nullptr, *d_post_tw = nullptr;
   double2 *d_twist_split = nullptr;
   int *d_perm = nullptr;
   uint64_t qmin = 0;
@@ -292,6 +292,7 @@ zinc_status zinc_ctx_destroy(zinc_ctx *ctx) {
   cudaFree(ctx->d_post_tw);
   cudaFree(ctx->d_twist_split);
   cudaFree(ctx->d_fft_tw_h);
+  cudaFree(ctx->d_fft_tw_hp);
   cudaFree(ctx->d_perm);
   delete ctx;
   return ZINC_OK;
@@ -451,9 +452,12 @@ zinc_status zinc_ctx_create_scheme(int log_n, int L, const int *limb_bits, int s
     perm[k] = (int)brv((uint32_t)((g - 1) / 4), log_m);
     g = g * 5 % (2ull * n);
   }
+  // the padded copy the encode kernels stage in shared memory (fft.cuh fft_twpad)
+  std::vector<double2> ftw_hp((size_t)fft_twpad_size(M / 4), make_double2(0.0, 0.0));
+  for (int e = 0; e < M / 4; ++e) ftw_hp[(size_t)fft_twpad(e)] = ftw_h[e];
   zinc_status st;
   if (cudaSetDevice(device) != cudaSuccess) { delete c; return fail(ZINC_ECUDA, "cudaSetDevice(%d) failed", device); }
-  if ((st = upload(&c->d_limbs, c->h_limbs)) || (st = upload(&c->d_tw, tw)) || (st = upload(&c->d_itw, itw)) ||
+  if ((st = upload(&c->d_fft_tw_hp, ftw_hp)) || (st = upload(&c->d_limbs, c->h_limbs)) || (st = upload(&c->d_tw, tw)) || (st = upload(&c->d_itw, itw)) ||
       (st = upload(&c->d_fft_tw, ftw)) || (st = upload(&c->d_twist, twist)) || (st = upload(&c->d_perm, perm)) ||
       (st = upload(&c->d_fft_tw_h, ftw_h)) || (st = upload(&c->d_post_tw, post_tw)) ||
       (st = upload(&c->d_twist_split, twist_split))) {
@@ -528,6 +532,7 @@ static EncodeArgs encode_args(const zinc_ctx *c, int kind, const void *slots, in
   a.fft_tw = c->d_fft_tw;
   a.twist = c->d_twist;
   a.fft_tw_h = c->d_fft_tw_h;
+  a.fft_tw_hp = c->d_fft_tw_hp;
   a.post_tw = c->d_post_tw;
   a.twist_split = c->d_twist_split;
   a.scale = ldexp(1.0, c->log_scale - (c->log_n - 1));

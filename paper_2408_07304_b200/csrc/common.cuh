@@ -160,6 +160,14 @@ ZINC_DEV int64_t ldm(const int64_t *p) {
   return __ldg(p);
 #endif
 }
+// Index of twiddle e in the padded shared-memory copy of a table (TW_SMEM = 2): one 16-byte pad per
+// 8, 64 and 512 entries.  The passes read entries (o + c) 2^k for consecutive o; unpadded, every
+// stride of 8 entries or more puts a warp's loads in one 128-byte bank row (measured 8x the ideal
+// wavefronts on 15 of the second pass's loads); padded, strides 2^0 .. 2^9 spread evenly.
+__host__ __device__ constexpr int fft_twpad(int e) { return e + (e >> 3) + (e >> 6) + (e >> 9); }
+// Entries of the padded copy of an n-entry table.
+__host__ __device__ constexpr int fft_twpad_size(int n) { return fft_twpad(n - 1) + 1; }
+
 // Index of coefficient x in a plaintext de-interleaved by 2^d (EncodeArgs::deint_log), d = 0: x.
 ZINC_DEV int deint_idx(int x, int d, int log_n) { return ((x & ((1 << d) - 1)) << (log_n - d)) + (x >> d); }
 // Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).

@@ -90,13 +90,13 @@ template <int LOGM> __host__ __device__ constexpr int encode_post_tw_entries() {
 
 // Shared memory bytes of one real-slot encode CTA (FFT buffer + twiddles).
 template <int LOGM> constexpr size_t encode_real_smem() {
-  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + (1 << (LOGM - 1)) / 2 + encode_post_tw_entries<LOGM>()) *
+  return ((1 << (LOGM - 1)) + (1 << (LOGM - 1)) / 16 + fft_twpad_size((1 << (LOGM - 1)) / 2) + encode_post_tw_entries<LOGM>()) *
          sizeof(double2);
 }
 
 // The half-length DIT FFT of the encode: NPASS = 3 radix-16 passes (FftPlan) or
 // NPASS = 4 radix-8 passes (3 + 3 + 3 + rest; half the registers per thread).
-template <int LH, int THREADS, int NPASS, bool TW_SMEM, class Ld, class St>
+template <int LH, int THREADS, int NPASS, int TW_SMEM, class Ld, class St>
 ZINC_DEV void encode_fft(const double2 *tw, Ld lds, St sts) {
   using P = FftPlan<LH>;
   if constexpr (NPASS == 3) {
@@ -138,8 +138,9 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   constexpr int M = 1 << LOGM, LH = LOGM - 1, H = 1 << LH;
   constexpr int PER = M / THREADS;
   static_assert(NPASS != 3 || FftPlan<LH>::THREADS == THREADS, "plan");
-  double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2], then post tables
-  double2 *sptw = stw + H / 2;
+  double2 *stw = buf + H + H / 16;  // FFT buffer [H + H/16], then twiddles [H/2, padded], then post tables
+  constexpr int TWP = fft_twpad_size(H / 2);
+  double2 *sptw = stw + TWP;
   constexpr int NPT = encode_post_tw_entries<LOGM>();
   double *bufd = reinterpret_cast<double *>(buf);
   __shared__ __align__(8) uint64_t mbar;
@@ -147,9 +148,9 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   if (tid == 0) mbar_init(&mbar, 1);
   __syncthreads();
   if (tid == 0) {
-    mbar_expect_tx(&mbar, (uint32_t)(M * sizeof(double) + (H / 2 + NPT) * sizeof(double2)));
+    mbar_expect_tx(&mbar, (uint32_t)(M * sizeof(double) + (TWP + NPT) * sizeof(double2)));
     bulk_g2s(buf, a.slots + b * M, M * sizeof(double), &mbar);  // raw slots into the buffer prefix
-    bulk_g2s(stw, a.fft_tw_h, (H / 2) * sizeof(double2), &mbar);
+    bulk_g2s(stw, a.fft_tw_hp, TWP * sizeof(double2), &mbar);
     bulk_g2s(sptw, a.post_tw, NPT * sizeof(double2), &mbar);
   }
   constexpr uint32_t MASK = 4u * M - 1u;  // mod 2N
@@ -170,7 +171,7 @@ ZINC_DEV void encode_real_body(const EncodeArgs &a, size_t b, double2 *buf) {
   __syncthreads();
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
-  encode_fft<LH, THREADS, NPASS, true>(stw, lds, sts);
+  encode_fft<LH, THREADS, NPASS, 2>(stw, lds, sts);
   __syncthreads();
   // Under a programmatic dependent launch the previous Zinc kernel may still read the scratch
   // this encode overwrites: the loads and the FFT above overlapped it, the stores wait.

@@ -29,8 +29,8 @@ ZINC_DEV double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
 // TWS: twiddle-table stride.  The table holds W_M^e of the full transform; a
 // CTA running an M/2-point sub-transform (the split N = 2^15 case) reads it
 // with stride 2 (W_{M/2}^e = W_M^{2e}).
-// TW_SMEM: the table lives in shared memory (plain loads instead of __ldg).
-template <int LOGM, int S0, int K, int THREADS, bool DIT, bool CONJ, int TWS = 1, bool TW_SMEM = false, class Load,
+// TW_SMEM: 1 the table lives in shared memory (plain loads instead of __ldg), 2 padded (fft_twpad).
+template <int LOGM, int S0, int K, int THREADS, bool DIT, bool CONJ, int TWS = 1, int TW_SMEM = 0, class Load,
           class Store>
 ZINC_DEV void fft_pass(const double2 *__restrict__ tw, Load load, Store store) {
   constexpr int M = 1 << LOGM;
@@ -52,7 +52,7 @@ ZINC_DEV void fft_pass(const double2 *__restrict__ tw, Load load, Store store) {
         for (int r = 0; r < G; ++r) {
           if (r & D) continue;
           const int e = (o + (r & (D - 1)) * T) * (M >> (S0 + l + 1)) * TWS;
-          double2 w = TW_SMEM ? tw[e] : __ldg(tw + e);
+          double2 w = TW_SMEM == 2 ? tw[fft_twpad(e)] : TW_SMEM ? tw[e] : __ldg(tw + e);
           if (CONJ) w = conj2(w);
           const double2 b = cmul(v[r + D], w);
           v[r + D] = csubd(v[r], b);
@@ -67,7 +67,7 @@ ZINC_DEV void fft_pass(const double2 *__restrict__ tw, Load load, Store store) {
         for (int r = 0; r < G; ++r) {
           if (r & D) continue;
           const int e = (o + (r & (D - 1)) * T) * (M >> (S0 + l + 1)) * TWS;
-          double2 w = TW_SMEM ? tw[e] : __ldg(tw + e);
+          double2 w = TW_SMEM == 2 ? tw[fft_twpad(e)] : TW_SMEM ? tw[e] : __ldg(tw + e);
           if (CONJ) w = conj2(w);
           const double2 a = v[r], b = v[r + D];
           v[r] = cadd(a, b);

@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   if constexpr (SPLIT) {
     if (threadIdx.x == 0) {
       mbar_init(&tw_mbar, 1);
-      mbar_expect_tx(&tw_mbar, (uint32_t)((M / 4) * sizeof(double2)));
-      bulk_g2s(stw, a.fft_tw_h, (uint32_t)((M / 4) * sizeof(double2)), &tw_mbar);
+      mbar_expect_tx(&tw_mbar, (uint32_t)(fft_twpad_size(M / 4) * sizeof(double2)));
+      bulk_g2s(stw, a.fft_tw_hp, (uint32_t)(fft_twpad_size(M / 4) * sizeof(double2)), &tw_mbar);
     }
   }
   __syncthreads();
@@ -61,9 +61,9 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
   if constexpr (SPLIT) {
-    fft_pass<LL, 0, P::K1, P::THREADS, true, false, 1, true>(stw, lds, sts);
+    fft_pass<LL, 0, P::K1, P::THREADS, true, false, 1, 2>(stw, lds, sts);
     __syncthreads();
-    fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, 1, true>(stw, lds, sts);
+    fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, 1, 2>(stw, lds, sts);
   } else {
     fft_pass<LL, 0, P::K1, P::THREADS, true, false, TWS>(a.fft_tw, lds, sts);
     __syncthreads();
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREAD
   if constexpr (!SPLIT) {
     fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false>(a.fft_tw, lds, emit);
   } else {
-    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, 1, true>(stw, lds, sts);
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, 1, 2>(stw, lds, sts);
     cluster_sync_all();
     const double2 *h0 = peer_smem(buf, 0), *h1 = peer_smem(buf, 1);
     // U independent iterations: their DSMEM, twiddle and twist loads are all in flight
@@ -209,7 +209,7 @@ template <int LOGM> static size_t fft_smem() {
 }
 // complex-slot encode: split CTAs also hold the sub-transform's twiddle table (M/4 entries)
 template <int LOGM> static size_t encode_smem() {
-  return fft_smem<LOGM>() + (LOGM > 13 ? (size_t)(1 << LOGM) / 4 * sizeof(double2) : 0);
+  return fft_smem<LOGM>() + (LOGM > 13 ? (size_t)fft_twpad_size((1 << LOGM) / 4) * sizeof(double2) : 0);
 }
 template <int LOGM>
 static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream_t s) {

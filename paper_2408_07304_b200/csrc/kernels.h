@@ -116,6 +116,7 @@ struct EncodeArgs {
   const int *perm;
   const double2 *fft_tw, *twist;
   const double2 *fft_tw_h;  // W_{M/2}^e, e < M/4 (real-slot path)
+  const double2 *fft_tw_hp; // the same table padded for shared memory (fft_twpad), TMA-staged by the encodes
   const double2 *post_tw;   // real-slot split step: [A | B | A5 | B5] (encode_real_post)
   const double2 *twist_split;  // complex-slot twist zeta^-j = A'[j >> 6] B[j & 63], j < M: [A' | B]
   int wide;                 // m_out holds 128-bit coefficients (int64 pairs)
