@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
           });
     }
   }
-  cb.settle();  // the peers finished reading this CTA's share
+  cb.settle_exit();  // the peers finished reading this CTA's share
 }
 
 // ============================================================ vanilla, NTT form
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
           });
     }
   }
-  cb.settle();  // the peers finished reading this CTA's share
+  cb.settle_exit();  // the peers finished reading this CTA's share
 }
 
 // ============================================================ vanilla, COEFF form
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_coeff_split_kern
           __stcs(ct1 + x, add_mod(csub(v, q), err_term<INTS>(se2[inv_sample_idx<LOGN>(x, r)], c), q));
         });
   }
-  cb.settle();  // the peers finished reading this CTA's share
+  cb.settle_exit();  // the peers finished reading this CTA's share
 }
 
 // ============================================================ decrypt (Eq. 10)
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) decrypt_split_kernel(Dec
                                      with_pre1(epilogue, pre));
     }
   }
-  cb.settle();
+  cb.settle_exit();
   bad = __syncthreads_or(bad);
   // the cluster's verdict: every CTA publishes its flag, rank 0 reads them over DSMEM
   if (threadIdx.x == 0) bad_flag = bad;
