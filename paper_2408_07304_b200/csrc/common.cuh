@@ -170,17 +170,27 @@ __host__ __device__ constexpr int fft_twpad_size(int n) { return fft_twpad(n - 1
 
 // Index of coefficient x in a plaintext de-interleaved by 2^d (EncodeArgs::deint_log), d = 0: x.
 ZINC_DEV int deint_idx(int x, int d, int log_n) { return ((x & ((1 << d) - 1)) << (log_n - d)) + (x >> d); }
+// The words x = 2^log_s i + r (i = 0, 1, ...) of a plaintext stored in natural order (d = 0) or
+// de-interleaved by 2^d = 2^log_s (deint_idx): word i of the subsequence sits at p[i stride].
+struct MSub {
+  const int64_t *p;
+  int stride;
+};
+ZINC_DEV MSub m_sub(const int64_t *m, int r, int log_s, int d, int log_n) {
+  if (!m) return MSub{nullptr, 1};
+  return d ? MSub{m + ((size_t)r << (log_n - d)), 1} : MSub{m + r, 1 << log_s};
+}
 // Residue of the scheme's error term: e (CKKS, BFV) or t e (BGV).
 // The plaintext-plus-error input of the first forward transform as a two-phase load
 // (ntt.cuh TwoPhase): fetch(x) reads m[x] from global memory, lift(raw, x) adds the sample
 // (stored at x >> SHIFT: 1 for parity-split sample buffers) and reduces.
 template <bool INTS, int SHIFT = 0>
 struct PtLoad {
-  const int64_t *m;
+  const int64_t *m;  // the CTA's subsequence (m_sub): word x sits at m[(x >> SHIFT) ms]
   const int8_t *se1;
   const LimbConst &c;
-  int d = 0, log_n = 0;  // m de-interleaved by 2^d (deint_idx)
-  ZINC_DEV int64_t fetch(int x) const { return m ? ldm(m + deint_idx(x, d, log_n)) : 0; }
+  int ms = 1;
+  ZINC_DEV int64_t fetch(int x) const { return m ? ldm(m + (x >> SHIFT) * ms) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const { return pt_plus_e<INTS>(raw, se1[x >> SHIFT], c); }
   ZINC_DEV uint64_t operator()(int x) const { return lift(fetch(x), x); }
 };
@@ -199,8 +209,8 @@ struct ZincTLoad {
   const int8_t *se;
   const LimbConst &c;
   int t;
-  int d = 0, log_n = 0;  // m de-interleaved by 2^d (deint_idx)
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + deint_idx(x, d, log_n)) : 0; }
+  int ms = 1;  // m is the CTA's subsequence (m_sub): word x sits at m[(x >> SHIFT) ms]
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + (x >> SHIFT) * ms) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     return t == 0 ? pt_plus_e<INTS>(raw, se[x >> SHIFT], c) : err_term<INTS>(se[x >> SHIFT], c);
   }

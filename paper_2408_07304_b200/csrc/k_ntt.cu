@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(ZincNttGeo<LOGN>::THREADS, ZincNttGeo<LOGN>::M
       for (int t = 0; t < 2; ++t) {
         const uint64_t *z = t ? z2 : z1;
         uint64_t *ctt = t ? ct1 : ct0;
-        ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, ZincTLoad<INTS>{m, t ? se2 : se1, c, t},
+        ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, ZincTLoad<INTS>{m ? m + r : nullptr, t ? se2 : se1, c, t, 2},  // x = 2 i + r
             [&](int x, uint64_t v0, uint64_t v1) {
               const ulonglong2 zz = ld2_nc(z + x);
               st2_cs(ctt + x, reduce_fold(zz.x + v0, c), reduce_fold(zz.y + v1, c));

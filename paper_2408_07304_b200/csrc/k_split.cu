@@ -63,12 +63,6 @@ ZINC_DEV int inv_sample_idx(int x, int r) {
 // CKKS plaintext words of this CTA's subsequence (x = S i + r) all below q_min / 2 in absolute
 // value (q_min over the CTA's limbs): then every lift of m + e is branch-free (lift_small), for
 // every limb, decided once per message instead of per word, limb and transform.
-template <int LOGN, int THREADS>
-ZINC_DEV bool plaintext_small(const int64_t *m, int r, const LimbConst *limbs, int lo, int hi, int d = 0) {
-  using G = SplitGeo<LOGN>;
-  return plaintext_small_sub<THREADS>(m, G::LOGS, r, G::NL, d, LOGN, limbs, lo, hi);
-}
-
 template <int LOGN> struct SplitSmem {
   using G = SplitGeo<LOGN>;
   static constexpr size_t DATA = SmemWords<G::LL>::value * sizeof(uint64_t);  // 34816
@@ -129,8 +123,8 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
   __syncthreads();
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
-  const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi, a.m_deint);
+  const MSub m = m_sub(a.m ? a.m + b * N : nullptr, r, G::LOGS, a.m_deint, LOGN);  // x = S i + r
+  const bool all_small = !INTS && t_lo == 0 && plaintext_small_sub<THREADS>(m, NL, a.limbs, lo, hi);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -141,7 +135,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
     for (int t = t_lo; t < t_hi; ++t) {
       const uint64_t *z = a.cache + (size_t)(t * L + i) * N;
       uint64_t *ctt = ct0 + (size_t)t * L * N;
-      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoadU<INTS, G::LOGS>{{m, t ? se2 : se1, c, t, a.m_deint, LOGN}, all_small},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, ZincTLoadU<INTS, G::LOGS>{{m.p, t ? se2 : se1, c, t, m.stride}, all_small},
           ZincNttOut<S>{z, ctt, c}, stw, [&]() {
             if (SPLIT_STW && t == t_hi - 1 && i + 1 < hi) tws.issue_n(stw, tw + N, G::STW);  // lands during pass C + exchange
           });
@@ -184,8 +178,8 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
   __syncthreads();
   pdl_trigger();
   pdl_wait();
-  const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const bool all_small = !INTS && t_lo == 0 && plaintext_small<LOGN, THREADS>(m, r, a.limbs, lo, hi, a.m_deint);
+  const MSub m = m_sub(a.m ? a.m + b * N : nullptr, r, G::LOGS, a.m_deint, LOGN);  // x = S i + r
+  const bool all_small = !INTS && t_lo == 0 && plaintext_small_sub<THREADS>(m, NL, a.limbs, lo, hi);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -198,7 +192,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
     if constexpr (SPLIT_STW) tws.wait();
 #pragma unroll 1
     for (int t = t_lo; t < t_hi; ++t) {
-      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m, se1, se2, su, c, t, a.m_deint, LOGN, all_small || t > 0},
+      ntt_forward_split<LOGN, NR>(sm, cb, tw, q, VanTLoad<INTS, G::LOGS>{m.p, se1, se2, su, c, t, m.stride, all_small || t > 0},
           [&](int x0, uint64_t (&v)[S]) {
             if (t < 2 || gridDim.z > 1) {
               uint64_t *dst = (t == 0 ? ct0 : t == 1 ? ct1 : a.u_hat + (b * L + i) * N) + x0;

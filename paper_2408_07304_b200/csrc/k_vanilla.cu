@@ -158,8 +158,8 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
   __syncthreads();
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
-  const int64_t *m = a.m ? a.m + b * N : nullptr;
-  const bool all_small = !INTS && plaintext_small_sub<THREADS>(m, 1, r, G::NL, a.m_deint, LOGN, a.limbs, lo, hi);
+  const MSub m = m_sub(a.m ? a.m + b * N : nullptr, r, 1, a.m_deint, LOGN);  // x = 2 i + r
+  const bool all_small = !INTS && plaintext_small_sub<THREADS>(m, G::NL, a.limbs, lo, hi);
   for (int i = lo; i < hi; ++i) {
     const LimbConst c = a.limbs[i];
     const uint64_t q = c.q;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
     // the instruction footprint); the sample of coefficient x = 2 i' + r sits at i' = x >> 1
 #pragma unroll 1
     for (int t = 0; t < 3; ++t) {
-      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, VanTLoad<INTS, 1>{m, se1, se2, su, c, t, a.m_deint, LOGN, all_small || t > 0},
+      ntt_forward_dit2<LOGN, true, NR>(sm, tw, q, VanTLoad<INTS, 1>{m.p, se1, se2, su, c, t, m.stride, all_small || t > 0},
           [&](int x, uint64_t v0, uint64_t v1) {
             if (t < 2) {
               st2((t == 0 ? ct0 : ct1) + x, canon(v0), canon(v1));

@@ -134,17 +134,16 @@ ZINC_DEV ulonglong2 ld2_nc(const void *p) {
 // CKKS plaintext words of a CTA's subsequence x = 2^log_s i + r (i < nl) all below q_min / 2 in
 // absolute value (q_min over the CTA's limbs): then every lift of m + e is branch-free
 // (lift_small) for every limb, decided once per message instead of per word, limb and transform.
-// d: m de-interleaved by 2^d (deint_idx).
+// ms: the CTA's subsequence of m (m_sub).
 template <int THREADS>
-ZINC_DEV bool plaintext_small_sub(const int64_t *m, int log_s, int r, int nl, int d, int log_n, const LimbConst *limbs,
-                                  int lo, int hi) {
-  if (!m) return true;
+ZINC_DEV bool plaintext_small_sub(MSub ms, int nl, const LimbConst *limbs, int lo, int hi) {
+  if (!ms.p) return true;
   uint64_t qmin = ~0ull;
   for (int i = lo; i < hi; ++i) qmin = min(qmin, limbs[i].q);
   const uint64_t half = qmin >> 1;
   int big = 0;
 #pragma unroll 4
-  for (int i = threadIdx.x; i < nl; i += THREADS) big |= (uint64_t)ldm(m + deint_idx((i << log_s) + r, d, log_n)) + half >= qmin;
+  for (int i = threadIdx.x; i < nl; i += THREADS) big |= (uint64_t)ldm(ms.p + i * ms.stride) + half >= qmin;
   return !__syncthreads_or(big);
 }
 
@@ -157,8 +156,8 @@ struct VanTLoad {
   const uint8_t *su;
   const LimbConst &c;
   int t;
-  int d, log_n;  // m de-interleaved by 2^d (deint_idx)
-  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + deint_idx(x, d, log_n)) : 0; }
+  int ms;  // m is the CTA's subsequence (m_sub): word x sits at m[(x >> SHIFT) ms]
+  ZINC_DEV int64_t fetch(int x) const { return (t == 0 && m) ? ldm(m + (x >> SHIFT) * ms) : 0; }
   ZINC_DEV uint64_t lift(int64_t raw, int x) const {
     const int i = x >> SHIFT;
     return t == 0 ? pt_plus_e<INTS>(raw, se1[i], c) : t == 1 ? err_term<INTS>(se2[i], c)
