@@ -14,13 +14,28 @@ namespace zinc {
 #endif
 
 // ============================================================ samplers (C-4) on a share
-// CBD samples of the coefficients x = S i + r (the forward split's subsequence), at i.
+// CBD samples of the coefficients x = S i + r (the forward split's subsequence), stored at i,
+// drawn by the CTA pair (r, r ^ 1) together: x = S i + r and S i + (r ^ 1) are the two halves of
+// one Philox block ((S/2) i + (r >> 1)); drawing them per CTA computed every block twice.
+// Each CTA draws the blocks of half the indices i and hands the partner's halves over
+// distributed shared memory, four samples per 32-bit store.  A cluster barrier must follow
+// before either CTA reads its buffer (and one must precede: the partner is running).
 template <int THREADS>
-ZINC_DEV void sample_cbd_sub(int8_t *dst, int nl, int S, int r, uint64_t seed, uint64_t msg, uint32_t tag) {
-  for (int i = threadIdx.x; i < nl; i += THREADS) {
-    const int x = S * i + r;
-    const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)(x >> 1));
-    dst[i] = (int8_t)((x & 1) ? cbd_hi(w) : cbd_lo(w));
+ZINC_DEV void sample_cbd_pair(int8_t *dst, int nl, int S, int r, uint64_t seed, uint64_t msg, uint32_t tag) {
+  const int h = r & 1, half = nl / 2;
+  const uint32_t peer = dsmem_addr(dst, (uint32_t)(r ^ 1));
+  for (int i4 = threadIdx.x; i4 < half / 4; i4 += THREADS) {
+    const int i0 = h * half + 4 * i4;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)((S / 2) * (i0 + j) + (r >> 1)));
+      lo |= ((uint32_t)cbd_lo(w) & 0xFFu) << (8 * j);
+      hi |= ((uint32_t)cbd_hi(w) & 0xFFu) << (8 * j);
+    }
+    // the even rank of the pair owns the even coefficients (the block's low half)
+    *reinterpret_cast<uint32_t *>(dst + i0) = h ? hi : lo;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer + (uint32_t)i0), "r"(h ? lo : hi) : "memory");
   }
 }
 // Ternary samples of x = S i + r (S >= 4: word r & 3 of block x >> 2), packed 2 bits at i.
@@ -118,9 +133,9 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) zinc_ntt_split_kernel(Zi
   if constexpr (SPLIT_STW) tws.issue_n(stw, a.tw + (size_t)lo * N, G::STW);
   // small batches spread the two transforms over gridDim.z = 2 (t = blockIdx.z)
   const int t_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, t_hi = gridDim.z > 1 ? t_lo + 1 : 2;
-  if (t_lo == 0) sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
-  if (t_hi == 2) sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ZINC_E2);
-  __syncthreads();
+  if (t_lo == 0) sample_cbd_pair<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ZINC_E1);
+  if (t_hi == 2) sample_cbd_pair<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ZINC_E2);
+  cluster_sync_all();  // the partner's halves have landed (once per message)
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
   const MSub m = m_sub(a.m ? a.m + b * N : nullptr, r, G::LOGS, a.m_deint, LOGN);  // x = S i + r
@@ -173,9 +188,9 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) vanilla_ntt_split_kernel
   // transform then writes u^ to a.u_hat and vanilla_combine_kernel forms pk u^)
   const int t_lo = gridDim.z > 1 ? (int)blockIdx.z : 0, t_hi = gridDim.z > 1 ? t_lo + 1 : 3;
   if (t_hi == 3) sample_ternary_sub<THREADS>(su, NL, S, r, a.seed, msg, TAG_ENC_U);
-  if (t_lo == 0) sample_cbd_sub<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
-  if (t_lo <= 1 && t_hi >= 2) sample_cbd_sub<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
-  __syncthreads();
+  if (t_lo == 0) sample_cbd_pair<THREADS>(se1, NL, S, r, a.seed, msg, TAG_ENC_E1);
+  if (t_lo <= 1 && t_hi >= 2) sample_cbd_pair<THREADS>(se2, NL, S, r, a.seed, msg, TAG_ENC_E2);
+  cluster_sync_all();  // the partner's halves have landed (once per message)
   pdl_trigger();
   pdl_wait();
   const MSub m = m_sub(a.m ? a.m + b * N : nullptr, r, G::LOGS, a.m_deint, LOGN);  // x = S i + r
