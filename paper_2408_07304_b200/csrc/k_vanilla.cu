@@ -150,12 +150,12 @@ __global__ void __launch_bounds__(VanillaDitGeo<LOGN>::THREADS, VanillaDitGeo<LO
   const int lo = blockIdx.y * a.limbs_per_cta;
   const int hi = min(L, lo + a.limbs_per_cta);
   tws.init();
-  __syncthreads();
+  cluster_sync_all();  // both CTAs run: the samplers below store into the partner's buffers
   tws.issue(stw, a.tw + (size_t)lo * N);
-  sample_ternary_parity<THREADS>(su, N, a.seed, msg, TAG_ENC_U, r);
-  sample_cbd_parity<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1, r);
-  sample_cbd_parity<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2, r);
-  __syncthreads();
+  sample_ternary_parity_pair<THREADS>(su, N, a.seed, msg, TAG_ENC_U, r);
+  sample_cbd_parity_pair<THREADS>(se1, N, a.seed, msg, TAG_ENC_E1, r);
+  sample_cbd_parity_pair<THREADS>(se2, N, a.seed, msg, TAG_ENC_E2, r);
+  cluster_sync_all();  // the partner's halves have landed (once per message)
   pdl_trigger();  // chained after the encode that wrote m: wait before reading it
   pdl_wait();
   const MSub m = m_sub(a.m ? a.m + b * N : nullptr, r, 1, a.m_deint, LOGN);  // x = 2 i + r

@@ -59,6 +59,48 @@ ZINC_DEV void sample_ternary_parity(uint8_t *dst, int n, uint64_t seed, uint64_t
     dst[blk2] = (uint8_t)packed;
   }
 }
+// The parity samplers for the CTA pair together: both parities are the halves of the same Philox
+// blocks, so each CTA draws half of the blocks and hands the partner's samples over distributed
+// shared memory (32-bit stores of four CBD samples / sixteen packed ternary samples).  A cluster
+// barrier must precede (the partner is running) and follow (its stores have landed).
+template <int THREADS>
+ZINC_DEV void sample_cbd_parity_pair(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag, int r) {
+  const uint32_t peer = dsmem_addr(dst, (uint32_t)(r ^ 1));
+  const int quarter = n / 4;  // blocks per CTA
+  for (int b4 = threadIdx.x; b4 < quarter / 4; b4 += THREADS) {
+    const int b0 = r * quarter + 4 * b4;
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)(b0 + j));  // coefficients 2 blk, 2 blk + 1
+      lo |= ((uint32_t)cbd_lo(w) & 0xFFu) << (8 * j);
+      hi |= ((uint32_t)cbd_hi(w) & 0xFFu) << (8 * j);
+    }
+    *reinterpret_cast<uint32_t *>(dst + b0) = r ? hi : lo;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer + (uint32_t)b0), "r"(r ? lo : hi) : "memory");
+  }
+}
+template <int THREADS>
+ZINC_DEV void sample_ternary_parity_pair(uint8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag, int r) {
+  // block b: coefficients 4b..4b+3; parity p keeps 4b + p (local 2b) and 4b + 2 + p (local 2b + 1);
+  // byte blk2 of a parity's buffer packs blocks 2 blk2, 2 blk2 + 1
+  const uint32_t peer = dsmem_addr(dst, (uint32_t)(r ^ 1));
+  const int per_cta = n / 16;  // bytes per CTA
+  for (int w4 = threadIdx.x; w4 < per_cta / 4; w4 += THREADS) {
+    const int byte0 = r * per_cta + 4 * w4;
+    uint32_t even = 0, odd = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 w = stream_block(seed, msg, tag, 0, (uint32_t)(2 * (byte0 + j) + h));
+        even |= ((uint32_t)(tern(w.x) + 1) | ((uint32_t)(tern(w.z) + 1) << 2)) << (8 * j + 4 * h);
+        odd |= ((uint32_t)(tern(w.y) + 1) | ((uint32_t)(tern(w.w) + 1) << 2)) << (8 * j + 4 * h);
+      }
+    *reinterpret_cast<uint32_t *>(dst + byte0) = r ? odd : even;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer + (uint32_t)byte0), "r"(r ? even : odd) : "memory");
+  }
+}
 template <int THREADS>
 ZINC_DEV void sample_cbd_smem(int8_t *dst, int n, uint64_t seed, uint64_t msg, uint32_t tag) {
   for (int blk = threadIdx.x; blk < n / 2; blk += THREADS) {
