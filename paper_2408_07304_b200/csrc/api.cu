@@ -557,7 +557,6 @@ static zinc_status encode_into(const zinc_ctx *c, int kind, const void *slots, s
   a.wait_mode = wait_mode;
   // few messages: a latency variant with more threads per message (knob ZINC_TUNE_SMALL_ENCODE)
   a.fast = batch < (size_t)c->num_sms ? (int)g_tune[ZINC_TUNE_SMALL_ENCODE].load() : 0;
-  if (ZINC_ENC15_THREADS == 512 && c->log_n == 15 && !a.fast) a.fast = 1;  // the 512-thread real-slot encode
   if (small_cluster(c, kind, batch) && !wide)
     LAUNCH(ZINC_K_ENCODE, s, launch_encode_cluster(c->log_n, a, batch, s));
   else

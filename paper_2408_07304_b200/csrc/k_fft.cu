@@ -9,23 +9,13 @@ namespace zinc {
 // bit-reversed position lies in half r, runs the first LOGM-1 DIT stages on
 // its M/2 points, and the last stage (pairs x, x + M/2 with W_M^x) reads both
 // halves over distributed shared memory; CTA r finishes x in [r M/4, (r+1) M/4).
-// Threads per CTA of the split (N = 2^15) complex encode: 256 runs the three-pass plan (radix 16 /
-// 16 / 32, 224 registers), 512 four passes of radix 8 / 8 / 8 / 16 at half the registers: twice
-// the warps on the SM's one resident CTA.
-template <int LL, int TH> struct EncPlan {
-  static constexpr int THREADS = TH, K1 = FftPlan<LL>::K1, K2 = FftPlan<LL>::K2, K3 = FftPlan<LL>::K3;
-};
-template <int LOGM> struct EncThreads {
-  static constexpr int value = LOGM > 13 ? ZINC_ENC15_THREADS : FftPlan<LOGM>::THREADS;
-};
 template <int LOGM>
-__global__ void __launch_bounds__(EncThreads<LOGM>::value) encode_kernel(EncodeArgs a) {
+__global__ void __launch_bounds__(FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS) encode_kernel(EncodeArgs a) {
   constexpr bool SPLIT = LOGM > 13;
   constexpr int LL = SPLIT ? LOGM - 1 : LOGM;
   constexpr int M = 1 << LOGM, ML = 1 << LL;
   constexpr int TWS = SPLIT ? 2 : 1;
-  constexpr int TH = EncThreads<LOGM>::value;
-  using P = EncPlan<LL, TH>;
+  using P = FftPlan<LL>;
   extern __shared__ __align__(16) double2 buf[];
   const size_t b = blockIdx.x / (SPLIT ? 2 : 1);
   const int r = SPLIT ? (int)cluster_rank() : 0;
@@ -70,13 +60,7 @@ __global__ void __launch_bounds__(EncThreads<LOGM>::value) encode_kernel(EncodeA
   if constexpr (SPLIT) mbar_wait(&tw_mbar, 0);
   auto lds = [&](int i) { return buf[pad16(i)]; };
   auto sts = [&](int i, double2 v) { buf[pad16(i)] = v; };
-  if constexpr (SPLIT && TH == 512) {
-    fft_pass<LL, 0, 3, TH, true, false, 1, 2>(stw, lds, sts);
-    __syncthreads();
-    fft_pass<LL, 3, 3, TH, true, false, 1, 2>(stw, lds, sts);
-    __syncthreads();
-    fft_pass<LL, 6, 3, TH, true, false, 1, 2>(stw, lds, sts);
-  } else if constexpr (SPLIT) {
+  if constexpr (SPLIT) {
     fft_pass<LL, 0, P::K1, P::THREADS, true, false, 1, 2>(stw, lds, sts);
     __syncthreads();
     fft_pass<LL, P::K1, P::K2, P::THREADS, true, false, 1, 2>(stw, lds, sts);
@@ -107,8 +91,7 @@ __global__ void __launch_bounds__(EncThreads<LOGM>::value) encode_kernel(EncodeA
   if constexpr (!SPLIT) {
     fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false>(a.fft_tw, lds, emit);
   } else {
-    if constexpr (TH == 512) fft_pass<LL, 9, LL - 9, TH, true, false, 1, 2>(stw, lds, sts);
-    else fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, 1, 2>(stw, lds, sts);
+    fft_pass<LL, P::K1 + P::K2, P::K3, P::THREADS, true, false, 1, 2>(stw, lds, sts);
     cluster_sync_all();
     const double2 *h0 = peer_smem(buf, 0), *h1 = peer_smem(buf, 1);
     // U independent iterations: their DSMEM, twiddle and twist loads are all in flight
@@ -247,7 +230,8 @@ static cudaError_t launch_encode_t(const EncodeArgs &a, size_t batch, cudaStream
     return launch_ex(encode_real_kernel<LOGM, false>, dim3((unsigned)batch), 256, encode_real_smem<LOGM>(), 1, s, a);
   }
   constexpr int C = LOGM > 13 ? 2 : 1;
-  return launch_ex(encode_kernel<LOGM>, dim3((unsigned)(batch * C)), EncThreads<LOGM>::value, encode_smem<LOGM>(), C, s, a);
+  return launch_ex(encode_kernel<LOGM>, dim3((unsigned)(batch * C)), FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
+                   encode_smem<LOGM>(), C, s, a);
 }
 // Messages one full wave of the (throughput) encode kernel covers: resident CTAs per SM (the
 // occupancy calculator, with the kernel's dynamic shared memory) x SMs / CTAs per message.
@@ -263,7 +247,8 @@ static size_t encode_wave_msgs_t(bool complex_slots, int num_sms) {
   }
   constexpr int C = LOGM > 13 ? 2 : 1;
   if (set_smem(encode_kernel<LOGM>, encode_smem<LOGM>()) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_kernel<LOGM>, EncThreads<LOGM>::value,
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, encode_kernel<LOGM>,
+                                                    FftPlan<(LOGM > 13 ? LOGM - 1 : LOGM)>::THREADS,
                                                     encode_smem<LOGM>()) != cudaSuccess)
     return 0;
   return (size_t)per_sm * num_sms / C;

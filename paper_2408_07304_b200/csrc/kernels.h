@@ -110,11 +110,6 @@ struct BfvScaleArgs {
   size_t batch;
   int n, L;
 };
-// Threads per CTA of the N = 2^15 encodes (one 204-220 KiB CTA per SM either way): 256 (radix-16 /
-// 32 passes, 214-224 registers) or 512 (radix-8 passes at half the registers).
-#ifndef ZINC_ENC15_THREADS
-#define ZINC_ENC15_THREADS 256
-#endif
 struct EncodeArgs {
   const double *slots;
   int complex_slots;
