@@ -588,6 +588,12 @@ static ZincCoeffArgs zinc_coeff_args(const zinc_ctx *c, const uint64_t *cache, c
   a.n = c->n;
   a.L = c->L;
   a.qmin = c->qmin;
+  {
+    const uint64_t qmax = *std::max_element(c->q.begin(), c->q.end());
+    int bits = 0;
+    while (bits < 64 && (qmax >> bits)) ++bits;
+    a.wide_hb = std::max(0, std::min(31, 63 - bits));
+  }
   a.m_stride = (size_t)c->n;
   // messages per CTA (tuning knob): grid = coefficient tiles x message groups
   // 0 (default): 8 messages per CTA when the cache tile is small (L <= 4: amortises the tile

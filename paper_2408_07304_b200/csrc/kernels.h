@@ -42,6 +42,7 @@ struct ZincCoeffArgs {
   const int64_t *m128;    // CKKS 128-bit plaintexts (int64 pairs [batch][N][2]); overrides m
   const char *prefetch;   // the next chunk's slots: warmed into L2 while this chunk streams
   size_t prefetch_bytes;  // (16-byte multiple; 0: none)
+  int wide_hb;            // 128-bit plaintexts: 63 - bits(q_max), the "tiny high word" bound (zinc_coeff.cuh)
   size_t m_stride;        // int64 words between messages' plaintexts in m (N, or 2 L N when the
                           // plaintexts sit in the ciphertexts' last c2 limb, see encrypt_any)
 };

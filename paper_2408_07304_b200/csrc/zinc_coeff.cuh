@@ -117,7 +117,36 @@ ZINC_DEV void zinc_coeff_body(const ZincCoeffArgs &a, int tile_x, int group_y, u
       const int64_t h0 = (int64_t)p0.y, h1 = (int64_t)p1.y;
       const bool hsmall = (uint64_t)(h0 < 0 ? -h0 : h0) < qmin && (uint64_t)(h1 < 0 ? -h1 : h1) < qmin;
       uint64_t *out = a.ct + b * 2 * lnn + j;
-      if (fold1 && __all_sync(0xffffffffu, hsmall)) {
+      // Tiny high words (the paper's value ranges put |m| a few bits past 2^64): V = hi 2^64 + lo +
+      // e1' is formed once per coefficient as a signed 128-bit value (hh, ll); with |hh| < 2^hb,
+      // hb = 63 - bits(q_max), the term hh 2^64 = hh r64 (mod q) is one 32 x 64-bit product below
+      // 2^hb q < 2^63 (2^hb q minus it when hh < 0): no Shoup product, no per-limb residue of e1'.
+      // The sum with fold(ll) and the cache word stays below 2^64 and one fold finishes.
+      const int hb = a.wide_hb;
+      const uint64_t ee0 = (uint64_t)(int64_t)e0, ee1 = (uint64_t)(int64_t)e1;
+      const uint64_t ll0 = p0.x + ee0, ll1 = p1.x + ee1;
+      const int64_t hh0 = h0 + (e0 < 0 ? -1 : 0) + (ll0 < p0.x ? 1 : 0), hh1 = h1 + (e1 < 0 ? -1 : 0) + (ll1 < p1.x ? 1 : 0);
+      const uint64_t ah0 = (uint64_t)(hh0 < 0 ? -hh0 : hh0), ah1 = (uint64_t)(hh1 < 0 ? -hh1 : hh1);
+      const bool tiny = hb > 0 && ((ah0 | ah1) >> hb) == 0;
+      if (fold1 && __all_sync(0xffffffffu, tiny)) {
+        const uint32_t a0 = (uint32_t)ah0, a1 = (uint32_t)ah1;
+#pragma unroll 2
+        for (int i = 0; i < L; ++i) {
+          const uint64_t q = sq[i], r64 = sr64[i], fm = sfmask[i], fcb = sfcb[i];
+          const uint32_t fc = (uint32_t)fcb, fb = (uint32_t)(fcb >> 32) & 0xff;
+          uint64_t z10, z11, z20, z21;
+          ld2(tile + (size_t)i * T + jl, z10, z11);
+          ld2(tile + (size_t)(L + i) * T + jl, z20, z21);
+          auto fold = [&](uint64_t x) { return fold_once(x, fb - 32, (uint32_t)(fm >> 32), fc); };
+          const uint64_t qk = q << hb;
+          const uint64_t t0 = (uint64_t)a0 * r64, t1 = (uint64_t)a1 * r64;  // below 2^hb q
+          // term below 2^63, fold(ll) below 2q, the cache word below q
+          const uint64_t s0 = (hh0 < 0 ? qk - t0 : t0) + fold(ll0) + z10;
+          const uint64_t s1 = (hh1 < 0 ? qk - t1 : t1) + fold(ll1) + z11;
+          st2_cs(out + (size_t)i * a.n, csub(fold(s0), q), csub(fold(s1), q));
+          st2_cs(out + lnn + (size_t)i * a.n, mod_add_signed(z20, f0, q), mod_add_signed(z21, f1, q));
+        }
+      } else if (fold1 && __all_sync(0xffffffffu, hsmall)) {
 #pragma unroll 2
         for (int i = 0; i < L; ++i) {
           const uint64_t q = sq[i], r64 = sr64[i], r64s = sr64sh[i], fm = sfmask[i], fcb = sfcb[i];
