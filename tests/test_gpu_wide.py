@@ -96,3 +96,36 @@ def test_paper_value_ranges_from_slots(Z, orc, S, shape):
         _, st, zz = Z.ckks_decrypt_batch(ctx, sk, form, a)
         assert (st.cpu().numpy() == 0).all()
         assert np.max(np.abs(zz.cpu().numpy() - z)) < 1e-4
+
+
+def test_i128_tiny_high_word_edges_bit_exact(Z, orc, S):
+    """The add/inject kernel's "tiny high word" path (|hi| < 2^7 at 56-bit primes, decided per warp
+    after e1' is added with its carry into hi): plaintexts at its boundaries -- hi in {0, +-1, +-126,
+    +-127, +-128, 129}, lo in {0, 1, 20, 2^63, 2^64 - 21, 2^64 - 1} (so that e1' carries or borrows
+    across 2^64), one message all tiny, one with a non-tiny coefficient in every warp, one mixing
+    warps -- bit-exact against Enc(0) + residues of the integers (Eq. 4)."""
+    ctx, P, sk, pk, o_sk_ntt, o_pk, caches = S
+    his = [0, 1, -1, 126, -126, 127, -127, 2, -2, 64]
+    his_edge = [128, -128, 129, -129, 127, -127, 0, 1000, -(1 << 40)]
+    los = [0, 1, 20, 1 << 63, (1 << 64) - 21, (1 << 64) - 1, 12345678901234567, (1 << 64) - 5]
+    rng = np.random.default_rng(77)
+
+    def msg(kind):
+        out = []
+        for j in range(P.n):
+            hi = his[rng.integers(len(his))]
+            if kind == 1 and j % 64 == 17:
+                hi = his_edge[rng.integers(len(his_edge))]
+            if kind == 2 and (j // 64) % 3 == 0:
+                hi = his_edge[rng.integers(len(his_edge))]
+            out.append(hi * (1 << 64) + los[rng.integers(len(los))])
+        return out
+
+    ints = [msg(k) for k in (0, 1, 2)]
+    m = torch.from_numpy(np.stack([orc.int_to_i128(v) for v in ints])).cuda()
+    ct = Z.zinc_encrypt_batch(ctx, caches[COEFF], COEFF, m, 13, 900).cpu().numpy()
+    o_cache = orc.precompute_cache(P, o_pk, 202, COEFF)
+    zero = np.zeros(P.n, dtype=np.int64)
+    for b in range(3):
+        base = orc.zinc_encrypt(P, o_cache, COEFF, zero, 13, 900 + b)
+        assert np.array_equal(ct[b], add_residues(orc, P, base, ints[b], COEFF)), b
