@@ -153,8 +153,11 @@ ZINC_DEV uint64_t pt_plus_e(int64_t m, int e, const LimbConst &c) {
 #endif
 ZINC_DEV int64_t ldm(const int64_t *p) {
 #if ZINC_M_NOALLOC
+  // volatile: callers guard this load with a null check (m = 0 encryptions), and a plain asm is a
+  // pure function the compiler may hoist above its guard (seen once: a fault in an experimental
+  // build of the N = 2^15 vanilla kernel, profiles/r02d_experiments.txt)
   int64_t v;
-  asm("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 #else
   return __ldg(p);
