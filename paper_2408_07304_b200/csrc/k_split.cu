@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) decrypt_split_kernel(Dec
     };
     // x0 is re-read only by the thread that wrote it (the same output positions every limb)
     auto pre = [&](int x) {
-      return make_ulonglong2(FORM == 1 ? __ldg(c1 + x) : 0, i > 0 ? (uint64_t)x0[x] : 0);
+      return make_ulonglong2(FORM == 1 ? (uint64_t)ldm(reinterpret_cast<const int64_t *>(c1) + x) : 0, i > 0 ? (uint64_t)x0[x] : 0);
     };
     if (FORM == 0) {
       ntt_inverse_split<LOGN, true>(sm, cb, itw, c,
@@ -403,7 +403,8 @@ __global__ void __launch_bounds__(256, ZINC_SPLIT_MINB) decrypt_split_kernel(Dec
     } else {
       const Tw *tw = a.tw + (size_t)i * N;
       // the forward split reads its early-pass twiddles from global memory here (stw = tw)
-      ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q, [&](int x) { return __ldg(c2 + x); },
+      ntt_forward_split<LOGN, NR, true>(sm, cb, tw, q,
+          [&](int x) { return (uint64_t)ldm(reinterpret_cast<const int64_t *>(c2) + x); },  // stride S, read once: no L1 allocation
           [&](int x0g, uint64_t (&v)[S]) {
 #pragma unroll
             for (int u = 0; u < S; u += 4) {
